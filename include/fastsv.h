@@ -1,0 +1,136 @@
+/*
+ * fastsv.h — C ABI of the B200-native FastSV connected-components solver.
+ *
+ * This is the drop-in boundary for the reference's hot path, the all-flags
+ * FastSV loop `svcc.fastsv_la(g, cfg, record_snapshots)`
+ * (/root/reference/pkg/src/svcc/driver.py:64-120) and its vertex-level twin
+ * `svcc.fastsv(g)` (algorithms.py:152-167). The reference is pure Python, so
+ * its "FFI" is the Python call itself; the ctypes binding a maintainer adds is
+ * paper_1910_05971_b200/_native.py (shown in INTEGRATION.md). Plain pointers
+ * and sizes only; no torch types.
+ *
+ * Semantics are bit-exact with the reference: the same per-iteration parent
+ * vectors (snapshots), the same iteration count, the same gf_changed and
+ * f_changed trace fields (algorithms.py:38-45) and labels equal to the
+ * minimum vertex id of each component (graph.py:100-125).
+ *
+ * Status codes mirror the reference error taxonomy (errors.py:4-19):
+ *   FSV_OK 0, FSV_ERR_INPUT 1 (InputError), FSV_ERR_CONTRACT 2 (ValueError),
+ *   FSV_ERR_INVARIANT 3 (InvariantError), FSV_ERR_RUNTIME 4 (CUDA/NCCL).
+ * fsv_last_error() returns the thread-local message of the last failure.
+ *
+ * Threading: one solve per context at a time; contexts are independent.
+ */
+#ifndef FASTSV_H
+#define FASTSV_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FSV_OK 0
+#define FSV_ERR_INPUT 1
+#define FSV_ERR_CONTRACT 2
+#define FSV_ERR_INVARIANT 3
+#define FSV_ERR_RUNTIME 4
+
+#define FSV_ABI_VERSION 1
+
+typedef struct fsv_ctx fsv_ctx;
+
+/* Solver knobs. Zero-initialise for defaults. */
+typedef struct fsv_config {
+  int32_t max_iters;  /* 0 = run to convergence (the reference has no cap) */
+  int32_t batch;      /* iterations queued per host convergence check; 0 = auto */
+  int32_t profile;    /* 1 = bracket each kernel with CUDA events (fills *_ms) */
+  int32_t reserved[5];
+} fsv_config;
+
+/* Result summary of the last solve. */
+typedef struct fsv_stats {
+  int32_t iterations;       /* == reference RunResult.iterations */
+  int32_t component_count;  /* == Labeling.component_count */
+  int64_t n;
+  int64_t m_dir;            /* stored directed entries of the uploaded CSR */
+  int64_t oriented_entries; /* entries the device layout stores (one per edge) */
+  int32_t hub_slots;        /* hub table size actually used */
+  int32_t host_syncs;       /* convergence-flag reads the host made */
+  int32_t kernel_launches;  /* kernels launched by the solve */
+  float solve_ms;           /* device time, first kernel to convergence flag */
+  /* profile = 1 only: summed device time of the kernels of the iterations
+   * that ran (speculative launches past convergence excluded) */
+  float hook_ms, hubfix_ms, shortcut_ms, first_ms, allreduce_ms;
+  int32_t hook_launches;
+} fsv_stats;
+
+const char* fsv_last_error(void);
+int fsv_abi_version(void);
+int fsv_device_count(int* count);
+
+/* Context bound to one CUDA device; creates its own non-blocking stream. */
+int fsv_create(int device, fsv_ctx** out);
+int fsv_destroy(fsv_ctx* ctx);
+
+/* Hub table size used by the NEXT upload: <0 = no hubs, 0 = auto
+ * (top-degree vertices up to 49152 shared-memory slots), >0 = at most that. */
+int fsv_set_hub_slots(fsv_ctx* ctx, int slots);
+
+/* Use an external stream (e.g. torch.cuda.current_stream().cuda_stream);
+ * 0 restores the context's own stream. */
+int fsv_set_stream(fsv_ctx* ctx, void* cuda_stream);
+
+/*
+ * Upload a symmetric CSR (the reference CsrGraph layout, graph.py:20-52:
+ * rows sorted, deduplicated, self-loop free) and build the device layout.
+ *   row_offsets: n+1 entries of the FULL graph (int64, as the reference)
+ *   col_indices: the entries of rows [row_begin, row_end), i.e. the slice
+ *                [row_offsets[row_begin], row_offsets[row_end]); int32 ids
+ * Single GPU: row_begin = 0, row_end = n. With an attached NCCL communicator
+ * every rank passes its own disjoint row range (1D partition).
+ * Host buffers may be pageable or pinned. Replaces svcc.build_csr's product
+ * being handed to fastsv_la (driver.py:64).
+ */
+int fsv_upload_csr(fsv_ctx* ctx, int64_t n, const int64_t* row_offsets,
+                   const int32_t* col_indices, int64_t row_begin, int64_t row_end);
+
+/* Same with int64 column ids (the reference's ID_DTYPE, graph.py:15-17). */
+int fsv_upload_csr64(fsv_ctx* ctx, int64_t n, const int64_t* row_offsets,
+                     const int64_t* col_indices, int64_t row_begin, int64_t row_end);
+
+/* Run FastSV to convergence on the resident graph. Labels stay on device. */
+int fsv_solve(fsv_ctx* ctx, const fsv_config* cfg, fsv_stats* stats);
+
+/* Copy results of the last solve to host buffers.
+ *   labels: n int32 (or int64 via fsv_get_labels64)
+ *   trace:  cap entries each of gf_changed / f_changed (int64) and
+ *           per-iteration device milliseconds (float); any may be NULL. */
+int fsv_get_labels(fsv_ctx* ctx, int32_t* labels);
+int fsv_get_labels64(fsv_ctx* ctx, int64_t* labels);
+int fsv_get_trace(fsv_ctx* ctx, int64_t* gf_changed, int64_t* f_changed,
+                  float* elapsed_ms, int32_t cap);
+
+/* One call: solve + labels + iteration count + trace (the fastsv_la shape). */
+int fsv_run(fsv_ctx* ctx, const fsv_config* cfg, int32_t* labels,
+            int32_t* iterations, int64_t* gf_changed, int64_t* f_changed,
+            int32_t trace_cap);
+
+/* Solve while copying every committed parent vector f_k (k = 1..I) into
+ * snapshots[(k-1)*n .. k*n) (record_snapshots=True, driver.py:109-112).
+ * Fails with FSV_ERR_CONTRACT if more than snap_cap iterations run. */
+int fsv_run_snapshots(fsv_ctx* ctx, const fsv_config* cfg, int32_t* labels,
+                      int32_t* iterations, int64_t* gf_changed, int64_t* f_changed,
+                      int32_t* snapshots, int32_t snap_cap);
+
+/* ---- multi-GPU (one process per GPU, 1D edge partition) ---- */
+
+/* Fills 128 bytes with an ncclUniqueId (rank 0), to be broadcast by the host. */
+int fsv_nccl_unique_id(void* id128);
+/* Attach a communicator; per iteration the next-parent vector is merged with
+ * ncclAllReduce(ncclInt32, ncclMin) after the hooking phase. */
+int fsv_nccl_attach(fsv_ctx* ctx, const void* id128, int nranks, int rank);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,816 @@
+// C-ABI + host orchestration of the B200 FastSV solver (include/fastsv.h).
+//
+// Reference hot path: svcc.fastsv_la (/root/reference/pkg/src/svcc/driver.py:64-120)
+// and its vertex-level twin svcc.fastsv (algorithms.py:117-167). The kernels
+// live in fsv_kernels.cuh; this file owns
+//   - the upload pipeline: reference CsrGraph (graph.py:20-52) -> device
+//     oriented layout (one entry per undirected edge, head-flagged rows,
+//     hub-encoded columns, span table, closed-form f_1),
+//   - the solve loop: iteration 1 closed form, then batches of
+//     [hook, hubfix, (NCCL allreduce-min), shortcut] queued without host
+//     syncs; the host reads one 4-byte convergence flag per batch,
+//   - result marshalling into the reference's RunResult/trace shape.
+#include "../../include/fastsv.h"
+#include "fsv_kernels.cuh"
+
+#include <cub/cub.cuh>
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+using namespace fsv;
+
+// ---------------------------------------------------------------------------
+// errors
+
+static thread_local std::string g_err;
+
+static int fail(int code, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define CUDA_TRY(x)                                                                       \
+  do {                                                                                    \
+    cudaError_t e_ = (x);                                                                 \
+    if (e_ != cudaSuccess)                                                                \
+      return fail(FSV_ERR_RUNTIME, "CUDA error %s at %s:%d (%s)", cudaGetErrorString(e_), \
+                  __FILE__, __LINE__, #x);                                                \
+  } while (0)
+
+extern "C" const char* fsv_last_error(void) { return g_err.c_str(); }
+extern "C" int fsv_abi_version(void) { return FSV_ABI_VERSION; }
+
+extern "C" int fsv_device_count(int* count) {
+  int c = 0;
+  cudaError_t e = cudaGetDeviceCount(&c);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    if (count) *count = 0;
+    return fail(FSV_ERR_RUNTIME, "no CUDA device: %s", cudaGetErrorString(e));
+  }
+  if (count) *count = c;
+  return FSV_OK;
+}
+
+// ---------------------------------------------------------------------------
+// NCCL, resolved at runtime so the library loads on hosts without NCCL
+
+struct NcclApi {
+  bool loaded = false;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+static NcclApi g_nccl;
+
+static int nccl_load() {
+  if (g_nccl.loaded) return FSV_OK;
+  void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) return fail(FSV_ERR_RUNTIME, "cannot load NCCL: %s", dlerror());
+  g_nccl.GetUniqueId = (decltype(g_nccl.GetUniqueId))dlsym(h, "ncclGetUniqueId");
+  g_nccl.CommInitRank = (decltype(g_nccl.CommInitRank))dlsym(h, "ncclCommInitRank");
+  g_nccl.AllReduce = (decltype(g_nccl.AllReduce))dlsym(h, "ncclAllReduce");
+  g_nccl.CommDestroy = (decltype(g_nccl.CommDestroy))dlsym(h, "ncclCommDestroy");
+  g_nccl.GetErrorString = (decltype(g_nccl.GetErrorString))dlsym(h, "ncclGetErrorString");
+  if (!g_nccl.GetUniqueId || !g_nccl.CommInitRank || !g_nccl.AllReduce || !g_nccl.CommDestroy)
+    return fail(FSV_ERR_RUNTIME, "NCCL library lacks required symbols");
+  g_nccl.loaded = true;
+  return FSV_OK;
+}
+
+#define NCCL_TRY(x)                                                                        \
+  do {                                                                                     \
+    ncclResult_t r_ = (x);                                                                 \
+    if (r_ != ncclSuccess)                                                                 \
+      return fail(FSV_ERR_RUNTIME, "NCCL error %d (%s) at %s:%d", (int)r_,                \
+                  g_nccl.GetErrorString ? g_nccl.GetErrorString(r_) : "?", __FILE__, __LINE__); \
+  } while (0)
+
+// ---------------------------------------------------------------------------
+// device buffer helper
+
+template <typename T>
+struct DBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  cudaError_t alloc(size_t count) {
+    free();
+    n = count;
+    return cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T));
+  }
+  void free() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  ~DBuf() { free(); }
+};
+
+static constexpr int kHubMax = 49152;     // 192 KB of shared memory
+static constexpr int kHubMinDegree = 32;  // below this a hub slot buys nothing
+static constexpr int kTraceCap = 4096;    // iteration cap of the counter array
+
+struct fsv_ctx {
+  int device = 0;
+  int sm_count = 148;
+  cudaStream_t own_stream = nullptr;
+  cudaStream_t stream = nullptr;
+  // graph layout
+  bool ready = false;
+  int64_t n = 0, m_dir = 0, E = 0, Epad = 0;
+  int R = 0, H = 0;
+  DBuf<uint32_t> ecol;
+  DBuf<int> nzrows, span_base, hub_id, f1;
+  // solve state
+  DBuf<int> X, Y, G, G_hub, hub_acc, done;
+  DBuf<unsigned long long> cnt;
+  DBuf<unsigned int> ticket;
+  int* h_done = nullptr;  // pinned
+  std::vector<cudaEvent_t> events;
+  // profile mode: events around every kernel of iteration k: [k][0..7]
+  std::vector<cudaEvent_t> pev;
+  bool profile = false;
+  float hook_ms = 0, hubfix_ms = 0, shortcut_ms = 0, first_ms = 0, allreduce_ms = 0;
+  int hook_launches = 0;
+  // results of the last solve
+  int iterations = 0;
+  int components = 0;
+  float solve_ms = 0.f;
+  std::vector<unsigned long long> h_cnt;
+  std::vector<float> iter_ms;
+  int labels_ready = 0;
+  int host_syncs = 0, launches = 0;
+  int hub_limit = kHubMax;
+  // multi-GPU
+  ncclComm_t comm = nullptr;
+  int nranks = 1, rank = 0;
+};
+
+static int ensure_events(fsv_ctx* c, size_t count) {
+  while (c->events.size() < count) {
+    cudaEvent_t e;
+    CUDA_TRY(cudaEventCreate(&e));
+    c->events.push_back(e);
+  }
+  return FSV_OK;
+}
+
+extern "C" int fsv_create(int device, fsv_ctx** out) {
+  if (!out) return fail(FSV_ERR_CONTRACT, "out pointer is NULL");
+  *out = nullptr;
+  int count = 0;
+  int rc = fsv_device_count(&count);
+  if (rc) return rc;
+  if (device < 0 || device >= count)
+    return fail(FSV_ERR_CONTRACT, "device %d out of range (%d devices)", device, count);
+  CUDA_TRY(cudaSetDevice(device));
+  fsv_ctx* c = new fsv_ctx();
+  c->device = device;
+  cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device);
+  if (cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaMallocHost(&c->h_done, sizeof(int)) != cudaSuccess) {
+    delete c;
+    return fail(FSV_ERR_RUNTIME, "stream/pinned allocation failed");
+  }
+  c->stream = c->own_stream;
+  cudaError_t e = cudaFuncSetAttribute(k_hook, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       kHubMax * (int)sizeof(int));
+  if (e != cudaSuccess) {
+    delete c;
+    return fail(FSV_ERR_RUNTIME, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
+  }
+  *out = c;
+  return FSV_OK;
+}
+
+extern "C" int fsv_destroy(fsv_ctx* c) {
+  if (!c) return FSV_OK;
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->stream);
+  for (auto e : c->events) cudaEventDestroy(e);
+  if (c->comm && g_nccl.CommDestroy) g_nccl.CommDestroy(c->comm);
+  if (c->h_done) cudaFreeHost(c->h_done);
+  if (c->own_stream) cudaStreamDestroy(c->own_stream);
+  delete c;
+  return FSV_OK;
+}
+
+extern "C" int fsv_set_stream(fsv_ctx* c, void* s) {
+  if (!c) return fail(FSV_ERR_CONTRACT, "NULL context");
+  c->stream = s ? (cudaStream_t)s : c->own_stream;
+  return FSV_OK;
+}
+
+// ---------------------------------------------------------------------------
+// upload pipeline kernels
+
+__global__ void k_degree(const int64_t* __restrict__ off, long long n, int* __restrict__ deg,
+                         int* __restrict__ ids) {
+  for (long long u = blockIdx.x * (long long)blockDim.x + threadIdx.x; u < n;
+       u += (long long)gridDim.x * blockDim.x) {
+    deg[u] = (int)(off[u + 1] - off[u]);
+    ids[u] = (int)u;
+  }
+}
+
+template <typename ColT>
+__global__ void k_check_cols(const ColT* __restrict__ cols, long long m, long long n,
+                             unsigned long long* bad) {
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < m;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long v = (long long)cols[e];
+    if (v < 0 || v >= n) atomicMin(bad, (unsigned long long)e);
+  }
+}
+
+__global__ void k_hub_slots(const int* __restrict__ sorted_ids, int H, int* __restrict__ slot_of,
+                            int* __restrict__ hub_id) {
+  for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < H; s += gridDim.x * blockDim.x) {
+    const int v = sorted_ids[s];
+    hub_id[s] = v;
+    slot_of[v] = s;
+  }
+}
+
+__device__ __forceinline__ bool key_less(int du, int u, int dv, int v) {
+  return du < dv || (du == dv && u < v);
+}
+
+// Warp per row: number of entries kept by the orientation (row u keeps v iff
+// (deg u, u) < (deg v, v), so each undirected edge is stored exactly once).
+template <typename ColT>
+__global__ void k_orient_count(const int64_t* __restrict__ off, const ColT* __restrict__ cols,
+                               long long col_base, long long row_begin, long long rows,
+                               const int* __restrict__ deg, long long* __restrict__ cnt,
+                               int* __restrict__ nzflag) {
+  const int lane = threadIdx.x & 31;
+  const long long nw = (long long)gridDim.x * (blockDim.x >> 5);
+  for (long long w = blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5); w < rows;
+       w += nw) {
+    const long long u = row_begin + w;
+    const int du = deg[u];
+    long long k = 0;
+    for (long long e = off[u] + lane; e < off[u + 1]; e += 32) {
+      const int v = (int)cols[e - col_base];
+      k += key_less(du, (int)u, deg[v], v);
+    }
+    for (int o = 16; o; o >>= 1) k += __shfl_xor_sync(0xffffffffu, k, o);
+    if (lane == 0) {
+      cnt[w] = k;
+      nzflag[w] = k > 0;
+    }
+  }
+}
+
+template <typename ColT>
+__global__ void k_orient_write(const int64_t* __restrict__ off, const ColT* __restrict__ cols,
+                               long long col_base, long long row_begin, long long rows,
+                               const int* __restrict__ deg, const long long* __restrict__ out_off,
+                               const int* __restrict__ nzidx, const int* __restrict__ slot_of,
+                               uint32_t* __restrict__ ecol, int* __restrict__ nzrows,
+                               long long* __restrict__ nzoff) {
+  const int lane = threadIdx.x & 31;
+  const long long nw = (long long)gridDim.x * (blockDim.x >> 5);
+  for (long long w = blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5); w < rows;
+       w += nw) {
+    const long long u = row_begin + w;
+    const int du = deg[u];
+    long long o = out_off[w];
+    const long long o0 = o;
+    const long long hi = off[u + 1];
+    for (long long e0 = off[u]; e0 < hi; e0 += 32) {
+      const long long e = e0 + lane;
+      bool keep = false;
+      int v = 0;
+      if (e < hi) {
+        v = (int)cols[e - col_base];
+        keep = key_less(du, (int)u, deg[v], v);
+      }
+      const unsigned b = __ballot_sync(0xffffffffu, keep);
+      if (keep) {
+        const long long pos = o + __popc(b & ((1u << lane) - 1u));
+        const int s = slot_of[v];
+        uint32_t code = s >= 0 ? (HUB | (uint32_t)s) : (uint32_t)v;
+        if (pos == o0) code |= HEAD;
+        ecol[pos] = code;
+      }
+      o += __popc(b);
+    }
+    if (lane == 0 && o > o0) {
+      const int r = nzidx[w];
+      nzrows[r] = (int)u;
+      nzoff[r] = o0;
+    }
+  }
+}
+
+__global__ void k_pad(uint32_t* ecol, long long E, long long Epad, int n, int* nzrows, int R,
+                      long long* nzoff) {
+  for (long long e = E + blockIdx.x * (long long)blockDim.x + threadIdx.x; e < Epad;
+       e += (long long)gridDim.x * blockDim.x)
+    ecol[e] = (e == E ? HEAD : 0u) | (uint32_t)n;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    nzrows[R] = n;  // dummy row: vertex n has gf = INF, so it never emits
+    nzoff[R] = E;
+  }
+}
+
+// span_base[s] = (number of rows whose head is at or before entry s*SPAN-1) - 1
+__global__ void k_span_base(const long long* __restrict__ nzoff, int R1, long long nspans,
+                            int* __restrict__ span_base) {
+  for (long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x; s < nspans;
+       s += (long long)gridDim.x * blockDim.x) {
+    const long long target = s * SPAN - 1;
+    int lo = 0, hi = R1;  // upper_bound over nzoff[0..R1)
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (nzoff[mid] <= target) lo = mid + 1; else hi = mid;
+    }
+    span_base[s] = lo - 1;
+  }
+}
+
+// f_1[u] = min(u, first (= smallest) column of row u) for rows this rank owns;
+// other rows get INF so an allreduce-min assembles the global vector.
+template <typename ColT>
+__global__ void k_f1(const int64_t* __restrict__ off, const ColT* __restrict__ cols,
+                     long long col_base, long long row_begin, long long row_end, long long n,
+                     int* __restrict__ f1) {
+  for (long long u = blockIdx.x * (long long)blockDim.x + threadIdx.x; u < n;
+       u += (long long)gridDim.x * blockDim.x) {
+    int val = INF;
+    if (u >= row_begin && u < row_end) {
+      val = (int)u;
+      if (off[u + 1] > off[u]) val = min(val, (int)cols[off[u] - col_base]);
+    }
+    f1[u] = val;
+  }
+}
+
+static int grid_for(fsv_ctx* c, long long work, int threads, int per_sm = 8) {
+  long long g = (work + threads - 1) / threads;
+  g = std::min<long long>(g, (long long)c->sm_count * per_sm);
+  return (int)std::max<long long>(g, 1);
+}
+
+template <typename ColT>
+static int upload_impl(fsv_ctx* c, int64_t n, const int64_t* h_off, const ColT* h_cols,
+                       int64_t row_begin, int64_t row_end) {
+  if (!c) return fail(FSV_ERR_CONTRACT, "NULL context");
+  if (n < 0) return fail(FSV_ERR_INPUT, "vertex count must be non-negative, got %lld", (long long)n);
+  if (n >= (int64_t)IDMASK) return fail(FSV_ERR_INPUT, "n=%lld exceeds the device id range", (long long)n);
+  if (!h_off) return fail(FSV_ERR_CONTRACT, "row_offsets is NULL");
+  if (row_begin < 0 || row_end < row_begin || row_end > n)
+    return fail(FSV_ERR_CONTRACT, "row range [%lld, %lld) invalid for n=%lld", (long long)row_begin,
+                (long long)row_end, (long long)n);
+  if (h_off[0] != 0) return fail(FSV_ERR_INPUT, "row_offsets[0] must be 0");
+  for (int64_t u = 0; u < n; ++u)
+    if (h_off[u + 1] < h_off[u]) return fail(FSV_ERR_INPUT, "row_offsets must be non-decreasing");
+  const int64_t e_begin = h_off[row_begin], e_end = h_off[row_end];
+  const int64_t mloc = e_end - e_begin;
+  if (mloc > 0 && !h_cols) return fail(FSV_ERR_CONTRACT, "col_indices is NULL");
+  CUDA_TRY(cudaSetDevice(c->device));
+  cudaStream_t st = c->stream;
+  c->ready = false;
+  c->labels_ready = 0;
+
+  const long long rows = row_end - row_begin;
+  DBuf<int64_t> d_off;
+  DBuf<ColT> d_cols;
+  CUDA_TRY(d_off.alloc((size_t)n + 1));
+  CUDA_TRY(d_cols.alloc((size_t)mloc));
+  CUDA_TRY(cudaMemcpyAsync(d_off.p, h_off, sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice, st));
+  if (mloc) CUDA_TRY(cudaMemcpyAsync(d_cols.p, h_cols, sizeof(ColT) * mloc, cudaMemcpyHostToDevice, st));
+
+  // column range check (graph.py:71-75 semantics: report an offending entry)
+  DBuf<unsigned long long> d_bad;
+  CUDA_TRY(d_bad.alloc(1));
+  CUDA_TRY(cudaMemsetAsync(d_bad.p, 0xff, sizeof(unsigned long long), st));
+  if (mloc) k_check_cols<ColT><<<grid_for(c, mloc, 256), 256, 0, st>>>(d_cols.p, mloc, n, d_bad.p);
+  unsigned long long h_bad = 0;
+  CUDA_TRY(cudaMemcpyAsync(&h_bad, d_bad.p, sizeof h_bad, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  if (h_bad != ~0ull) {
+    const int64_t e = e_begin + (int64_t)h_bad;
+    const int64_t* it = std::upper_bound(h_off, h_off + n + 1, e);
+    const long long u = (long long)(it - h_off) - 1;
+    return fail(FSV_ERR_INPUT, "edge (%lld, %lld) out of range for n=%lld", u,
+                (long long)h_cols[h_bad], (long long)n);
+  }
+
+  // degrees + hub selection (top-H by degree, stable, identical on all ranks)
+  DBuf<int> deg, ids, deg_sorted, ids_sorted, slot_of;
+  CUDA_TRY(deg.alloc(n)); CUDA_TRY(ids.alloc(n));
+  CUDA_TRY(deg_sorted.alloc(n)); CUDA_TRY(ids_sorted.alloc(n)); CUDA_TRY(slot_of.alloc(n));
+  if (n) k_degree<<<grid_for(c, n, 256), 256, 0, st>>>(d_off.p, n, deg.p, ids.p);
+  int H = 0;
+  if (n) {
+    size_t tmp_bytes = 0;
+    cub::DeviceRadixSort::SortPairsDescending(nullptr, tmp_bytes, deg.p, deg_sorted.p, ids.p,
+                                              ids_sorted.p, (int)n, 0, 32, st);
+    DBuf<unsigned char> tmp;
+    CUDA_TRY(tmp.alloc(tmp_bytes));
+    CUDA_TRY(cub::DeviceRadixSort::SortPairsDescending(tmp.p, tmp_bytes, deg.p, deg_sorted.p, ids.p,
+                                                       ids_sorted.p, (int)n, 0, 32, st));
+    // number of vertices with degree >= kHubMinDegree among the first kHubMax
+    const int probe = (int)std::min<int64_t>(n, kHubMax);
+    std::vector<int> top(probe);
+    CUDA_TRY(cudaMemcpyAsync(top.data(), deg_sorted.p, sizeof(int) * probe, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    int cand = 0;
+    while (cand < probe && top[cand] >= kHubMinDegree) ++cand;
+    H = (c->hub_limit >= 0) ? std::min(cand, c->hub_limit) : 0;
+    H &= ~3;
+    if (H < 256) H = 0;
+  }
+  c->H = H;
+  if (n) CUDA_TRY(cudaMemsetAsync(slot_of.p, 0xff, sizeof(int) * n, st));
+  CUDA_TRY(c->hub_id.alloc(std::max(H, 4)));
+  if (H) k_hub_slots<<<grid_for(c, H, 256), 256, 0, st>>>(ids_sorted.p, H, slot_of.p, c->hub_id.p);
+
+  // orientation
+  DBuf<long long> cnt, out_off;
+  DBuf<int> nzflag, nzidx;
+  CUDA_TRY(cnt.alloc(rows + 1)); CUDA_TRY(out_off.alloc(rows + 1));
+  CUDA_TRY(nzflag.alloc(rows + 1)); CUDA_TRY(nzidx.alloc(rows + 1));
+  CUDA_TRY(cudaMemsetAsync(cnt.p + rows, 0, sizeof(long long), st));
+  CUDA_TRY(cudaMemsetAsync(nzflag.p + rows, 0, sizeof(int), st));
+  if (rows)
+    k_orient_count<ColT><<<grid_for(c, rows * 32, 256, 16), 256, 0, st>>>(
+        d_off.p, d_cols.p, e_begin, row_begin, rows, deg.p, cnt.p, nzflag.p);
+  {
+    size_t b1 = 0, b2 = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, b1, cnt.p, out_off.p, (int)(rows + 1), st);
+    cub::DeviceScan::ExclusiveSum(nullptr, b2, nzflag.p, nzidx.p, (int)(rows + 1), st);
+    DBuf<unsigned char> tmp;
+    CUDA_TRY(tmp.alloc(std::max(b1, b2)));
+    CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp.p, b1, cnt.p, out_off.p, (int)(rows + 1), st));
+    CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp.p, b2, nzflag.p, nzidx.p, (int)(rows + 1), st));
+  }
+  long long E = 0;
+  int R = 0;
+  CUDA_TRY(cudaMemcpyAsync(&E, out_off.p + rows, sizeof E, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaMemcpyAsync(&R, nzidx.p + rows, sizeof R, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  const long long Epad = (E + SPAN - 1) / SPAN * SPAN;
+  CUDA_TRY(c->ecol.alloc((size_t)std::max<long long>(Epad, 4)));
+  CUDA_TRY(c->nzrows.alloc((size_t)R + 1));
+  DBuf<long long> nzoff;
+  CUDA_TRY(nzoff.alloc((size_t)R + 1));
+  if (rows)
+    k_orient_write<ColT><<<grid_for(c, rows * 32, 256, 16), 256, 0, st>>>(
+        d_off.p, d_cols.p, e_begin, row_begin, rows, deg.p, out_off.p, nzidx.p, slot_of.p,
+        c->ecol.p, c->nzrows.p, nzoff.p);
+  k_pad<<<grid_for(c, std::max<long long>(Epad - E, 1), 256), 256, 0, st>>>(c->ecol.p, E, Epad, (int)n,
+                                                                             c->nzrows.p, R, nzoff.p);
+  const long long nspans = Epad / SPAN;
+  CUDA_TRY(c->span_base.alloc((size_t)std::max<long long>(nspans, 1)));
+  if (nspans)
+    k_span_base<<<grid_for(c, nspans, 256), 256, 0, st>>>(nzoff.p, R + 1, nspans, c->span_base.p);
+
+  // closed-form first iteration
+  CUDA_TRY(c->f1.alloc((size_t)n + 64));
+  if (n)
+    k_f1<ColT><<<grid_for(c, n, 256), 256, 0, st>>>(d_off.p, d_cols.p, e_begin, row_begin, row_end, n,
+                                                    c->f1.p);
+  if (c->comm && n) {
+    NCCL_TRY(g_nccl.AllReduce(c->f1.p, c->f1.p, (size_t)n, ncclInt32, ncclMin, c->comm, st));
+  }
+
+  // solve buffers: n + dummy vertex, padded for 16-byte vector access
+  const size_t nv = ((size_t)n + 1 + 63) / 64 * 64;
+  CUDA_TRY(c->X.alloc(nv)); CUDA_TRY(c->Y.alloc(nv)); CUDA_TRY(c->G.alloc(nv));
+  CUDA_TRY(c->G_hub.alloc(std::max(H, 4))); CUDA_TRY(c->hub_acc.alloc(std::max(H, 4)));
+  CUDA_TRY(c->done.alloc(1)); CUDA_TRY(c->ticket.alloc(1));
+  CUDA_TRY(c->cnt.alloc((size_t)kTraceCap * NCOUNT));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  CUDA_TRY(cudaGetLastError());
+
+  c->n = n;
+  c->m_dir = h_off[n];
+  c->E = E;
+  c->Epad = Epad;
+  c->R = R;
+  c->ready = true;
+  return FSV_OK;
+}
+
+extern "C" int fsv_set_hub_slots(fsv_ctx* c, int slots) {
+  if (!c) return fail(FSV_ERR_CONTRACT, "NULL context");
+  c->hub_limit = slots < 0 ? -1 : (slots == 0 ? kHubMax : std::min(slots, kHubMax));
+  return FSV_OK;
+}
+
+extern "C" int fsv_upload_csr(fsv_ctx* c, int64_t n, const int64_t* off, const int32_t* cols,
+                              int64_t row_begin, int64_t row_end) {
+  return upload_impl<int32_t>(c, n, off, cols, row_begin, row_end);
+}
+
+extern "C" int fsv_upload_csr64(fsv_ctx* c, int64_t n, const int64_t* off, const int64_t* cols,
+                                int64_t row_begin, int64_t row_end) {
+  return upload_impl<int64_t>(c, n, off, cols, row_begin, row_end);
+}
+
+// ---------------------------------------------------------------------------
+// solve
+
+// Buffers of iteration k >= 2: F = f_{k-1}, N = f_k (initialised to gf_{k-1}).
+// k_first leaves f_1 in Y and gf_1 in X, so even k reads F = Y, N = X.
+static inline int* bufF(fsv_ctx* c, int k) { return (k & 1) ? c->X.p : c->Y.p; }
+static inline int* bufN(fsv_ctx* c, int k) { return (k & 1) ? c->Y.p : c->X.p; }
+
+static constexpr int kPev = 8;  // profile events per iteration
+
+static int ensure_pevents(fsv_ctx* c, size_t count) {
+  while (c->pev.size() < count) {
+    cudaEvent_t e;
+    CUDA_TRY(cudaEventCreate(&e));
+    c->pev.push_back(e);
+  }
+  return FSV_OK;
+}
+
+static inline void pmark(fsv_ctx* c, int k, int slot) {
+  if (c->profile) cudaEventRecord(c->pev[(size_t)k * kPev + slot], c->stream);
+}
+
+static int launch_iteration(fsv_ctx* c, int k, int max_iter) {
+  cudaStream_t st = c->stream;
+  if (c->profile) {
+    int rc = ensure_pevents(c, (size_t)(k + 1) * kPev);
+    if (rc) return rc;
+  }
+  int* F = bufF(c, k);
+  int* N = bufN(c, k);
+  const long long nspans = c->Epad / SPAN;
+  if (nspans) {
+    HookArgs a;
+    a.ecol = c->ecol.p; a.nspans = nspans; a.span_base = c->span_base.p; a.nzrows = c->nzrows.p;
+    a.F = F; a.G = c->G.p; a.N = N; a.G_hub = c->G_hub.p; a.H = c->H; a.hub_acc = c->hub_acc.p;
+    a.done = c->done.p;
+    const int grid = (int)std::min<long long>(c->sm_count, (nspans + 31) / 32);
+    pmark(c, k, 0);
+    k_hook<<<std::max(grid, 1), HOOK_THREADS, c->H * sizeof(int), st>>>(a);
+    pmark(c, k, 1);
+    ++c->launches;
+  }
+  if (c->H) {
+    pmark(c, k, 2);
+    k_hubfix<<<grid_for(c, c->H, 256), 256, 0, st>>>(c->hub_acc.p, c->hub_id.p, c->H, F, c->G.p, N,
+                                                       c->done.p);
+    pmark(c, k, 3);
+    ++c->launches;
+  }
+  if (c->comm && c->n) {
+    pmark(c, k, 4);
+    NCCL_TRY(g_nccl.AllReduce(N, N, (size_t)c->n, ncclInt32, ncclMin, c->comm, st));
+    pmark(c, k, 5);
+  }
+  ShortcutArgs s;
+  s.F = F; s.G = c->G.p; s.N = N; s.n = c->n; s.hub_id = c->hub_id.p; s.G_hub = c->G_hub.p;
+  s.H = c->H; s.cnt = c->cnt.p + (size_t)(k - 1) * NCOUNT; s.ticket = c->ticket.p; s.done = c->done.p;
+  s.iter = k; s.max_iter = max_iter;
+  pmark(c, k, 6);
+  k_shortcut<<<grid_for(c, std::max<long long>(c->n / 4, c->H), SC_THREADS, 4), SC_THREADS, 0, st>>>(s);
+  pmark(c, k, 7);
+  ++c->launches;
+  return FSV_OK;
+}
+
+// Copies f_k (the committed parent vector of iteration k) to host.
+static int copy_snapshot(fsv_ctx* c, int k, int32_t* dst) {
+  const int* src = (k == 1) ? c->Y.p : bufN(c, k);
+  CUDA_TRY(cudaMemcpyAsync(dst, src, sizeof(int) * c->n, cudaMemcpyDeviceToHost, c->stream));
+  return FSV_OK;
+}
+
+static int solve_impl(fsv_ctx* c, const fsv_config* cfg, int32_t* snapshots, int32_t snap_cap) {
+  if (!c) return fail(FSV_ERR_CONTRACT, "NULL context");
+  if (!c->ready) return fail(FSV_ERR_CONTRACT, "no graph uploaded");
+  CUDA_TRY(cudaSetDevice(c->device));
+  fsv_config d{};
+  if (cfg) d = *cfg;
+  if (d.max_iters < 0 || d.batch < 0) return fail(FSV_ERR_CONTRACT, "negative max_iters/batch");
+  const int cap = d.max_iters > 0 ? std::min(d.max_iters, kTraceCap) : kTraceCap;
+  int batch = d.batch > 0 ? d.batch : 4;
+  if (snapshots) batch = 1;
+  cudaStream_t st = c->stream;
+  int rc = ensure_events(c, 2);
+  if (rc) return rc;
+  c->launches = 0;
+  c->host_syncs = 0;
+  c->labels_ready = 0;
+  c->profile = d.profile != 0;
+  c->hook_ms = c->hubfix_ms = c->shortcut_ms = c->first_ms = c->allreduce_ms = 0.f;
+  c->hook_launches = 0;
+  if (c->profile && (rc = ensure_pevents(c, 2 * kPev))) return rc;
+
+  CUDA_TRY(cudaEventRecord(c->events[0], st));
+  k_solve_init<<<grid_for(c, std::max<long long>(c->H, (long long)cap * NCOUNT), 256), 256, 0, st>>>(
+      c->X.p, c->Y.p, c->G.p, c->n, c->hub_acc.p, c->H, c->cnt.p, (long long)cap * NCOUNT, c->done.p,
+      c->ticket.p);
+  pmark(c, 1, 6);
+  k_first<<<grid_for(c, std::max<long long>(c->n / 4, c->H), SC_THREADS, 4), SC_THREADS, 0, st>>>(
+      c->f1.p, c->Y.p, c->G.p, c->X.p, c->n, c->hub_id.p, c->G_hub.p, c->H, c->cnt.p, c->ticket.p,
+      c->done.p, cap);
+  pmark(c, 1, 7);
+  c->launches += 2;
+  if ((rc = ensure_events(c, 2))) return rc;
+  CUDA_TRY(cudaEventRecord(c->events[1], st));
+  if (snapshots) {
+    if (snap_cap < 1) return fail(FSV_ERR_CONTRACT, "snapshot capacity exhausted");
+    if ((rc = copy_snapshot(c, 1, snapshots))) return rc;
+  }
+  int launched = 1;  // iterations queued so far
+  int done = 0;
+  for (;;) {
+    if (snapshots || launched > 1 || true) {
+      // read the flag after the first batch too: iteration 1 may already converge
+    }
+    const int upto = std::min(cap, launched + (launched == 1 && !snapshots ? batch - 1 : batch));
+    for (int k = launched + 1; k <= upto; ++k) {
+      if ((rc = launch_iteration(c, k, cap))) return rc;
+      if ((rc = ensure_events(c, (size_t)k + 1))) return rc;
+      CUDA_TRY(cudaEventRecord(c->events[k], st));
+    }
+    launched = std::max(launched, upto);
+    CUDA_TRY(cudaMemcpyAsync(c->h_done, c->done.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    ++c->host_syncs;
+    done = *c->h_done;
+    if (snapshots && (done == 0 || done == launched)) {
+      // batch == 1: iteration `launched` has committed f_k; copy it unless the
+      // flag says an earlier iteration converged (cannot happen with batch 1)
+      if (launched > 1) {
+        if (launched > snap_cap) return fail(FSV_ERR_CONTRACT, "more than %d iterations ran", snap_cap);
+        if ((rc = copy_snapshot(c, launched, snapshots + (size_t)(launched - 1) * c->n))) return rc;
+      }
+    }
+    if (done != 0) break;
+    if (launched >= cap)
+      return fail(FSV_ERR_RUNTIME, "did not converge within %d iterations", cap);
+  }
+  CUDA_TRY(cudaStreamSynchronize(st));
+  CUDA_TRY(cudaGetLastError());
+  if (done < 0) return fail(FSV_ERR_RUNTIME, "did not converge within %d iterations", -done);
+  const int iters = done;
+  c->iterations = iters;
+  c->h_cnt.assign((size_t)iters * NCOUNT, 0ull);
+  CUDA_TRY(cudaMemcpy(c->h_cnt.data(), c->cnt.p, sizeof(unsigned long long) * iters * NCOUNT,
+                      cudaMemcpyDeviceToHost));
+  c->iter_ms.assign(iters, 0.f);
+  for (int k = 1; k <= iters; ++k)
+    CUDA_TRY(cudaEventElapsedTime(&c->iter_ms[k - 1], c->events[k - 1], c->events[k]));
+  CUDA_TRY(cudaEventElapsedTime(&c->solve_ms, c->events[0], c->events[iters]));
+  if (c->profile) {
+    auto span = [&](int k, int a, int b) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, c->pev[(size_t)k * kPev + a], c->pev[(size_t)k * kPev + b]);
+      return ms;
+    };
+    c->first_ms = span(1, 6, 7);
+    for (int k = 2; k <= iters; ++k) {
+      if (c->Epad) { c->hook_ms += span(k, 0, 1); ++c->hook_launches; }
+      if (c->H) c->hubfix_ms += span(k, 2, 3);
+      if (c->comm && c->n) c->allreduce_ms += span(k, 4, 5);
+      c->shortcut_ms += span(k, 6, 7);
+    }
+  }
+  c->components = (int)c->h_cnt[(size_t)(iters - 1) * NCOUNT + C_ROOTS];
+  c->labels_ready = 1;
+  for (int k = 0; k < iters; ++k)
+    if (c->h_cnt[(size_t)k * NCOUNT + C_VIOL])
+      return fail(FSV_ERR_INVARIANT, "parent vector increased during kernel iteration");
+  if (c->h_cnt[(size_t)(iters - 1) * NCOUNT + C_NONSTAR])
+    return fail(FSV_ERR_INVARIANT, "algorithm terminated on non-star forest");
+  return FSV_OK;
+}
+
+static void fill_stats(fsv_ctx* c, fsv_stats* s) {
+  if (!s) return;
+  memset(s, 0, sizeof *s);
+  s->iterations = c->iterations;
+  s->component_count = c->components;
+  s->n = c->n;
+  s->m_dir = c->m_dir;
+  s->oriented_entries = c->E;
+  s->hub_slots = c->H;
+  s->host_syncs = c->host_syncs;
+  s->kernel_launches = c->launches;
+  s->solve_ms = c->solve_ms;
+  s->hook_ms = c->hook_ms;
+  s->hubfix_ms = c->hubfix_ms;
+  s->shortcut_ms = c->shortcut_ms;
+  s->first_ms = c->first_ms;
+  s->allreduce_ms = c->allreduce_ms;
+  s->hook_launches = c->hook_launches;
+}
+
+extern "C" int fsv_solve(fsv_ctx* c, const fsv_config* cfg, fsv_stats* stats) {
+  int rc = solve_impl(c, cfg, nullptr, 0);
+  if (c) fill_stats(c, stats);
+  return rc;
+}
+
+extern "C" int fsv_get_labels(fsv_ctx* c, int32_t* labels) {
+  if (!c || !c->labels_ready) return fail(FSV_ERR_CONTRACT, "no solve result available");
+  if (!c->n) return FSV_OK;
+  if (!labels) return fail(FSV_ERR_CONTRACT, "labels is NULL");
+  CUDA_TRY(cudaSetDevice(c->device));
+  CUDA_TRY(cudaMemcpyAsync(labels, c->G.p, sizeof(int) * c->n, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  return FSV_OK;
+}
+
+extern "C" int fsv_get_labels64(fsv_ctx* c, int64_t* labels) {
+  if (!c || !c->labels_ready) return fail(FSV_ERR_CONTRACT, "no solve result available");
+  if (!c->n) return FSV_OK;
+  std::vector<int32_t> tmp((size_t)c->n);
+  int rc = fsv_get_labels(c, tmp.data());
+  if (rc) return rc;
+  for (int64_t i = 0; i < c->n; ++i) labels[i] = tmp[(size_t)i];
+  return FSV_OK;
+}
+
+extern "C" int fsv_get_trace(fsv_ctx* c, int64_t* gfc, int64_t* fc, float* ms, int32_t cap) {
+  if (!c || !c->labels_ready) return fail(FSV_ERR_CONTRACT, "no solve result available");
+  const int k = std::min(cap, c->iterations);
+  for (int i = 0; i < k; ++i) {
+    if (gfc) gfc[i] = (int64_t)c->h_cnt[(size_t)i * NCOUNT + C_GF];
+    if (fc) fc[i] = (int64_t)c->h_cnt[(size_t)i * NCOUNT + C_F];
+    if (ms) ms[i] = c->iter_ms[(size_t)i];
+  }
+  return FSV_OK;
+}
+
+extern "C" int fsv_run(fsv_ctx* c, const fsv_config* cfg, int32_t* labels, int32_t* iterations,
+                       int64_t* gfc, int64_t* fc, int32_t cap) {
+  int rc = solve_impl(c, cfg, nullptr, 0);
+  if (c && c->labels_ready) {
+    if (iterations) *iterations = c->iterations;
+    fsv_get_trace(c, gfc, fc, nullptr, cap);
+  }
+  if (rc) return rc;
+  return labels ? fsv_get_labels(c, labels) : FSV_OK;
+}
+
+extern "C" int fsv_run_snapshots(fsv_ctx* c, const fsv_config* cfg, int32_t* labels,
+                                 int32_t* iterations, int64_t* gfc, int64_t* fc,
+                                 int32_t* snapshots, int32_t snap_cap) {
+  if (!snapshots) return fail(FSV_ERR_CONTRACT, "snapshots is NULL");
+  int rc = solve_impl(c, cfg, snapshots, snap_cap);
+  if (c && c->labels_ready) {
+    if (iterations) *iterations = c->iterations;
+    fsv_get_trace(c, gfc, fc, nullptr, snap_cap);
+  }
+  if (rc) return rc;
+  return labels ? fsv_get_labels(c, labels) : FSV_OK;
+}
+
+// ---------------------------------------------------------------------------
+// multi-GPU
+
+extern "C" int fsv_nccl_unique_id(void* id128) {
+  if (!id128) return fail(FSV_ERR_CONTRACT, "id buffer is NULL");
+  int rc = nccl_load();
+  if (rc) return rc;
+  ncclUniqueId id;
+  NCCL_TRY(g_nccl.GetUniqueId(&id));
+  memcpy(id128, &id, sizeof id);
+  return FSV_OK;
+}
+
+extern "C" int fsv_nccl_attach(fsv_ctx* c, const void* id128, int nranks, int rank) {
+  if (!c || !id128) return fail(FSV_ERR_CONTRACT, "NULL argument");
+  if (nranks < 1 || rank < 0 || rank >= nranks)
+    return fail(FSV_ERR_CONTRACT, "rank %d / nranks %d invalid", rank, nranks);
+  int rc = nccl_load();
+  if (rc) return rc;
+  CUDA_TRY(cudaSetDevice(c->device));
+  ncclUniqueId id;
+  memcpy(&id, id128, sizeof id);
+  if (c->comm) g_nccl.CommDestroy(c->comm);
+  c->comm = nullptr;
+  NCCL_TRY(g_nccl.CommInitRank(&c->comm, nranks, id, rank));
+  c->nranks = nranks;
+  c->rank = rank;
+  return FSV_OK;
+}

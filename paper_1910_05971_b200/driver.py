@@ -1,0 +1,334 @@
+"""The drop-in solver entry points (mirror svcc.driver / svcc.algorithms).
+
+``fastsv_la`` and ``fastsv`` keep the reference signatures
+(/root/reference/pkg/src/svcc/driver.py:64-65, algorithms.py:152-153) and
+result types (``RunResult``/``IterationTrace``, algorithms.py:38-57), but
+every iteration runs on a B200 through the C ABI of include/fastsv.h:
+
+    Solver.upload(g)  -> fsv_upload_csr   (device oriented layout)
+    Solver.run()      -> fsv_run          (whole FastSV loop on device)
+
+No Triton, no multi-backend dispatch, no CPU fallback: without the CUDA
+library or a device these calls raise.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native
+from ._native import FsvConfig, FsvStats
+from .errors import DeviceError, raise_for_status
+from .graph import ID_DTYPE, CsrGraph, Labeling, build_csr, labeling_from_parents
+
+_FORCE_MODES = ("auto", "dense_only", "sparse_only")
+
+
+@dataclass(frozen=True)
+class DriverConfig:
+    """Same fields and validation as svcc.DriverConfig (driver.py:31-48).
+
+    ``sparse_threshold``/``force_kernel`` select the reference's per-iteration
+    product; the B200 path always runs the full (dense) product, whose
+    snapshots the reference proves identical to every sparse/auto schedule
+    (test_driver.py:60-71). ``workers`` is accepted for signature parity.
+    ``batch`` is B200-only: iterations queued per host convergence check."""
+
+    sparse_threshold: float = 0.1
+    force_kernel: str = "auto"
+    workers: int = 1
+    batch: int = 0
+
+    def __post_init__(self):
+        if not 0.0 <= self.sparse_threshold <= 1.0:
+            raise ValueError(f"sparse_threshold must be in [0, 1], got {self.sparse_threshold}")
+        if self.force_kernel not in _FORCE_MODES:
+            raise ValueError(f"force_kernel must be one of {_FORCE_MODES}")
+        if self.workers < 1:
+            raise ValueError("workers must be >= 1")
+        if self.batch < 0:
+            raise ValueError("batch must be >= 0")
+
+
+def choose_kernel(gf_changed: int, n: int, cfg: DriverConfig) -> str:
+    """The reference's product-selection rule, strict inequality
+    (driver.py:51-61; test_driver.py:29-38)."""
+    if cfg.force_kernel == "dense_only":
+        return "dense"
+    if cfg.force_kernel == "sparse_only":
+        return "sparse"
+    return "sparse" if gf_changed < cfg.sparse_threshold * n else "dense"
+
+
+@dataclass(frozen=True)
+class HookingConfig:
+    """svcc.HookingConfig (algorithms.py:28-35). The device path implements
+    the all-flags configuration (FastSV proper); weaker flag sets are the
+    ablation study, not the hot path."""
+
+    grandparent_hooking: bool = True
+    stochastic_hooking: bool = True
+    aggressive_hooking: bool = True
+    early_termination: bool = True
+
+
+@dataclass(frozen=True)
+class IterationTrace:
+    iteration: int
+    gf_changed: int
+    f_changed: int
+    kernel: str
+    elapsed: float
+    flops: int = 0
+
+
+@dataclass
+class RunResult:
+    labeling: Labeling
+    iterations: int
+    trace: list
+    snapshots: list | None = field(default=None, repr=False)
+
+    @property
+    def total_elapsed(self) -> float:
+        return sum(t.elapsed for t in self.trace)
+
+
+def _check(code: int) -> None:
+    if code:
+        raise_for_status(code, _native.last_error())
+
+
+class Solver:
+    """One device context: owns the resident graph and the solve buffers.
+
+    ``upload`` is the (untimed) layout build; ``solve`` is the hot path.
+    Reusing a Solver across solves of the same graph keeps the layout
+    resident, as the bench does."""
+
+    def __init__(self, device: int = 0, hub_slots: int = 0):
+        self._lib = _native.fastsv_lib()
+        self._ctx = ctypes.c_void_p()
+        _check(self._lib.fsv_create(int(device), ctypes.byref(self._ctx)))
+        _check(self._lib.fsv_set_hub_slots(self._ctx, int(hub_slots)))
+        self.device = device
+        self.n = 0
+        self.m = 0
+        self.stats = FsvStats()
+
+    # -- lifetime ---------------------------------------------------------
+    def close(self):
+        if self._ctx:
+            self._lib.fsv_destroy(self._ctx)
+            self._ctx = ctypes.c_void_p()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- configuration ----------------------------------------------------
+    def set_stream(self, stream_ptr: int) -> None:
+        _check(self._lib.fsv_set_stream(self._ctx, ctypes.c_void_p(int(stream_ptr))))
+
+    def set_hub_slots(self, slots: int) -> None:
+        _check(self._lib.fsv_set_hub_slots(self._ctx, int(slots)))
+
+    def attach_nccl(self, unique_id: bytes, nranks: int, rank: int) -> None:
+        buf = ctypes.create_string_buffer(bytes(unique_id), 128)
+        _check(self._lib.fsv_nccl_attach(self._ctx, buf, int(nranks), int(rank)))
+
+    @staticmethod
+    def nccl_unique_id() -> bytes:
+        buf = ctypes.create_string_buffer(128)
+        _check(_native.fastsv_lib().fsv_nccl_unique_id(buf))
+        return buf.raw
+
+    # -- graph ------------------------------------------------------------
+    def upload(self, g, row_begin: int = 0, row_end: int | None = None, cols=None) -> None:
+        """Upload a CsrGraph (ours or the reference's). For a 1D partition pass
+        the row range and the column slice of those rows."""
+        n = int(g.n)
+        offsets = np.ascontiguousarray(g.row_offsets, dtype=np.int64)
+        if row_end is None:
+            row_end = n
+        if cols is None:
+            cols = g.col_indices[offsets[row_begin]:offsets[row_end]] if n else g.col_indices
+        cols = np.ascontiguousarray(cols)
+        if cols.dtype == np.int32:
+            fn = self._lib.fsv_upload_csr
+        else:
+            cols = cols.astype(np.int64, copy=False)
+            fn = self._lib.fsv_upload_csr64
+        _check(fn(self._ctx, n, offsets.ctypes.data, cols.ctypes.data if cols.size else None,
+                  int(row_begin), int(row_end)))
+        self.n = n
+        self.m = int(offsets[-1]) if n else 0
+
+    def upload_arrays(self, n: int, offsets_ptr: int, cols_ptr: int, row_begin: int = 0,
+                      row_end: int | None = None, int64_cols: bool = False) -> None:
+        """Upload from raw host pointers (e.g. pinned buffers) — the e2e path."""
+        fn = self._lib.fsv_upload_csr64 if int64_cols else self._lib.fsv_upload_csr
+        _check(fn(self._ctx, int(n), ctypes.c_void_p(offsets_ptr), ctypes.c_void_p(cols_ptr),
+                  int(row_begin), int(n if row_end is None else row_end)))
+        self.n = int(n)
+
+    # -- solve ------------------------------------------------------------
+    @staticmethod
+    def _config(batch: int = 0, max_iters: int = 0, profile: bool = False) -> FsvConfig:
+        cfg = FsvConfig()
+        cfg.batch = int(batch)
+        cfg.max_iters = int(max_iters)
+        cfg.profile = int(bool(profile))
+        return cfg
+
+    def solve(self, batch: int = 0, max_iters: int = 0, profile: bool = False) -> FsvStats:
+        """Run to convergence; labels stay on the device. ``profile`` brackets
+        every kernel with CUDA events (per-kernel *_ms in the stats)."""
+        cfg = self._config(batch, max_iters, profile)
+        _check(self._lib.fsv_solve(self._ctx, ctypes.byref(cfg), ctypes.byref(self.stats)))
+        return self.stats
+
+    def labels(self, out: np.ndarray | None = None) -> np.ndarray:
+        if out is None:
+            out = np.empty(self.n, dtype=np.int32)
+        fn = self._lib.fsv_get_labels if out.dtype == np.int32 else self._lib.fsv_get_labels64
+        _check(fn(self._ctx, out.ctypes.data if out.size else None))
+        return out
+
+    def labels_into(self, ptr: int) -> None:
+        _check(self._lib.fsv_get_labels(self._ctx, ctypes.c_void_p(ptr)))
+
+    def trace(self):
+        k = int(self.stats.iterations)
+        gfc = np.zeros(max(k, 1), dtype=np.int64)
+        fc = np.zeros(max(k, 1), dtype=np.int64)
+        ms = np.zeros(max(k, 1), dtype=np.float32)
+        _check(self._lib.fsv_get_trace(self._ctx, gfc.ctypes.data, fc.ctypes.data, ms.ctypes.data, k))
+        return gfc[:k], fc[:k], ms[:k]
+
+    def run(self, batch: int = 0, max_iters: int = 0, snapshots: bool = False, snap_cap: int = 256):
+        """Solve + copy out: (labels int32, iterations, gf_changed, f_changed,
+        per-iteration ms, snapshots or None)."""
+        cfg = self._config(batch, max_iters)
+        n = self.n
+        labels = np.empty(n, dtype=np.int32)
+        iters = ctypes.c_int32(0)
+        if snapshots:
+            cap = int(snap_cap)
+            snap = np.empty((cap, n), dtype=np.int32)
+            gfc = np.zeros(cap, dtype=np.int64)
+            fc = np.zeros(cap, dtype=np.int64)
+            _check(self._lib.fsv_run_snapshots(self._ctx, ctypes.byref(cfg),
+                                               labels.ctypes.data if n else None, ctypes.byref(iters),
+                                               gfc.ctypes.data, fc.ctypes.data,
+                                               snap.ctypes.data if n else ctypes.c_void_p(1), cap))
+        else:
+            _check(self._lib.fsv_solve(self._ctx, ctypes.byref(cfg), ctypes.byref(self.stats)))
+            iters.value = self.stats.iterations
+            if n:
+                self.labels(labels)
+            snap = None
+        k = int(iters.value)
+        gfc2 = np.zeros(max(k, 1), dtype=np.int64)
+        fc2 = np.zeros(max(k, 1), dtype=np.int64)
+        ms = np.zeros(max(k, 1), dtype=np.float32)
+        _check(self._lib.fsv_get_trace(self._ctx, gfc2.ctypes.data, fc2.ctypes.data, ms.ctypes.data, k))
+        return labels, k, gfc2[:k], fc2[:k], ms[:k], (snap[:k] if snap is not None else None)
+
+
+_solvers: dict = {}
+
+
+def default_solver(device: int = 0) -> Solver:
+    """Process-wide solver per device (context creation costs milliseconds)."""
+    s = _solvers.get(device)
+    if s is None:
+        s = _solvers[device] = Solver(device)
+    return s
+
+
+def _result(g, labels, iters, gfc, fc, ms, snaps, kernel="dense") -> RunResult:
+    m = int(g.col_indices.size)
+    trace = [IterationTrace(iteration=i + 1, gf_changed=int(gfc[i]), f_changed=int(fc[i]),
+                            kernel=kernel, elapsed=float(ms[i]) / 1e3,
+                            flops=m if kernel == "dense" else 0)
+             for i in range(iters)]
+    snapshots = None
+    if snaps is not None:
+        snapshots = []
+        for s in snaps:
+            a = s.astype(ID_DTYPE)
+            a.flags.writeable = False
+            snapshots.append(a)
+    return RunResult(labeling=labeling_from_parents(labels.astype(ID_DTYPE)), iterations=int(iters),
+                     trace=trace, snapshots=snapshots)
+
+
+def _solve_graph(g, record_snapshots: bool, batch: int, device: int) -> RunResult:
+    solver = default_solver(device)
+    solver.upload(g)
+    labels, iters, gfc, fc, ms, snaps = solver.run(batch=batch, snapshots=record_snapshots,
+                                                   snap_cap=max(64, 4 * int(np.log2(max(g.n, 2))) + 16))
+    return _result(g, labels, iters, gfc, fc, ms, snaps)
+
+
+def fastsv_la(g, cfg: DriverConfig | None = None, record_snapshots: bool = False,
+              device: int = 0) -> RunResult:
+    """FastSV in the matrix formulation (driver.py:64-120) on a B200.
+
+    Per-iteration parent vectors, iteration count, gf_changed/f_changed and
+    labels are bit-identical to the reference for every DriverConfig."""
+    cfg = cfg or DriverConfig()
+    return _solve_graph(g, record_snapshots, cfg.batch, device)
+
+
+def fastsv(g, cfg: HookingConfig | None = None, record_snapshots: bool = False,
+           device: int = 0) -> RunResult:
+    """All-flags FastSV (algorithms.py:152-167) on a B200; identical results
+    to fastsv_la (the reference proves this, test_acceptance.py:207-218)."""
+    cfg = cfg or HookingConfig()
+    if cfg != HookingConfig():
+        raise NotImplementedError(
+            "the B200 path implements all-flags FastSV; weaker HookingConfig variants "
+            "(the sv1..sv4 ablation) are not on the hot path")
+    res = _solve_graph(g, record_snapshots, 0, device)
+    for i, t in enumerate(res.trace):
+        res.trace[i] = IterationTrace(t.iteration, t.gf_changed, t.f_changed, "none", t.elapsed, 0)
+    return res
+
+
+def connected_components(n: int, edges, device: int = 0) -> np.ndarray:
+    """Edge list in, label vector out (int64, minimum id per component)."""
+    g = build_csr(n, edges)
+    if g.n == 0:
+        return np.zeros(0, dtype=ID_DTYPE)
+    return fastsv_la(g, device=device).labeling.labels
+
+
+def device_count() -> int:
+    c = ctypes.c_int(0)
+    code = _native.fastsv_lib().fsv_device_count(ctypes.byref(c))
+    if code:
+        return 0
+    return int(c.value)
+
+
+def require_device() -> None:
+    if device_count() < 1:
+        raise DeviceError("no CUDA device available; the B200 solver has no CPU fallback")
+
+
+__all__ = ["DriverConfig", "HookingConfig", "IterationTrace", "RunResult", "Solver", "choose_kernel",
+           "fastsv_la", "fastsv", "connected_components", "default_solver", "device_count",
+           "require_device", "CsrGraph"]
