@@ -127,6 +127,7 @@ struct DBuf {
 static constexpr int kHubMax = 49152;     // 192 KB of shared memory
 static constexpr int kHubMinDegree = 32;  // below this a hub slot buys nothing
 static constexpr int kTraceCap = 4096;    // iteration cap of the counter array
+static constexpr int kScBlocksPerSm = 16; // vertex-pass grid cap (blocks of 512)
 
 struct fsv_ctx {
   int device = 0;
@@ -138,11 +139,12 @@ struct fsv_ctx {
   int64_t n = 0, m_dir = 0, E = 0, Epad = 0;
   int R = 0, H = 0;
   DBuf<uint32_t> ecol;
-  DBuf<int> nzrows, span_base, hub_id, f1;
+  DBuf<int> span_row, hub_id, f1;
   // solve state
   DBuf<int> X, Y, G, G_hub, hub_acc, done;
   DBuf<unsigned long long> cnt;
   DBuf<unsigned int> ticket;
+  DBuf<unsigned> partials;
   int* h_done = nullptr;  // pinned
   std::vector<cudaEvent_t> events;
   // profile mode: events around every kernel of iteration k: [k][0..7]
@@ -159,6 +161,7 @@ struct fsv_ctx {
   int labels_ready = 0;
   int host_syncs = 0, launches = 0;
   int hub_limit = kHubMax;
+  int sc_grid = 296;  // resident blocks of the vertex-pass kernels
   // multi-GPU
   ncclComm_t comm = nullptr;
   int nranks = 1, rank = 0;
@@ -191,6 +194,11 @@ extern "C" int fsv_create(int device, fsv_ctx** out) {
     return fail(FSV_ERR_RUNTIME, "stream/pinned allocation failed");
   }
   c->stream = c->own_stream;
+  {
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_shortcut, SC_THREADS, 0);
+    c->sc_grid = std::max(1, per_sm) * c->sm_count;
+  }
   cudaError_t e = cudaFuncSetAttribute(k_hook, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        kHubMax * (int)sizeof(int));
   if (e != cudaSuccess) {
@@ -274,7 +282,7 @@ __global__ void k_orient_count(const int64_t* __restrict__ off, const ColT* __re
     }
     for (int o = 16; o; o >>= 1) k += __shfl_xor_sync(0xffffffffu, k, o);
     if (lane == 0) {
-      cnt[w] = k;
+      cnt[w] = k ? k + 1 : 0;  // + header entry
       nzflag[w] = k > 0;
     }
   }
@@ -293,8 +301,9 @@ __global__ void k_orient_write(const int64_t* __restrict__ off, const ColT* __re
        w += nw) {
     const long long u = row_begin + w;
     const int du = deg[u];
-    long long o = out_off[w];
-    const long long o0 = o;
+    const long long o0 = out_off[w];
+    if (out_off[w + 1] == o0) continue;  // no kept entries: no header either
+    long long o = o0 + 1;                 // entry o0 is the row header
     const long long hi = off[u + 1];
     for (long long e0 = off[u]; e0 < hi; e0 += 32) {
       const long long e = e0 + lane;
@@ -306,15 +315,13 @@ __global__ void k_orient_write(const int64_t* __restrict__ off, const ColT* __re
       }
       const unsigned b = __ballot_sync(0xffffffffu, keep);
       if (keep) {
-        const long long pos = o + __popc(b & ((1u << lane) - 1u));
         const int s = slot_of[v];
-        uint32_t code = s >= 0 ? (HUB | (uint32_t)s) : (uint32_t)v;
-        if (pos == o0) code |= HEAD;
-        ecol[pos] = code;
+        ecol[o + __popc(b & ((1u << lane) - 1u))] = s >= 0 ? (HUB | (uint32_t)s) : (uint32_t)v;
       }
       o += __popc(b);
     }
-    if (lane == 0 && o > o0) {
+    if (lane == 0) {
+      ecol[o0] = HDR | (uint32_t)u;
       const int r = nzidx[w];
       nzrows[r] = (int)u;
       nzoff[r] = o0;
@@ -326,25 +333,27 @@ __global__ void k_pad(uint32_t* ecol, long long E, long long Epad, int n, int* n
                       long long* nzoff) {
   for (long long e = E + blockIdx.x * (long long)blockDim.x + threadIdx.x; e < Epad;
        e += (long long)gridDim.x * blockDim.x)
-    ecol[e] = (e == E ? HEAD : 0u) | (uint32_t)n;
+    ecol[e] = HDR | (uint32_t)n;  // empty rows of the dummy vertex n (gf = INF)
   if (blockIdx.x == 0 && threadIdx.x == 0) {
-    nzrows[R] = n;  // dummy row: vertex n has gf = INF, so it never emits
+    nzrows[R] = n;
     nzoff[R] = E;
   }
 }
 
-// span_base[s] = (number of rows whose head is at or before entry s*SPAN-1) - 1
-__global__ void k_span_base(const long long* __restrict__ nzoff, int R1, long long nspans,
-                            int* __restrict__ span_base) {
+// span_row[s] = vertex of the row whose entries include s*SPAN when that
+// entry is an edge (the row started in an earlier span), else -1.
+__global__ void k_span_row(const long long* __restrict__ nzoff, const int* __restrict__ nzrows,
+                           int R1, long long nspans, int* __restrict__ span_row) {
   for (long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x; s < nspans;
        s += (long long)gridDim.x * blockDim.x) {
-    const long long target = s * SPAN - 1;
+    const long long target = s * SPAN;
     int lo = 0, hi = R1;  // upper_bound over nzoff[0..R1)
     while (lo < hi) {
       const int mid = (lo + hi) >> 1;
       if (nzoff[mid] <= target) lo = mid + 1; else hi = mid;
     }
-    span_base[s] = lo - 1;
+    const int r = lo - 1;
+    span_row[s] = (r < 0 || nzoff[r] == target) ? -1 : nzrows[r];
   }
 }
 
@@ -472,19 +481,20 @@ static int upload_impl(fsv_ctx* c, int64_t n, const int64_t* h_off, const ColT* 
   CUDA_TRY(cudaStreamSynchronize(st));
   const long long Epad = (E + SPAN - 1) / SPAN * SPAN;
   CUDA_TRY(c->ecol.alloc((size_t)std::max<long long>(Epad, 4)));
-  CUDA_TRY(c->nzrows.alloc((size_t)R + 1));
+  DBuf<int> nzrows;
+  CUDA_TRY(nzrows.alloc((size_t)R + 1));
   DBuf<long long> nzoff;
   CUDA_TRY(nzoff.alloc((size_t)R + 1));
   if (rows)
     k_orient_write<ColT><<<grid_for(c, rows * 32, 256, 16), 256, 0, st>>>(
         d_off.p, d_cols.p, e_begin, row_begin, rows, deg.p, out_off.p, nzidx.p, slot_of.p,
-        c->ecol.p, c->nzrows.p, nzoff.p);
+        c->ecol.p, nzrows.p, nzoff.p);
   k_pad<<<grid_for(c, std::max<long long>(Epad - E, 1), 256), 256, 0, st>>>(c->ecol.p, E, Epad, (int)n,
-                                                                             c->nzrows.p, R, nzoff.p);
+                                                                             nzrows.p, R, nzoff.p);
   const long long nspans = Epad / SPAN;
-  CUDA_TRY(c->span_base.alloc((size_t)std::max<long long>(nspans, 1)));
+  CUDA_TRY(c->span_row.alloc((size_t)std::max<long long>(nspans, 1)));
   if (nspans)
-    k_span_base<<<grid_for(c, nspans, 256), 256, 0, st>>>(nzoff.p, R + 1, nspans, c->span_base.p);
+    k_span_row<<<grid_for(c, nspans, 256), 256, 0, st>>>(nzoff.p, nzrows.p, R + 1, nspans, c->span_row.p);
 
   // closed-form first iteration
   CUDA_TRY(c->f1.alloc((size_t)n + 64));
@@ -500,6 +510,7 @@ static int upload_impl(fsv_ctx* c, int64_t n, const int64_t* h_off, const ColT* 
   CUDA_TRY(c->X.alloc(nv)); CUDA_TRY(c->Y.alloc(nv)); CUDA_TRY(c->G.alloc(nv));
   CUDA_TRY(c->G_hub.alloc(std::max(H, 4))); CUDA_TRY(c->hub_acc.alloc(std::max(H, 4)));
   CUDA_TRY(c->done.alloc(1)); CUDA_TRY(c->ticket.alloc(1));
+  CUDA_TRY(c->partials.alloc((size_t)c->sc_grid * 8));
   CUDA_TRY(c->cnt.alloc((size_t)kTraceCap * NCOUNT));
   CUDA_TRY(cudaStreamSynchronize(st));
   CUDA_TRY(cudaGetLastError());
@@ -539,6 +550,13 @@ static inline int* bufN(fsv_ctx* c, int k) { return (k & 1) ? c->Y.p : c->X.p; }
 
 static constexpr int kPev = 8;  // profile events per iteration
 
+// Vertex-parallel kernels run one resident wave (grid-stride inside): their
+// end-of-block counter barrier makes extra waves expensive.
+static inline int vertex_grid(fsv_ctx* c) {
+  const long long want = (std::max<long long>(c->n / 4, c->H) + SC_THREADS - 1) / SC_THREADS;
+  return (int)std::max<long long>(1, std::min<long long>(want, c->sc_grid));
+}
+
 static int ensure_pevents(fsv_ctx* c, size_t count) {
   while (c->pev.size() < count) {
     cudaEvent_t e;
@@ -563,7 +581,7 @@ static int launch_iteration(fsv_ctx* c, int k, int max_iter) {
   const long long nspans = c->Epad / SPAN;
   if (nspans) {
     HookArgs a;
-    a.ecol = c->ecol.p; a.nspans = nspans; a.span_base = c->span_base.p; a.nzrows = c->nzrows.p;
+    a.ecol = c->ecol.p; a.nspans = nspans; a.span_row = c->span_row.p;
     a.F = F; a.G = c->G.p; a.N = N; a.G_hub = c->G_hub.p; a.H = c->H; a.hub_acc = c->hub_acc.p;
     a.done = c->done.p;
     const int grid = (int)std::min<long long>(c->sm_count, (nspans + 31) / 32);
@@ -587,9 +605,10 @@ static int launch_iteration(fsv_ctx* c, int k, int max_iter) {
   ShortcutArgs s;
   s.F = F; s.G = c->G.p; s.N = N; s.n = c->n; s.hub_id = c->hub_id.p; s.G_hub = c->G_hub.p;
   s.H = c->H; s.cnt = c->cnt.p + (size_t)(k - 1) * NCOUNT; s.ticket = c->ticket.p; s.done = c->done.p;
+  s.partials = c->partials.p;
   s.iter = k; s.max_iter = max_iter;
   pmark(c, k, 6);
-  k_shortcut<<<grid_for(c, std::max<long long>(c->n / 4, c->H), SC_THREADS, 4), SC_THREADS, 0, st>>>(s);
+  k_shortcut<<<vertex_grid(c), SC_THREADS, 0, st>>>(s);
   pmark(c, k, 7);
   ++c->launches;
   return FSV_OK;
@@ -628,9 +647,8 @@ static int solve_impl(fsv_ctx* c, const fsv_config* cfg, int32_t* snapshots, int
       c->X.p, c->Y.p, c->G.p, c->n, c->hub_acc.p, c->H, c->cnt.p, (long long)cap * NCOUNT, c->done.p,
       c->ticket.p);
   pmark(c, 1, 6);
-  k_first<<<grid_for(c, std::max<long long>(c->n / 4, c->H), SC_THREADS, 4), SC_THREADS, 0, st>>>(
-      c->f1.p, c->Y.p, c->G.p, c->X.p, c->n, c->hub_id.p, c->G_hub.p, c->H, c->cnt.p, c->ticket.p,
-      c->done.p, cap);
+  k_first<<<vertex_grid(c), SC_THREADS, 0, st>>>(c->f1.p, c->Y.p, c->G.p, c->X.p, c->n, c->hub_id.p, c->G_hub.p, c->H, c->cnt.p,
+                  c->partials.p, c->ticket.p, c->done.p, cap);
   pmark(c, 1, 7);
   c->launches += 2;
   if ((rc = ensure_events(c, 2))) return rc;
@@ -711,7 +729,7 @@ static void fill_stats(fsv_ctx* c, fsv_stats* s) {
   s->component_count = c->components;
   s->n = c->n;
   s->m_dir = c->m_dir;
-  s->oriented_entries = c->E;
+  s->oriented_entries = c->E - c->R;  // edges only (headers excluded)
   s->hub_slots = c->H;
   s->host_syncs = c->host_syncs;
   s->kernel_launches = c->launches;

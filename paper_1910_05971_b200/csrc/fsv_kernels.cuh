@@ -31,14 +31,17 @@
 namespace fsv {
 
 constexpr int INF = 0x7fffffff;
-constexpr uint32_t HEAD = 0x80000000u;   // first entry of an oriented row
-constexpr uint32_t HUB = 0x40000000u;    // column is a hub: low bits = slot
+// Oriented layout entry codes (uint32):
+//   header  HDR | u          first entry of the row of vertex u
+//   edge    [HUB] | v/slot   neighbour v (or its hub slot) of the current row
+constexpr uint32_t HDR = 0x80000000u;
+constexpr uint32_t HUB = 0x40000000u;    // edge column is a hub: low bits = slot
 constexpr uint32_t IDMASK = 0x3fffffffu;
-constexpr int EPL = 4;                   // entries per lane per step (one 16-B load)
+constexpr int EPL = 8;                   // contiguous entries per lane per step
 constexpr int STEP = 32 * EPL;           // entries per warp step
-constexpr int STEPS = 8;                 // steps per span
+constexpr int STEPS = 4;                 // steps per span
 constexpr int SPAN = STEP * STEPS;       // entries per warp task
-constexpr int HOOK_THREADS = 1024;
+constexpr int HOOK_THREADS = 768;
 constexpr int SC_THREADS = 512;
 constexpr int NCOUNT = 8;                // counters per iteration
 enum { C_GF = 0, C_F = 1, C_NONSTAR = 2, C_ROOTS = 3, C_VIOL = 4 };
@@ -51,11 +54,11 @@ __device__ __forceinline__ uint64_t policy_evict_first() {
   return p;
 }
 
-// Streamed once per iteration: bypass L1, evict first from L2 so the parent
-// vectors stay L2-resident.
+// Streamed once per iteration: evict first from L2 so the parent vectors
+// stay L2-resident. L1 may allocate: a lane's two 16-byte halves share sectors.
 __device__ __forceinline__ uint4 ld_stream(const uint4* p, uint64_t pol) {
   uint4 r;
-  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+  asm volatile("ld.global.nc.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
                : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p), "l"(pol));
   return r;
 }
@@ -69,10 +72,9 @@ __device__ __forceinline__ void red_min(int* p, int v) {
 // ---- argument blocks --------------------------------------------------------
 
 struct HookArgs {
-  const uint32_t* ecol;   // oriented entries, padded to a multiple of SPAN
+  const uint32_t* ecol;   // oriented entries (headers + edges), padded to SPAN
   long long nspans;
-  const int* span_base;   // row index of the entry just before each span
-  const int* nzrows;      // row index -> vertex id (R rows + dummy)
+  const int* span_row;    // vertex of the row open at each span start, -1 if none
   const int* F;           // f_k
   const int* G;           // gf_k
   int* N;                 // f_{k+1}, pre-initialised to gf_k
@@ -91,6 +93,7 @@ struct ShortcutArgs {
   int* G_hub;
   int H;
   unsigned long long* cnt;  // this iteration's NCOUNT counters
+  unsigned* partials;       // per-block partial counters [grid][8]
   unsigned int* ticket;
   int* done;
   int iter;               // 1-based iteration number
@@ -109,37 +112,63 @@ __device__ __forceinline__ void emit_row(int u, int gu, int val, const int* __re
   }
 }
 
-// Column side of entry (row u, column c): v <- gf_k[u].
-__device__ __forceinline__ void emit_col(uint32_t c, int gu, int gv, const int* __restrict__ F,
+// Column side of edge entry c of a row whose gf is gu: v <- gu (kept for
+// the hub-accumulator fix-up path and for clarity; k_hook batches these).
+__device__ __forceinline__ void emit_col(uint32_t c, int gu, const int* __restrict__ F,
                                          const int* __restrict__ G, int* __restrict__ N,
                                          int* __restrict__ hub_acc) {
-  if (gu < gv) {
-    int x = (int)(c & IDMASK);
-    if (c & HUB) {
-      red_min(hub_acc + x, gu);
-    } else {
-      red_min(N + x, gu);
-      int t = ldg(F + x);
-      if (t != x && gu < ldg(G + t)) red_min(N + t, gu);
-    }
+  const int x = (int)(c & IDMASK);
+  if (c & HUB) {
+    red_min(hub_acc + x, gu);
+  } else {
+    red_min(N + x, gu);
+    int t = ldg(F + x);
+    if (t != x && gu < ldg(G + t)) red_min(N + t, gu);
   }
 }
 
+// One gathered gf value per entry: hub edges from the shared-memory table
+// (32-bit shared address, no generic conversion), everything else from
+// global through the read-only path. Both loads are predicated, no branch.
+__device__ __forceinline__ int gather_gf(uint32_t c, uint32_t s_base, const int* __restrict__ G) {
+  int v;
+  asm("{\n\t.reg .pred p;\n\t"
+      "setp.ne.u32 p, %1, 0;\n\t"
+      "@p  ld.shared.b32 %0, [%2];\n\t"
+      "@!p ld.global.nc.b32 %0, [%3];\n\t}"
+      : "=r"(v)
+      : "r"(c & HUB), "r"(s_base + (c << 2)), "l"(G + (c & IDMASK)));
+  return v;
+}
+
 // ---- phase H: hooking over the oriented layout ------------------------------
+//
+// Warp task = SPAN consecutive entries; lane l of a step owns entries
+// [8l, 8l+8). Every entry gathers one gf value: a header its row vertex's,
+// an edge its neighbour's (shared-memory hub table or global). Rows are
+// contiguous, so
+//   - the row open when a lane starts is the last header of the nearest lane
+//     to the left that has one (one shuffle), or the step carry;
+//   - row minima spanning lanes are combined by a segmented scan, and the
+//     run still open at the span end is emitted as a partial (min-atomics are
+//     idempotent, so partials need no fix-up).
+// Fast path: an edge can only emit if its gf differs from its row's gf
+// (row side needs val < gu, column side gu < val). When no entry of the step
+// differs and no carried minimum is pending, the whole step is a no-op apart
+// from carry bookkeeping — the common case once components have converged.
 
 __global__ void __launch_bounds__(HOOK_THREADS, 1) k_hook(HookArgs a) {
-  extern __shared__ int4 s_raw[];
-  int* s_hub = reinterpret_cast<int*>(s_raw);
+  extern __shared__ int s_hub[];
   if (*(volatile const int*)a.done) return;
-  {
-    const int4* src = reinterpret_cast<const int4*>(a.G_hub);
-    for (int i = threadIdx.x; i < (a.H >> 2); i += blockDim.x) s_raw[i] = src[i];
-  }
+  for (int i = threadIdx.x; i < (a.H >> 2); i += blockDim.x)
+    reinterpret_cast<int4*>(s_hub)[i] = reinterpret_cast<const int4*>(a.G_hub)[i];
   __syncthreads();
+  const uint32_t s_base = (uint32_t)__cvta_generic_to_shared(s_hub);
 
   const int* __restrict__ F = a.F;
   const int* __restrict__ G = a.G;
   int* __restrict__ N = a.N;
+  int* __restrict__ hub_acc = a.hub_acc;
   const int lane = threadIdx.x & 31;
   const unsigned lt = (1u << lane) - 1u;
   const long long nwarps = (long long)gridDim.x * (blockDim.x >> 5);
@@ -147,49 +176,106 @@ __global__ void __launch_bounds__(HOOK_THREADS, 1) k_hook(HookArgs a) {
   const uint64_t pol = policy_evict_first();
 
   for (long long s = gw; s < a.nspans; s += nwarps) {
-    int base = ldg(a.span_base + s);  // row index of the entry before this span
-    int carry = INF;                  // min of the run open at the step boundary
-    const uint4* p = reinterpret_cast<const uint4*>(a.ecol) + s * (SPAN / 4) + lane;
-    uint4 nxt = ld_stream(p, pol);
+    int carry_u = ldg(a.span_row + s);              // row open at the span start
+    int carry_gu = carry_u >= 0 ? ldg(G + carry_u) : INF;
+    int carry_run = INF;
+    const uint4* p = reinterpret_cast<const uint4*>(a.ecol + s * SPAN) + 2 * lane;
+    uint4 n0 = ld_stream(p, pol), n1 = ld_stream(p + 1, pol);
 #pragma unroll 1
     for (int st = 0; st < STEPS; ++st) {
-      const uint4 cw = nxt;
-      if (st + 1 < STEPS) nxt = ld_stream(p + (st + 1) * 32, pol);
-      const uint32_t c[EPL] = {cw.x, cw.y, cw.z, cw.w};
-      int gv[EPL];
-#pragma unroll
-      for (int j = 0; j < EPL; ++j) {
-        const int x = (int)(c[j] & IDMASK);
-        gv[j] = (c[j] & HUB) ? s_hub[x] : ldg(G + x);
+      const uint32_t c[EPL] = {n0.x, n0.y, n0.z, n0.w, n1.x, n1.y, n1.z, n1.w};
+      if (st + 1 < STEPS) {
+        n0 = ld_stream(p + (st + 1) * 64, pol);
+        n1 = ld_stream(p + (st + 1) * 64 + 1, pol);
       }
-      int excl = 0, total = 0;
+      int val[EPL];
 #pragma unroll
-      for (int j = 0; j < EPL; ++j) {
-        const unsigned b = __ballot_sync(0xffffffffu, c[j] & HEAD);
-        excl += __popc(b & lt);
-        total += __popc(b);
-      }
-      int ridx = base + excl;  // row of the entries before this lane's first head
-      int cu = -1, cgu = INF;
-      if (ridx >= 0) { cu = ldg(a.nzrows + ridx); cgu = ldg(G + cu); }
-      int run = INF, pre = INF, fu = -1, fgu = INF;
-      bool seen = false;
+      for (int j = 0; j < EPL; ++j) val[j] = gather_gf(c[j], s_base, G);
+      // last header of this lane
+      int lu = -1, lgu = INF;
 #pragma unroll
-      for (int j = 0; j < EPL; ++j) {
-        if (c[j] & HEAD) {
-          if (!seen) { pre = run; seen = true; fu = cu; fgu = cgu; }
-          else emit_row(cu, cgu, run, F, G, N);   // run closed inside the lane
-          ++ridx;
-          cu = ldg(a.nzrows + ridx);
-          cgu = ldg(G + cu);
-          run = gv[j];
-        } else {
-          run = min(run, gv[j]);
+      for (int j = 0; j < EPL; ++j)
+        if ((int)c[j] < 0) { lu = (int)(c[j] & IDMASK); lgu = val[j]; }
+      const unsigned hb = __ballot_sync(0xffffffffu, lu >= 0);
+      const unsigned left = hb & lt;
+      const int src = left ? 31 - __clz(left) : lane;
+      int in_u = __shfl_sync(0xffffffffu, lu, src);
+      int in_gu = __shfl_sync(0xffffffffu, lgu, src);
+      if (!left) { in_u = carry_u; in_gu = carry_gu; }
+      // does any entry differ from its row's gf?
+      bool need = false;
+      {
+        int rg = in_gu;
+#pragma unroll
+        for (int j = 0; j < EPL; ++j) {
+          rg = ((int)c[j] < 0) ? val[j] : rg;
+          need |= (val[j] != rg);
         }
-        emit_col(c[j], cgu, gv[j], F, G, N, a.hub_acc);
       }
-      // segmented inclusive scan of (seen, run) across lanes: the min of the
-      // run that is open at the end of each lane
+      if (!__any_sync(0xffffffffu, need) && carry_run >= carry_gu) {
+        if (hb) {
+          const int last = 31 - __clz(hb);
+          carry_u = __shfl_sync(0xffffffffu, lu, last);
+          carry_gu = __shfl_sync(0xffffffffu, lgu, last);
+          carry_run = INF;
+        }
+        continue;
+      }
+      // ---- slow path ------------------------------------------------------
+      // One emission slot per entry, filled branch-free:
+      //   header j: closes the row before it (the lane's first header closes
+      //             the row entering the lane; handled after the scan)
+      //             target = previous row vertex, value = its run min,
+      //             threshold = its gf
+      //   edge j:   column side, target = v (or hub slot), value = row gf,
+      //             threshold = gf[v]
+      // then every active slot does N[target] <-min value and the stochastic
+      // N[F[target]] <-min value, with all loads of the lane in flight together.
+      int cu = in_u, cgu = in_gu, run = INF, pre = INF;
+      bool seen = false;
+      unsigned act = 0, hubm = 0;
+      int w[EPL], y[EPL];
+#pragma unroll
+      for (int j = 0; j < EPL; ++j) {
+        const bool h = (int)c[j] < 0;
+        const bool first = h && !seen;
+        pre = first ? run : pre;
+        const int yj = h ? run : cgu;
+        const int gj = h ? cgu : val[j];
+        w[j] = h ? cu : (int)(c[j] & IDMASK);
+        y[j] = yj;
+        act |= ((yj < gj) && !first ? 1u : 0u) << j;
+        hubm |= (!h && (c[j] & HUB) ? 1u : 0u) << j;
+        seen |= h;
+        cu = h ? (int)(c[j] & IDMASK) : cu;
+        cgu = h ? val[j] : cgu;
+        run = h ? INF : min(run, val[j]);
+      }
+      if (act) {
+        int t[EPL];
+#pragma unroll
+        for (int j = 0; j < EPL; ++j) {
+          t[j] = -1;
+          if ((act >> j) & 1u) {
+            if ((hubm >> j) & 1u) {
+              red_min(hub_acc + w[j], y[j]);
+            } else {
+              red_min(N + w[j], y[j]);
+              t[j] = ldg(F + w[j]);
+            }
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < EPL; ++j) {
+          if (t[j] == w[j]) t[j] = -1;
+          if (t[j] >= 0) val[j] = ldg(G + t[j]);
+        }
+#pragma unroll
+        for (int j = 0; j < EPL; ++j)
+          if (t[j] >= 0 && y[j] < val[j]) red_min(N + t[j], y[j]);
+      }
+      // segmented inclusive scan of (seen, run): min of the run open at the
+      // end of each lane
       int sv = run, sf = seen ? 1 : 0;
 #pragma unroll
       for (int off = 1; off < 32; off <<= 1) {
@@ -199,19 +285,22 @@ __global__ void __launch_bounds__(HOOK_THREADS, 1) k_hook(HookArgs a) {
       }
       const int ev = __shfl_up_sync(0xffffffffu, sv, 1);
       const int ef = __shfl_up_sync(0xffffffffu, sf, 1);
-      const int cin = (lane == 0) ? carry : (ef ? ev : min(ev, carry));
-      if (seen) emit_row(fu, fgu, min(cin, pre), F, G, N);  // run entering the lane closes here
+      const int cin = (lane == 0) ? carry_run : (ef ? ev : min(ev, carry_run));
+      if (seen) {
+        const int v = min(cin, pre);
+        if (v < in_gu) emit_row(in_u, in_gu, v, F, G, N);  // row entering the lane closes here
+      }
       const int lv = __shfl_sync(0xffffffffu, sv, 31);
       const int lf = __shfl_sync(0xffffffffu, sf, 31);
-      carry = lf ? lv : min(lv, carry);
-      base += total;
+      carry_run = lf ? lv : min(lv, carry_run);
+      if (hb) {
+        const int last = 31 - __clz(hb);
+        carry_u = __shfl_sync(0xffffffffu, lu, last);
+        carry_gu = __shfl_sync(0xffffffffu, lgu, last);
+      }
     }
-    // the run still open at the span end is a partial minimum of row `base`;
-    // min-atomics are idempotent, so partials need no fix-up
-    if (lane == 0 && carry < INF) {
-      const int u = ldg(a.nzrows + base);
-      emit_row(u, ldg(G + u), carry, F, G, N);
-    }
+    // the run still open at the span end: partial minimum of row carry_u
+    if (lane == 0 && carry_run < carry_gu) emit_row(carry_u, carry_gu, carry_run, F, G, N);
   }
 }
 
@@ -231,11 +320,14 @@ __global__ void k_hubfix(int* __restrict__ hub_acc, const int* __restrict__ hub_
 }
 
 // ---- counters + convergence flag --------------------------------------------
+// Each block writes its five partial counts; the last block to finish (ticket)
+// sums them, stores this iteration's counters and raises the convergence flag
+// when gf did not change. No same-address atomics besides the ticket.
 
 template <int NT>
-__device__ __forceinline__ void finish_counters(const unsigned (&c)[5], unsigned long long* cnt,
-                                                unsigned int* ticket, int* done, int iter,
-                                                int max_iter) {
+__device__ __forceinline__ void finish_counters(const unsigned (&c)[5], unsigned* partials,
+                                                unsigned long long* cnt, unsigned int* ticket,
+                                                int* done, int iter, int max_iter) {
   __shared__ unsigned s_part[NT / 32][5];
   __shared__ bool s_last;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -246,9 +338,9 @@ __device__ __forceinline__ void finish_counters(const unsigned (&c)[5], unsigned
   }
   __syncthreads();
   if (threadIdx.x < 5) {
-    unsigned long long sum = 0;
+    unsigned sum = 0;
     for (int i = 0; i < NT / 32; ++i) sum += s_part[i][threadIdx.x];
-    if (sum) atomicAdd(cnt + threadIdx.x, sum);
+    partials[(size_t)blockIdx.x * 8 + threadIdx.x] = sum;
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -257,16 +349,51 @@ __device__ __forceinline__ void finish_counters(const unsigned (&c)[5], unsigned
     s_last = (t == gridDim.x - 1);
   }
   __syncthreads();
-  if (s_last && threadIdx.x == 0) {
-    __threadfence();
-    const unsigned long long gfc = atomicAdd(cnt + C_GF, 0ull);
-    if (gfc == 0ull) atomicExch(done, iter);
-    else if (max_iter > 0 && iter >= max_iter) atomicExch(done, -iter);
-    *ticket = 0u;
+  if (!s_last) return;
+  __threadfence();
+  unsigned long long acc[5] = {0ull, 0ull, 0ull, 0ull, 0ull};
+  for (unsigned b = threadIdx.x; b < gridDim.x; b += NT) {
+#pragma unroll
+    for (int k = 0; k < 5; ++k) acc[k] += __ldcg(partials + (size_t)b * 8 + k);
   }
+  __shared__ unsigned long long s_acc[NT / 32][5];
+#pragma unroll
+  for (int k = 0; k < 5; ++k) {
+    unsigned long long v = acc[k];
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) s_acc[w][k] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < 5) {
+    unsigned long long sum = 0;
+    for (int i = 0; i < NT / 32; ++i) sum += s_acc[i][threadIdx.x];
+    cnt[threadIdx.x] = sum;
+    if (threadIdx.x == C_GF) {
+      if (sum == 0ull) atomicExch(done, iter);
+      else if (max_iter > 0 && iter >= max_iter) atomicExch(done, -iter);
+    }
+  }
+  if (threadIdx.x == 0) *ticket = 0u;
 }
 
 // ---- phase G: grandparents, counters, next N init ---------------------------
+
+__device__ __forceinline__ void shortcut_group(long long i, const int4* N4, const int* __restrict__ N,
+                                               int4* F4, int4* G4, unsigned (&c)[5]) {
+  const int4 nu = N4[i];
+  const int4 go = G4[i];
+  const int4 fo = F4[i];
+  int4 gg;
+  gg.x = ldg(N + nu.x); gg.y = ldg(N + nu.y); gg.z = ldg(N + nu.z); gg.w = ldg(N + nu.w);
+  const int u = (int)(i << 2);
+  c[C_GF] += (gg.x != go.x) + (gg.y != go.y) + (gg.z != go.z) + (gg.w != go.w);
+  c[C_F] += (nu.x != fo.x) + (nu.y != fo.y) + (nu.z != fo.z) + (nu.w != fo.w);
+  c[C_NONSTAR] += (gg.x != nu.x) + (gg.y != nu.y) + (gg.z != nu.z) + (gg.w != nu.w);
+  c[C_ROOTS] += (nu.x == u) + (nu.y == u + 1) + (nu.z == u + 2) + (nu.w == u + 3);
+  c[C_VIOL] += (nu.x > fo.x) + (nu.y > fo.y) + (nu.z > fo.z) + (nu.w > fo.w);
+  G4[i] = gg;
+  F4[i] = gg;
+}
 
 __global__ void __launch_bounds__(SC_THREADS) k_shortcut(ShortcutArgs a) {
   if (*(volatile const int*)a.done) return;
@@ -278,21 +405,12 @@ __global__ void __launch_bounds__(SC_THREADS) k_shortcut(ShortcutArgs a) {
   int4* F4 = reinterpret_cast<int4*>(a.F);
   int4* G4 = reinterpret_cast<int4*>(a.G);
   const int4* N4 = reinterpret_cast<const int4*>(a.N);
-  for (long long i = t0; i < n4; i += stride) {
-    const int4 nu = N4[i];
-    const int4 go = G4[i];
-    const int4 fo = F4[i];
-    int4 gg;
-    gg.x = ldg(N + nu.x); gg.y = ldg(N + nu.y); gg.z = ldg(N + nu.z); gg.w = ldg(N + nu.w);
-    const int u = (int)(i << 2);
-    c[C_GF] += (gg.x != go.x) + (gg.y != go.y) + (gg.z != go.z) + (gg.w != go.w);
-    c[C_F] += (nu.x != fo.x) + (nu.y != fo.y) + (nu.z != fo.z) + (nu.w != fo.w);
-    c[C_NONSTAR] += (gg.x != nu.x) + (gg.y != nu.y) + (gg.z != nu.z) + (gg.w != nu.w);
-    c[C_ROOTS] += (nu.x == u) + (nu.y == u + 1) + (nu.z == u + 2) + (nu.w == u + 3);
-    c[C_VIOL] += (nu.x > fo.x) + (nu.y > fo.y) + (nu.z > fo.z) + (nu.w > fo.w);
-    G4[i] = gg;
-    F4[i] = gg;
+  long long i = t0;
+  for (; i + stride < n4; i += 2 * stride) {   // two independent groups in flight
+    shortcut_group(i, N4, N, F4, G4, c);
+    shortcut_group(i + stride, N4, N, F4, G4, c);
   }
+  if (i < n4) shortcut_group(i, N4, N, F4, G4, c);
   for (long long u = (n4 << 2) + t0; u < a.n; u += stride) {
     const int nu = N[u], go = a.G[u], fo = a.F[u];
     const int gg = ldg(N + nu);
@@ -304,7 +422,7 @@ __global__ void __launch_bounds__(SC_THREADS) k_shortcut(ShortcutArgs a) {
     const int h = ldg(a.hub_id + s);
     a.G_hub[s] = ldg(N + ldg(N + h));
   }
-  finish_counters<SC_THREADS>(c, a.cnt, a.ticket, a.done, a.iter, a.max_iter);
+  finish_counters<SC_THREADS>(c, a.partials, a.cnt, a.ticket, a.done, a.iter, a.max_iter);
 }
 
 // ---- iteration 1 in closed form ---------------------------------------------
@@ -313,7 +431,8 @@ __global__ void __launch_bounds__(SC_THREADS) k_shortcut(ShortcutArgs a) {
 __global__ void __launch_bounds__(SC_THREADS) k_first(const int* __restrict__ f1, int* Y, int* G,
                                                       int* X, long long n, const int* __restrict__ hub_id,
                                                       int* G_hub, int H, unsigned long long* cnt,
-                                                      unsigned int* ticket, int* done, int max_iter) {
+                                                      unsigned* partials, unsigned int* ticket,
+                                                      int* done, int max_iter) {
   unsigned c[5] = {0u, 0u, 0u, 0u, 0u};
   const long long stride = (long long)gridDim.x * blockDim.x;
   const long long t0 = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -344,7 +463,7 @@ __global__ void __launch_bounds__(SC_THREADS) k_first(const int* __restrict__ f1
     const int h = ldg(hub_id + s);
     G_hub[s] = ldg(f1 + ldg(f1 + h));
   }
-  finish_counters<SC_THREADS>(c, cnt, ticket, done, 1, max_iter);
+  finish_counters<SC_THREADS>(c, partials, cnt, ticket, done, 1, max_iter);
 }
 
 // ---- solve-start initialisation ----------------------------------------------
