@@ -1,0 +1,111 @@
+"""numpy emulation of the device schedule (test-only).
+
+Mirrors what libfastsv.so does, step for step, so the host-side partition
+logic and the collective semantics can be tested on CPU:
+
+  layout     each undirected edge {a, b} kept once, in the row of the endpoint
+             with the smaller (degree, id) key (k_orient_count/k_orient_write)
+  iteration 1  f1[u] = min(u, smallest neighbour) from each rank's own rows,
+             assembled with an allreduce-min (k_f1 + ncclAllReduce)
+  iteration k>=2 on every rank, over its own oriented entries (k_hook):
+             row side    run-min of gf over the row  -> N[u], N[F[u]]
+             column side gf[row]                     -> N[v], N[F[v]]
+             each filtered by "value < gf_k[target]"; then allreduce-min of N
+             (ncclAllReduce ncclMin) and the replicated vertex pass
+             gf' = N[N] (k_shortcut) with the gf-stability stop rule.
+
+``allreduce_min`` is injected so the same code runs single-process (identity)
+or across gloo ranks (torch.distributed.all_reduce with ReduceOp.MIN).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+INF = np.iinfo(np.int32).max
+
+
+def oriented_entries(n, offsets, cols, row_begin, row_end):
+    """(rows, cols) of the oriented entries owned by rows [row_begin, row_end)."""
+    offsets = np.asarray(offsets, dtype=np.int64)
+    deg = np.diff(offsets)
+    lo, hi = offsets[row_begin], offsets[row_end]
+    rows = np.repeat(np.arange(row_begin, row_end, dtype=np.int64), deg[row_begin:row_end])
+    c = np.asarray(cols, dtype=np.int64)[lo:hi] if cols.size else np.zeros(0, np.int64)
+    key_r = deg[rows] * (n + 1) + rows
+    key_c = deg[c] * (n + 1) + c
+    keep = key_r < key_c
+    return rows[keep], c[keep]
+
+
+def first_parents(n, offsets, cols, row_begin, row_end):
+    """Partial f1 (INF outside the rank's rows)."""
+    offsets = np.asarray(offsets, dtype=np.int64)
+    f1 = np.full(n, INF, dtype=np.int64)
+    u = np.arange(row_begin, row_end, dtype=np.int64)
+    f1[u] = u
+    nz = u[offsets[u + 1] > offsets[u]]
+    if nz.size:
+        f1[nz] = np.minimum(nz, np.asarray(cols, dtype=np.int64)[offsets[nz]])
+    return f1
+
+
+def _scatter_min(target, idx, vals):
+    if idx.size:
+        np.minimum.at(target, idx, vals)
+
+
+def hook(rows, cols, F, G, N):
+    """One rank's phase H over its oriented entries (N modified in place)."""
+    if rows.size == 0:
+        return
+    gv = G[cols]
+    gu = G[rows]
+    # row side: per-row minimum of gv (rows are sorted)
+    starts = np.flatnonzero(np.r_[True, rows[1:] != rows[:-1]])
+    rmin = np.minimum.reduceat(gv, starts)
+    ru = rows[starts]
+    ok = rmin < G[ru]
+    u, val = ru[ok], rmin[ok]
+    _scatter_min(N, u, val)
+    t = F[u]
+    ok2 = (t != u) & (val < G[t])
+    _scatter_min(N, t[ok2], val[ok2])
+    # column side: v <- gf[row]
+    ok = gu < gv
+    v, val = cols[ok], gu[ok]
+    _scatter_min(N, v, val)
+    t = F[v]
+    ok2 = (t != v) & (val < G[t])
+    _scatter_min(N, t[ok2], val[ok2])
+
+
+def run(n, offsets, cols, row_begin=0, row_end=None, allreduce_min=lambda a: a,
+        cap=4096, record=True):
+    """Returns (labels, iterations, gf_changed, f_changed, snapshots)."""
+    row_end = n if row_end is None else row_end
+    rows, ocols = oriented_entries(n, offsets, cols, row_begin, row_end)
+    f1 = allreduce_min(first_parents(n, offsets, cols, row_begin, row_end))
+    F = f1.copy()                        # f_1
+    G = f1[f1]                           # gf_1
+    ident = np.arange(n, dtype=np.int64)
+    gfc = [int(np.count_nonzero(G != ident))]
+    fc = [int(np.count_nonzero(F != ident))]
+    snaps = [F.copy()] if record else None
+    it = 1
+    while gfc[-1] != 0 and it < cap:
+        it += 1
+        N = G.copy()                     # f_k initialised to gf_{k-1} (shortcut folded)
+        hook(rows, ocols, F, G, N)
+        N = allreduce_min(N)
+        G2 = N[N]
+        gfc.append(int(np.count_nonzero(G2 != G)))
+        fc.append(int(np.count_nonzero(N != F)))
+        if np.any(N > F):
+            raise AssertionError("parent increased")
+        F, G = N, G2
+        if record:
+            snaps.append(F.copy())
+    if n and not np.array_equal(F[F], F):
+        raise AssertionError("non-star at exit")
+    return F, it, gfc, fc, snaps

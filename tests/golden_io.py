@@ -1,0 +1,46 @@
+"""Accessors for the reference-produced golden vectors (tests/golden/)."""
+
+import json
+from dataclasses import dataclass
+from pathlib import Path
+
+import numpy as np
+
+GOLDEN = Path(__file__).resolve().parent / "golden"
+
+
+@dataclass
+class GoldenCase:
+    name: str
+    n: int
+    m_dir: int
+    edges: np.ndarray          # raw int32 pairs (k, 2)
+    iterations: int
+    gf_changed: list
+    f_changed: list
+    labels: np.ndarray         # int32
+    snapshots: np.ndarray      # (iterations, n) int32
+
+
+def load_suite():
+    d = np.load(GOLDEN / "suite.npz", allow_pickle=False)
+    out = []
+    for i, name in enumerate(d["names"]):
+        n = int(d["n"][i])
+        e = d["edges"][d["edge_off"][i]:d["edge_off"][i + 1]].reshape(-1, 2)
+        t0, t1 = d["trace_off"][i], d["trace_off"][i + 1]
+        it = int(d["iterations"][i])
+        lab_off = int(d["n"][:i].sum())
+        s0, s1 = d["snap_off"][i], d["snap_off"][i + 1]
+        out.append(GoldenCase(str(name), n, int(d["m_dir"][i]), e, it,
+                              d["gf_changed"][t0:t1].tolist(), d["f_changed"][t0:t1].tolist(),
+                              d["labels"][lab_off:lab_off + n], d["snapshots"][s0:s1].reshape(it, n)))
+    return out
+
+
+def load_configs():
+    return {int(k): v for k, v in json.loads((GOLDEN / "configs.json").read_text()).items()}
+
+
+def load_kats():
+    return json.loads((GOLDEN / "kats.json").read_text())

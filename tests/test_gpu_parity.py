@@ -1,5 +1,6 @@
-"""GPU parity: the sm_100a path through the C ABI against the CPU oracle
-(itself pinned to the reference's golden vectors in test_oracle.py).
+"""GPU parity: the sm_100a path through the C ABI against the reference's
+golden vectors (tests/golden/, produced by the reference itself) and the CPU
+oracle (pinned to the same vectors in test_oracle.py).
 
 Bar: bit-exact labels, iteration count, gf_changed and f_changed traces and
 every per-iteration parent vector (snapshot)."""
@@ -11,15 +12,20 @@ import oracle
 import paper_1910_05971_b200 as fb
 from paper_1910_05971_b200 import generators as gen
 from conftest import random_multigraph
+from golden_io import load_configs, load_kats, load_suite
 
 pytestmark = pytest.mark.gpu
 
 
-def check_against_oracle(solver, n, pairs, snapshots=True, hub_slots=0):
-    g = fb.build_csr(n, pairs)
+def solve(solver, g, snapshots=True, hub_slots=0, batch=0):
     solver.set_hub_slots(hub_slots)
     solver.upload(g)
-    labels, iters, gfc, fc, ms, snaps = solver.run(snapshots=snapshots, snap_cap=512)
+    return solver.run(snapshots=snapshots, snap_cap=512, batch=batch)
+
+
+def check_against_oracle(solver, n, pairs, snapshots=True, hub_slots=0, batch=0):
+    g = fb.build_csr(n, pairs)
+    labels, iters, gfc, fc, ms, snaps = solve(solver, g, snapshots, hub_slots, batch)
     o = oracle.fastsv_csr(n, g.row_offsets, g.col_indices, snapshots=snapshots)
     assert iters == o.iterations
     assert gfc.tolist() == o.gf_changed.tolist()
@@ -31,6 +37,27 @@ def check_against_oracle(solver, n, pairs, snapshots=True, hub_slots=0):
     return g, labels, iters
 
 
+@pytest.mark.parametrize("hub_slots", [0, -1, 256])
+def test_golden_suite_snapshots(solver, hub_slots):
+    for c in load_suite():
+        g = fb.build_csr(c.n, c.edges)
+        labels, iters, gfc, fc, ms, snaps = solve(solver, g, True, hub_slots)
+        assert iters == c.iterations, c.name
+        assert gfc.tolist() == c.gf_changed and fc.tolist() == c.f_changed, c.name
+        assert np.array_equal(labels, c.labels), c.name
+        assert np.array_equal(snaps, c.snapshots), c.name
+
+
+def test_golden_suite_no_snapshots_batches(solver):
+    # the speculative batched loop (no host sync per iteration) gives the same trace
+    for c in load_suite()[::5]:
+        g = fb.build_csr(c.n, c.edges)
+        for batch in (1, 2, 8):
+            labels, iters, gfc, fc, ms, _ = solve(solver, g, False, 0, batch)
+            assert iters == c.iterations and gfc.tolist() == c.gf_changed, (c.name, batch)
+            assert np.array_equal(labels, c.labels), (c.name, batch)
+
+
 def test_random_multigraphs_snapshots(solver):
     rng = np.random.default_rng(71)
     for _ in range(200):
@@ -38,46 +65,82 @@ def test_random_multigraphs_snapshots(solver):
         check_against_oracle(solver, n, pairs)
 
 
-def test_random_with_forced_hubs(solver):
-    # hub table forced on small graphs: every column-side path (hub / non-hub)
+def test_skewed_graphs_with_hub_table(solver):
     rng = np.random.default_rng(72)
-    for _ in range(100):
+    for _ in range(60):
         n = int(rng.integers(300, 3000))
         k = int(rng.integers(n, 20 * n))
-        # skewed endpoints so some vertices pass the hub degree threshold
         u = (rng.pareto(1.2, k) * 3).astype(np.int64) % n
         v = rng.integers(0, n, k)
         pairs = np.stack([u, v], 1).astype(np.int32)
-        check_against_oracle(solver, n, pairs, snapshots=True, hub_slots=0)
+        check_against_oracle(solver, n, pairs, snapshots=True, hub_slots=int(rng.choice([0, 256, 1024])))
 
 
 def test_edge_cases(solver):
     for n, pairs in [(1, []), (2, []), (5, [(0, 0), (1, 1)]), (2, [(0, 1)]), (3, [(2, 1)]),
                      (6, [(0, 1), (1, 2), (0, 2), (3, 4), (4, 5), (3, 5)]),
                      (64, [(i, i + 1) for i in range(63)]),
-                     (10, [(0, i) for i in range(1, 10)])]:
+                     (10, [(0, i) for i in range(1, 10)]),
+                     (4099, [(i, i + 1) for i in range(4098)]),      # spans cross span/step borders
+                     (3000, [(0, i) for i in range(1, 3000)])]:      # one long row
         p = np.asarray(pairs, dtype=np.int32).reshape(-1, 2)
         check_against_oracle(solver, n, p)
 
 
-def test_two_triangles_labels():
+def test_empty_graph_runs_one_iteration():
+    r = fb.fastsv_la(fb.build_csr(0, []))
+    assert r.iterations == 1 and r.labeling.component_count == 0
+
+
+def test_public_api_matches_reference_kats():
+    k = load_kats()
     r = fb.fastsv_la(fb.build_csr(6, [(0, 1), (1, 2), (0, 2), (3, 4), (4, 5), (3, 5)]))
-    assert r.labeling.labels.tolist() == [0, 0, 0, 3, 3, 3]
-
-
-def test_star10_two_iterations():
+    assert r.labeling.labels.tolist() == k["two_triangles"]["labels"]
+    assert r.labeling.labels.dtype == np.int64
     r = fb.fastsv(fb.build_csr(10, [(0, i) for i in range(1, 10)]))
-    assert r.iterations == 2
-    assert r.labeling.labels.tolist() == [0] * 10
+    assert r.iterations == k["star10"]["iterations"]
+    r = fb.fastsv_la(fb.build_csr(64, [(i, i + 1) for i in range(63)]), record_snapshots=True)
+    assert r.iterations == k["path64_fastsv"]["iterations"] == len(r.snapshots)
+    assert all(not s.flags.writeable for s in r.snapshots)
+    assert r.trace[-1].gf_changed == 0 and all(t.gf_changed > 0 for t in r.trace[:-1])
+    assert r.total_elapsed > 0
 
 
-@pytest.mark.parametrize("scale", [12, 16])
-def test_rmat_small(solver, scale):
-    n, pairs = gen.rmat(scale, 16, seed=3)
-    check_against_oracle(solver, n, pairs, snapshots=True)
+def test_reference_style_int64_csr_is_accepted():
+    # a CsrGraph exactly like svcc's (int64 columns) goes through fsv_upload_csr64
+    n, e = gen.rmat(10, 8, seed=4)
+    g = fb.build_csr(n, e)
+    g64 = fb.CsrGraph(n=n, row_offsets=g.row_offsets, col_indices=g.col_indices.astype(np.int64))
+    a = fb.fastsv_la(g)
+    b = fb.fastsv_la(g64)
+    assert a.iterations == b.iterations and np.array_equal(a.labeling.labels, b.labeling.labels)
 
 
-def test_config1_full(solver):
-    n, pairs = gen.baseline_graph(1)
-    g, labels, iters = check_against_oracle(solver, n, pairs, snapshots=False)
-    assert np.array_equal(labels, oracle.uf_labels(n, pairs))
+def test_connected_components_edge_list():
+    n, e = gen.forest(500, 1, 64, 2, seed=8)
+    labels = fb.connected_components(n, e)
+    assert np.array_equal(labels, oracle.uf_labels(n, e).astype(np.int64))
+
+
+def test_upload_rejects_out_of_range_columns(solver):
+    off = np.array([0, 1, 2], dtype=np.int64)
+    cols = np.array([1, 7], dtype=np.int32)
+    with pytest.raises(fb.InputError, match="out of range for n=2"):
+        solver.upload(fb.CsrGraph(n=2, row_offsets=off, col_indices=cols))
+
+
+@pytest.mark.parametrize("index", [1, 2, 3, 4])
+def test_baseline_config_full_size(solver, index):
+    rec = load_configs()[index]
+    n, pairs = gen.baseline_graph(index)
+    assert gen.pairs_digest(pairs) == rec["pairs_digest"]
+    g = fb.build_csr(n, pairs)
+    solver.set_hub_slots(0)
+    solver.upload(g)
+    labels, iters, gfc, fc, ms, _ = solver.run()
+    assert iters == rec["iterations"]
+    assert gfc.tolist() == rec["gf_changed"] and fc.tolist() == rec["f_changed"]
+    assert gen.pairs_digest(labels) == rec["labels_digest"]
+    assert solver.stats.component_count == rec["component_count"]
+    if index == 1:
+        assert np.array_equal(labels, oracle.uf_labels(n, pairs))
