@@ -44,7 +44,14 @@ typedef struct fsv_config {
   int32_t max_iters;  /* 0 = run to convergence (the reference has no cap) */
   int32_t batch;      /* iterations queued per host convergence check; 0 = auto */
   int32_t profile;    /* 1 = bracket each kernel with CUDA events (fills *_ms) */
-  int32_t reserved[5];
+  /* product choice per iteration, svcc.choose_kernel (driver.py:51-61):
+   * 0 = reference default (auto, threshold 0.1), 1 = dense only,
+   * 2 = sparse only, 3 = auto with `sparse_threshold`. A sparse iteration
+   * pushes only the vertices whose gf changed (SpMSpV, kernels.py:71-102);
+   * results are identical either way, only the trace's kernel/flops differ. */
+  int32_t sparse_policy;
+  double sparse_threshold;  /* double: the rule must round like Python's 0.1 * n */
+  int32_t reserved[2];
 } fsv_config;
 
 /* Result summary of the last solve. */
@@ -60,8 +67,9 @@ typedef struct fsv_stats {
   float solve_ms;           /* device time, first kernel to convergence flag */
   /* profile = 1 only: summed device time of the kernels of the iterations
    * that ran (speculative launches past convergence excluded) */
-  float hook_ms, hubfix_ms, shortcut_ms, first_ms, allreduce_ms;
+  float hook_ms, hubfix_ms, shortcut_ms, first_ms, allreduce_ms, push_ms;
   int32_t hook_launches;
+  int32_t sparse_iterations;  /* iterations that ran the sparse push */
 } fsv_stats;
 
 const char* fsv_last_error(void);
@@ -109,6 +117,11 @@ int fsv_get_labels(fsv_ctx* ctx, int32_t* labels);
 int fsv_get_labels64(fsv_ctx* ctx, int64_t* labels);
 int fsv_get_trace(fsv_ctx* ctx, int64_t* gf_changed, int64_t* f_changed,
                   float* elapsed_ms, int32_t cap);
+/* Same plus the product kind per iteration (0 dense, 1 sparse) and its
+ * flops (dense: m_dir; sparse: degree sum of the pushed vertices), the
+ * IterationTrace.kernel / .flops fields (algorithms.py:38-45). */
+int fsv_get_trace_ex(fsv_ctx* ctx, int64_t* gf_changed, int64_t* f_changed,
+                     float* elapsed_ms, int32_t* kernel, int64_t* flops, int32_t cap);
 
 /* One call: solve + labels + iteration count + trace (the fastsv_la shape). */
 int fsv_run(fsv_ctx* ctx, const fsv_config* cfg, int32_t* labels,

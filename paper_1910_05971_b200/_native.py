@@ -20,7 +20,8 @@ FSV_OK, FSV_ERR_INPUT, FSV_ERR_CONTRACT, FSV_ERR_INVARIANT, FSV_ERR_RUNTIME = 0,
 
 
 class FsvConfig(ctypes.Structure):
-    _fields_ = [("max_iters", c_int32), ("batch", c_int32), ("profile", c_int32), ("reserved", c_int32 * 5)]
+    _fields_ = [("max_iters", c_int32), ("batch", c_int32), ("profile", c_int32),
+                ("sparse_policy", c_int32), ("sparse_threshold", c_double), ("reserved", c_int32 * 2)]
 
 
 class FsvStats(ctypes.Structure):
@@ -28,7 +29,8 @@ class FsvStats(ctypes.Structure):
                 ("m_dir", c_int64), ("oriented_entries", c_int64), ("hub_slots", c_int32),
                 ("host_syncs", c_int32), ("kernel_launches", c_int32), ("solve_ms", c_float),
                 ("hook_ms", c_float), ("hubfix_ms", c_float), ("shortcut_ms", c_float),
-                ("first_ms", c_float), ("allreduce_ms", c_float), ("hook_launches", c_int32)]
+                ("first_ms", c_float), ("allreduce_ms", c_float), ("push_ms", c_float),
+                ("hook_launches", c_int32), ("sparse_iterations", c_int32)]
 
 
 # symbol -> (restype, argtypes); mirrors include/fastsv.h one to one
@@ -46,6 +48,7 @@ FASTSV_SYMBOLS = {
     "fsv_get_labels": (c_int, [c_void_p, c_void_p]),
     "fsv_get_labels64": (c_int, [c_void_p, c_void_p]),
     "fsv_get_trace": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_int32]),
+    "fsv_get_trace_ex": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int32]),
     "fsv_run": (c_int, [c_void_p, POINTER(FsvConfig), c_void_p, POINTER(c_int32), c_void_p,
                         c_void_p, c_int32]),
     "fsv_run_snapshots": (c_int, [c_void_p, POINTER(FsvConfig), c_void_p, POINTER(c_int32),

@@ -107,19 +107,26 @@ static int nccl_load() {
 // ---------------------------------------------------------------------------
 // device buffer helper
 
+// Device buffer that only reallocates when it must grow (uploads of
+// successive graphs reuse the same memory; cudaFree synchronises the device).
 template <typename T>
 struct DBuf {
   T* p = nullptr;
-  size_t n = 0;
+  size_t n = 0;    // elements requested by the last alloc
+  size_t cap = 0;  // elements allocated
   cudaError_t alloc(size_t count) {
+    n = count;
+    if (p && count <= cap) return cudaSuccess;
     free();
     n = count;
-    return cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T));
+    cap = std::max<size_t>(count, 1);
+    return cudaMalloc(&p, cap * sizeof(T));
   }
   void free() {
     if (p) cudaFree(p);
     p = nullptr;
     n = 0;
+    cap = 0;
   }
   ~DBuf() { free(); }
 };
@@ -127,7 +134,6 @@ struct DBuf {
 static constexpr int kHubMax = 49152;     // 192 KB of shared memory
 static constexpr int kHubMinDegree = 32;  // below this a hub slot buys nothing
 static constexpr int kTraceCap = 4096;    // iteration cap of the counter array
-static constexpr int kScBlocksPerSm = 16; // vertex-pass grid cap (blocks of 512)
 
 struct fsv_ctx {
   int device = 0;
@@ -140,6 +146,25 @@ struct fsv_ctx {
   int R = 0, H = 0;
   DBuf<uint32_t> ecol;
   DBuf<int> span_row, hub_id, f1;
+  // full symmetric CSR of this rank's rows, for sparse (push) iterations
+  DBuf<int64_t> csr_off;
+  DBuf<int> csr_cols;
+  int64_t col_base = 0, row_begin = 0, row_end = 0;
+  // changed-gf lists of the vertex pass (one region per warp)
+  DBuf<int> dlist, dcount, mode;
+  DBuf<int2> chunks;
+  DBuf<PushDesc> pdesc;
+  DBuf<long long> pbtotal;
+  // upload workspace (grow-only, reused across uploads)
+  struct {
+    DBuf<unsigned long long> bad;
+    DBuf<int> deg, ids, deg_sorted, ids_sorted, slot_of, nzflag, nzidx, nzrows;
+    DBuf<long long> cnt, out_off, nzoff;
+    DBuf<unsigned char> tmp;
+    DBuf<int64_t> cols64;
+  } ws;
+  long long rcap = 0;
+  int dgrid = 1;
   // solve state
   DBuf<int> X, Y, G, G_hub, hub_acc, done;
   DBuf<unsigned long long> cnt;
@@ -150,8 +175,11 @@ struct fsv_ctx {
   // profile mode: events around every kernel of iteration k: [k][0..7]
   std::vector<cudaEvent_t> pev;
   bool profile = false;
-  float hook_ms = 0, hubfix_ms = 0, shortcut_ms = 0, first_ms = 0, allreduce_ms = 0;
+  float hook_ms = 0, hubfix_ms = 0, shortcut_ms = 0, first_ms = 0, allreduce_ms = 0, push_ms = 0;
   int hook_launches = 0;
+  int policy = 0;
+  double threshold = 0.1;
+  std::vector<int> h_mode;
   // results of the last solve
   int iterations = 0;
   int components = 0;
@@ -374,11 +402,24 @@ __global__ void k_f1(const int64_t* __restrict__ off, const ColT* __restrict__ c
   }
 }
 
+__global__ void k_narrow(const int64_t* __restrict__ in, long long m, int* __restrict__ out) {
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < m;
+       e += (long long)gridDim.x * blockDim.x)
+    out[e] = (int)in[e];
+}
+
 static int grid_for(fsv_ctx* c, long long work, int threads, int per_sm = 8) {
   long long g = (work + threads - 1) / threads;
   g = std::min<long long>(g, (long long)c->sm_count * per_sm);
   return (int)std::max<long long>(g, 1);
 }
+
+template <typename ColT>
+static DBuf<ColT>& cols_buffer(fsv_ctx* c);
+template <>
+DBuf<int32_t>& cols_buffer<int32_t>(fsv_ctx* c) { return c->csr_cols; }
+template <>
+DBuf<int64_t>& cols_buffer<int64_t>(fsv_ctx* c) { return c->ws.cols64; }
 
 template <typename ColT>
 static int upload_impl(fsv_ctx* c, int64_t n, const int64_t* h_off, const ColT* h_cols,
@@ -402,15 +443,15 @@ static int upload_impl(fsv_ctx* c, int64_t n, const int64_t* h_off, const ColT* 
   c->labels_ready = 0;
 
   const long long rows = row_end - row_begin;
-  DBuf<int64_t> d_off;
-  DBuf<ColT> d_cols;
+  DBuf<int64_t>& d_off = c->csr_off;
+  DBuf<ColT>& d_cols = cols_buffer<ColT>(c);
   CUDA_TRY(d_off.alloc((size_t)n + 1));
   CUDA_TRY(d_cols.alloc((size_t)mloc));
   CUDA_TRY(cudaMemcpyAsync(d_off.p, h_off, sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice, st));
   if (mloc) CUDA_TRY(cudaMemcpyAsync(d_cols.p, h_cols, sizeof(ColT) * mloc, cudaMemcpyHostToDevice, st));
 
   // column range check (graph.py:71-75 semantics: report an offending entry)
-  DBuf<unsigned long long> d_bad;
+  DBuf<unsigned long long>& d_bad = c->ws.bad;
   CUDA_TRY(d_bad.alloc(1));
   CUDA_TRY(cudaMemsetAsync(d_bad.p, 0xff, sizeof(unsigned long long), st));
   if (mloc) k_check_cols<ColT><<<grid_for(c, mloc, 256), 256, 0, st>>>(d_cols.p, mloc, n, d_bad.p);
@@ -426,7 +467,11 @@ static int upload_impl(fsv_ctx* c, int64_t n, const int64_t* h_off, const ColT* 
   }
 
   // degrees + hub selection (top-H by degree, stable, identical on all ranks)
-  DBuf<int> deg, ids, deg_sorted, ids_sorted, slot_of;
+  auto& deg = c->ws.deg;
+  auto& ids = c->ws.ids;
+  auto& deg_sorted = c->ws.deg_sorted;
+  auto& ids_sorted = c->ws.ids_sorted;
+  auto& slot_of = c->ws.slot_of;
   CUDA_TRY(deg.alloc(n)); CUDA_TRY(ids.alloc(n));
   CUDA_TRY(deg_sorted.alloc(n)); CUDA_TRY(ids_sorted.alloc(n)); CUDA_TRY(slot_of.alloc(n));
   if (n) k_degree<<<grid_for(c, n, 256), 256, 0, st>>>(d_off.p, n, deg.p, ids.p);
@@ -435,7 +480,7 @@ static int upload_impl(fsv_ctx* c, int64_t n, const int64_t* h_off, const ColT* 
     size_t tmp_bytes = 0;
     cub::DeviceRadixSort::SortPairsDescending(nullptr, tmp_bytes, deg.p, deg_sorted.p, ids.p,
                                               ids_sorted.p, (int)n, 0, 32, st);
-    DBuf<unsigned char> tmp;
+    auto& tmp = c->ws.tmp;
     CUDA_TRY(tmp.alloc(tmp_bytes));
     CUDA_TRY(cub::DeviceRadixSort::SortPairsDescending(tmp.p, tmp_bytes, deg.p, deg_sorted.p, ids.p,
                                                        ids_sorted.p, (int)n, 0, 32, st));
@@ -456,8 +501,10 @@ static int upload_impl(fsv_ctx* c, int64_t n, const int64_t* h_off, const ColT* 
   if (H) k_hub_slots<<<grid_for(c, H, 256), 256, 0, st>>>(ids_sorted.p, H, slot_of.p, c->hub_id.p);
 
   // orientation
-  DBuf<long long> cnt, out_off;
-  DBuf<int> nzflag, nzidx;
+  auto& cnt = c->ws.cnt;
+  auto& out_off = c->ws.out_off;
+  auto& nzflag = c->ws.nzflag;
+  auto& nzidx = c->ws.nzidx;
   CUDA_TRY(cnt.alloc(rows + 1)); CUDA_TRY(out_off.alloc(rows + 1));
   CUDA_TRY(nzflag.alloc(rows + 1)); CUDA_TRY(nzidx.alloc(rows + 1));
   CUDA_TRY(cudaMemsetAsync(cnt.p + rows, 0, sizeof(long long), st));
@@ -469,7 +516,7 @@ static int upload_impl(fsv_ctx* c, int64_t n, const int64_t* h_off, const ColT* 
     size_t b1 = 0, b2 = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, b1, cnt.p, out_off.p, (int)(rows + 1), st);
     cub::DeviceScan::ExclusiveSum(nullptr, b2, nzflag.p, nzidx.p, (int)(rows + 1), st);
-    DBuf<unsigned char> tmp;
+    auto& tmp = c->ws.tmp;
     CUDA_TRY(tmp.alloc(std::max(b1, b2)));
     CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp.p, b1, cnt.p, out_off.p, (int)(rows + 1), st));
     CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp.p, b2, nzflag.p, nzidx.p, (int)(rows + 1), st));
@@ -481,9 +528,9 @@ static int upload_impl(fsv_ctx* c, int64_t n, const int64_t* h_off, const ColT* 
   CUDA_TRY(cudaStreamSynchronize(st));
   const long long Epad = (E + SPAN - 1) / SPAN * SPAN;
   CUDA_TRY(c->ecol.alloc((size_t)std::max<long long>(Epad, 4)));
-  DBuf<int> nzrows;
+  auto& nzrows = c->ws.nzrows;
   CUDA_TRY(nzrows.alloc((size_t)R + 1));
-  DBuf<long long> nzoff;
+  auto& nzoff = c->ws.nzoff;
   CUDA_TRY(nzoff.alloc((size_t)R + 1));
   if (rows)
     k_orient_write<ColT><<<grid_for(c, rows * 32, 256, 16), 256, 0, st>>>(
@@ -505,12 +552,37 @@ static int upload_impl(fsv_ctx* c, int64_t n, const int64_t* h_off, const ColT* 
     NCCL_TRY(g_nccl.AllReduce(c->f1.p, c->f1.p, (size_t)n, ncclInt32, ncclMin, c->comm, st));
   }
 
+  // keep the rank's symmetric columns (int32) for sparse iterations
+  if constexpr (sizeof(ColT) != 4) {
+    CUDA_TRY(c->csr_cols.alloc((size_t)std::max<int64_t>(mloc, 1)));
+    if (mloc)
+      k_narrow<<<grid_for(c, mloc, 256), 256, 0, st>>>(d_cols.p, mloc, c->csr_cols.p);
+  }
+  c->col_base = e_begin;
+  c->row_begin = row_begin;
+  c->row_end = row_end;
+
   // solve buffers: n + dummy vertex, padded for 16-byte vector access
   const size_t nv = ((size_t)n + 1 + 63) / 64 * 64;
   CUDA_TRY(c->X.alloc(nv)); CUDA_TRY(c->Y.alloc(nv)); CUDA_TRY(c->G.alloc(nv));
   CUDA_TRY(c->G_hub.alloc(std::max(H, 4))); CUDA_TRY(c->hub_acc.alloc(std::max(H, 4)));
   CUDA_TRY(c->done.alloc(1)); CUDA_TRY(c->ticket.alloc(1));
   CUDA_TRY(c->partials.alloc((size_t)c->sc_grid * 8));
+  {
+    const long long want = (std::max<long long>(n / 4, 1) + SC_THREADS - 1) / SC_THREADS;
+    c->dgrid = (int)std::max<long long>(1, std::min<long long>(want, c->sc_grid));
+    const long long stride_groups = (long long)c->dgrid * SC_THREADS;
+    const long long iters = (n / 4 + stride_groups - 1) / stride_groups;
+    c->rcap = 4 * 32 * std::max<long long>(iters, 1) + 32;
+    const long long warps = (long long)c->dgrid * (SC_THREADS / 32);
+    CUDA_TRY(c->dlist.alloc((size_t)(warps * c->rcap)));
+    CUDA_TRY(c->dcount.alloc((size_t)warps));
+    CUDA_TRY(c->mode.alloc((size_t)kTraceCap + 2));
+    const long long max_batches = n / 32 + warps + 2;
+    CUDA_TRY(c->pdesc.alloc((size_t)(max_batches * 32)));
+    CUDA_TRY(c->pbtotal.alloc((size_t)max_batches));
+    CUDA_TRY(c->chunks.alloc((size_t)(mloc / PUSH_CHUNK + max_batches + 64)));
+  }
   CUDA_TRY(c->cnt.alloc((size_t)kTraceCap * NCOUNT));
   CUDA_TRY(cudaStreamSynchronize(st));
   CUDA_TRY(cudaGetLastError());
@@ -548,13 +620,22 @@ extern "C" int fsv_upload_csr64(fsv_ctx* c, int64_t n, const int64_t* off, const
 static inline int* bufF(fsv_ctx* c, int k) { return (k & 1) ? c->X.p : c->Y.p; }
 static inline int* bufN(fsv_ctx* c, int k) { return (k & 1) ? c->Y.p : c->X.p; }
 
-static constexpr int kPev = 8;  // profile events per iteration
+static constexpr int kPev = 10;  // profile events per iteration
 
 // Vertex-parallel kernels run one resident wave (grid-stride inside): their
 // end-of-block counter barrier makes extra waves expensive.
-static inline int vertex_grid(fsv_ctx* c) {
-  const long long want = (std::max<long long>(c->n / 4, c->H) + SC_THREADS - 1) / SC_THREADS;
-  return (int)std::max<long long>(1, std::min<long long>(want, c->sc_grid));
+static inline int vertex_grid(fsv_ctx* c) { return c->dgrid; }
+
+static DeltaOut delta_out(fsv_ctx* c) {
+  DeltaOut d;
+  d.list = c->dlist.p;
+  d.count = c->dcount.p;
+  d.rcap = c->rcap;
+  d.mode = c->mode.p;
+  d.policy = c->policy == 1 ? 1 : (c->policy == 2 ? 2 : 0);
+  d.threshold = c->threshold;
+  d.n_total = c->n;
+  return d;
 }
 
 static int ensure_pevents(fsv_ctx* c, size_t count) {
@@ -579,33 +660,47 @@ static int launch_iteration(fsv_ctx* c, int k, int max_iter) {
   int* F = bufF(c, k);
   int* N = bufN(c, k);
   const long long nspans = c->Epad / SPAN;
-  if (nspans) {
+  {
     HookArgs a;
     a.ecol = c->ecol.p; a.nspans = nspans; a.span_row = c->span_row.p;
     a.F = F; a.G = c->G.p; a.N = N; a.G_hub = c->G_hub.p; a.H = c->H; a.hub_acc = c->hub_acc.p;
-    a.done = c->done.p;
-    const int grid = (int)std::min<long long>(c->sm_count, (nspans + 31) / 32);
+    a.done = c->done.p; a.mode = c->mode.p; a.iter = k;
+    PushArgs& p = a.push;
+    p.list = c->dlist.p; p.count = c->dcount.p; p.rcap = c->rcap;
+    p.nregions = c->dgrid * (SC_THREADS / 32);
+    p.off = c->csr_off.p; p.cols = c->csr_cols.p; p.col_base = c->col_base;
+    p.row_begin = (int)c->row_begin; p.row_end = (int)c->row_end;
+    p.F = F; p.G = c->G.p; p.N = N; p.mode = c->mode.p; p.iter = k;
+    unsigned long long* slot = c->cnt.p + (size_t)(k - 1) * NCOUNT;
+    p.flops = slot + C_FLOPS; p.nchunks = slot + C_CHUNKS; p.nbatches = slot + C_BATCHES;
+    p.barrier = reinterpret_cast<unsigned*>(slot + C_BARRIER); p.chunks = c->chunks.p;
+    p.desc = c->pdesc.p; p.btotal = c->pbtotal.p;
+    // persistent, one CTA per SM; cooperative launch guarantees co-residency
+    // for the grid barrier of the sparse (push) path
     pmark(c, k, 0);
-    k_hook<<<std::max(grid, 1), HOOK_THREADS, c->H * sizeof(int), st>>>(a);
+    void* kargs[] = {&a};
+    CUDA_TRY(cudaLaunchCooperativeKernel((const void*)k_hook, dim3(c->sm_count), dim3(HOOK_THREADS),
+                                         kargs, (size_t)c->H * sizeof(int), st));
     pmark(c, k, 1);
     ++c->launches;
   }
   if (c->H) {
     pmark(c, k, 2);
     k_hubfix<<<grid_for(c, c->H, 256), 256, 0, st>>>(c->hub_acc.p, c->hub_id.p, c->H, F, c->G.p, N,
-                                                       c->done.p);
+                                                       c->done.p, c->mode.p, k);
     pmark(c, k, 3);
     ++c->launches;
   }
   if (c->comm && c->n) {
-    pmark(c, k, 4);
+    pmark(c, k, 8);
     NCCL_TRY(g_nccl.AllReduce(N, N, (size_t)c->n, ncclInt32, ncclMin, c->comm, st));
-    pmark(c, k, 5);
+    pmark(c, k, 9);
   }
   ShortcutArgs s;
   s.F = F; s.G = c->G.p; s.N = N; s.n = c->n; s.hub_id = c->hub_id.p; s.G_hub = c->G_hub.p;
   s.H = c->H; s.cnt = c->cnt.p + (size_t)(k - 1) * NCOUNT; s.ticket = c->ticket.p; s.done = c->done.p;
   s.partials = c->partials.p;
+  s.dl = delta_out(c);
   s.iter = k; s.max_iter = max_iter;
   pmark(c, k, 6);
   k_shortcut<<<vertex_grid(c), SC_THREADS, 0, st>>>(s);
@@ -638,17 +733,29 @@ static int solve_impl(fsv_ctx* c, const fsv_config* cfg, int32_t* snapshots, int
   c->host_syncs = 0;
   c->labels_ready = 0;
   c->profile = d.profile != 0;
-  c->hook_ms = c->hubfix_ms = c->shortcut_ms = c->first_ms = c->allreduce_ms = 0.f;
+  if (d.sparse_policy < 0 || d.sparse_policy > 3)
+    return fail(FSV_ERR_CONTRACT, "sparse_policy must be 0..3");
+  if (d.sparse_policy == 3 && !(d.sparse_threshold >= 0.0 && d.sparse_threshold <= 1.0))
+    return fail(FSV_ERR_CONTRACT, "sparse_threshold must be in [0, 1]");
+  c->policy = d.sparse_policy;
+  c->threshold = d.sparse_policy == 3 ? d.sparse_threshold : 0.1;
+  c->hook_ms = c->hubfix_ms = c->shortcut_ms = c->first_ms = c->allreduce_ms = c->push_ms = 0.f;
   c->hook_launches = 0;
   if (c->profile && (rc = ensure_pevents(c, 2 * kPev))) return rc;
 
   CUDA_TRY(cudaEventRecord(c->events[0], st));
   k_solve_init<<<grid_for(c, std::max<long long>(c->H, (long long)cap * NCOUNT), 256), 256, 0, st>>>(
       c->X.p, c->Y.p, c->G.p, c->n, c->hub_acc.p, c->H, c->cnt.p, (long long)cap * NCOUNT, c->done.p,
-      c->ticket.p);
+      c->ticket.p, c->mode.p, c->policy == 2 ? 1 : 0);
   pmark(c, 1, 6);
-  k_first<<<vertex_grid(c), SC_THREADS, 0, st>>>(c->f1.p, c->Y.p, c->G.p, c->X.p, c->n, c->hub_id.p, c->G_hub.p, c->H, c->cnt.p,
-                  c->partials.p, c->ticket.p, c->done.p, cap);
+  {
+    FirstArgs fa;
+    fa.f1 = c->f1.p; fa.Y = c->Y.p; fa.G = c->G.p; fa.X = c->X.p; fa.n = c->n;
+    fa.hub_id = c->hub_id.p; fa.G_hub = c->G_hub.p; fa.H = c->H; fa.cnt = c->cnt.p;
+    fa.partials = c->partials.p; fa.ticket = c->ticket.p; fa.done = c->done.p; fa.max_iter = cap;
+    fa.dl = delta_out(c);
+    k_first<<<vertex_grid(c), SC_THREADS, 0, st>>>(fa);
+  }
   pmark(c, 1, 7);
   c->launches += 2;
   if ((rc = ensure_events(c, 2))) return rc;
@@ -657,13 +764,14 @@ static int solve_impl(fsv_ctx* c, const fsv_config* cfg, int32_t* snapshots, int
     if (snap_cap < 1) return fail(FSV_ERR_CONTRACT, "snapshot capacity exhausted");
     if ((rc = copy_snapshot(c, 1, snapshots))) return rc;
   }
-  int launched = 1;  // iterations queued so far
+  int launched = 1;  // iterations queued so far (k_first is iteration 1)
   int done = 0;
+  bool first_round = true;
   for (;;) {
-    if (snapshots || launched > 1 || true) {
-      // read the flag after the first batch too: iteration 1 may already converge
-    }
-    const int upto = std::min(cap, launched + (launched == 1 && !snapshots ? batch - 1 : batch));
+    // the first round also holds iteration 1, so it queues batch-1 more
+    const int more = first_round ? batch - 1 : batch;
+    first_round = false;
+    const int upto = std::min(cap, launched + more);
     for (int k = launched + 1; k <= upto; ++k) {
       if ((rc = launch_iteration(c, k, cap))) return rc;
       if ((rc = ensure_events(c, (size_t)k + 1))) return rc;
@@ -694,6 +802,8 @@ static int solve_impl(fsv_ctx* c, const fsv_config* cfg, int32_t* snapshots, int
   c->h_cnt.assign((size_t)iters * NCOUNT, 0ull);
   CUDA_TRY(cudaMemcpy(c->h_cnt.data(), c->cnt.p, sizeof(unsigned long long) * iters * NCOUNT,
                       cudaMemcpyDeviceToHost));
+  c->h_mode.assign((size_t)iters + 1, 0);
+  CUDA_TRY(cudaMemcpy(c->h_mode.data(), c->mode.p, sizeof(int) * (iters + 1), cudaMemcpyDeviceToHost));
   c->iter_ms.assign(iters, 0.f);
   for (int k = 1; k <= iters; ++k)
     CUDA_TRY(cudaEventElapsedTime(&c->iter_ms[k - 1], c->events[k - 1], c->events[k]));
@@ -706,9 +816,15 @@ static int solve_impl(fsv_ctx* c, const fsv_config* cfg, int32_t* snapshots, int
     };
     c->first_ms = span(1, 6, 7);
     for (int k = 2; k <= iters; ++k) {
-      if (c->Epad) { c->hook_ms += span(k, 0, 1); ++c->hook_launches; }
+      const float hk = span(k, 0, 1);
+      if (c->h_mode[k] == 0) {
+        c->hook_ms += hk;
+        ++c->hook_launches;
+      } else {
+        c->push_ms += hk;
+      }
       if (c->H) c->hubfix_ms += span(k, 2, 3);
-      if (c->comm && c->n) c->allreduce_ms += span(k, 4, 5);
+      if (c->comm && c->n) c->allreduce_ms += span(k, 8, 9);
       c->shortcut_ms += span(k, 6, 7);
     }
   }
@@ -739,7 +855,11 @@ static void fill_stats(fsv_ctx* c, fsv_stats* s) {
   s->shortcut_ms = c->shortcut_ms;
   s->first_ms = c->first_ms;
   s->allreduce_ms = c->allreduce_ms;
+  s->push_ms = c->push_ms;
   s->hook_launches = c->hook_launches;
+  int sp = 0;
+  for (int k = 2; k <= c->iterations && k < (int)c->h_mode.size(); ++k) sp += c->h_mode[k] == 1;
+  s->sparse_iterations = sp;
 }
 
 extern "C" int fsv_solve(fsv_ctx* c, const fsv_config* cfg, fsv_stats* stats) {
@@ -775,6 +895,23 @@ extern "C" int fsv_get_trace(fsv_ctx* c, int64_t* gfc, int64_t* fc, float* ms, i
     if (gfc) gfc[i] = (int64_t)c->h_cnt[(size_t)i * NCOUNT + C_GF];
     if (fc) fc[i] = (int64_t)c->h_cnt[(size_t)i * NCOUNT + C_F];
     if (ms) ms[i] = c->iter_ms[(size_t)i];
+  }
+  return FSV_OK;
+}
+
+extern "C" int fsv_get_trace_ex(fsv_ctx* c, int64_t* gfc, int64_t* fc, float* ms, int32_t* kernel,
+                                int64_t* flops, int32_t cap) {
+  int rc = fsv_get_trace(c, gfc, fc, ms, cap);
+  if (rc) return rc;
+  const int k = std::min(cap, c->iterations);
+  for (int i = 0; i < k; ++i) {
+    const int md = (i + 1 < (int)c->h_mode.size()) ? c->h_mode[(size_t)i + 1] : 0;
+    if (kernel) kernel[i] = md;
+    if (flops) {
+      // dense product: m_dir (kernels.py:67-68); sparse: pushed degree sum
+      // (kernels.py:94,102); iteration 1 sparse pushes the whole vector = m_dir
+      flops[i] = (md == 1 && i > 0) ? (int64_t)c->h_cnt[(size_t)i * NCOUNT + C_FLOPS] : c->m_dir;
+    }
   }
   return FSV_OK;
 }
@@ -832,3 +969,10 @@ extern "C" int fsv_nccl_attach(fsv_ctx* c, const void* id128, int nranks, int ra
   c->rank = rank;
   return FSV_OK;
 }
+
+#ifdef FSV_DEBUG_TIMING
+extern "C" int fsv_debug_timing(unsigned long long* out, int count) {
+  CUDA_TRY(cudaMemcpyFromSymbol(out, fsv::g_dbg_t, sizeof(unsigned long long) * count));
+  return FSV_OK;
+}
+#endif

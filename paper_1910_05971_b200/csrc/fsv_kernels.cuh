@@ -30,6 +30,19 @@
 
 namespace fsv {
 
+#ifdef FSV_DEBUG_TIMING
+// dev-only phase timestamps of the sparse path: [block][0..3]
+__device__ unsigned long long g_dbg_t[1024 * 4];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define DBG_T(slot) do { if (threadIdx.x == 0) g_dbg_t[blockIdx.x * 4 + (slot)] = gtimer(); } while (0)
+#else
+#define DBG_T(slot) do { } while (0)
+#endif
+
 constexpr int INF = 0x7fffffff;
 // Oriented layout entry codes (uint32):
 //   header  HDR | u          first entry of the row of vertex u
@@ -43,8 +56,9 @@ constexpr int STEPS = 4;                 // steps per span
 constexpr int SPAN = STEP * STEPS;       // entries per warp task
 constexpr int HOOK_THREADS = 768;
 constexpr int SC_THREADS = 512;
-constexpr int NCOUNT = 8;                // counters per iteration
-enum { C_GF = 0, C_F = 1, C_NONSTAR = 2, C_ROOTS = 3, C_VIOL = 4 };
+constexpr int NCOUNT = 16;               // counter slots per iteration
+enum { C_GF = 0, C_F = 1, C_NONSTAR = 2, C_ROOTS = 3, C_VIOL = 4,   // vertex-pass counters
+       C_FLOPS = 5, C_CHUNKS = 6, C_BATCHES = 7, C_BARRIER = 8 };     // push bookkeeping
 
 // ---- memory helpers -------------------------------------------------------
 
@@ -71,6 +85,40 @@ __device__ __forceinline__ void red_min(int* p, int v) {
 
 // ---- argument blocks --------------------------------------------------------
 
+// Sparse iteration (push). Phase 1 turns the delta list into batches of 32
+// vertices (descriptor per vertex: row start, exclusive prefix of degrees
+// within the batch, gf) and cuts each batch's flattened entry range into
+// PUSH_CHUNK-entry chunks; phase 2 (after a grid barrier) processes chunks.
+struct PushDesc {
+  long long start;   // first column index of the row (rank-local)
+  long long excl;    // entries of the batch before this vertex
+  int val;           // gf[v] pushed to every neighbour
+  int pad;
+};
+
+struct PushArgs {
+  const int* list;        // delta regions of the previous vertex pass
+  const int* count;
+  long long rcap;
+  int nregions;
+  const int64_t* off;     // full symmetric CSR offsets (n+1)
+  const int* cols;        // columns of rows [row_begin, row_end)
+  long long col_base;     // off[row_begin]
+  int row_begin, row_end;
+  const int* F;
+  const int* G;
+  int* N;
+  const int* mode;        // mode[iter]
+  int iter;
+  unsigned long long* flops;    // this iteration's pushed-entry count
+  unsigned long long* nchunks;  // chunk list length
+  unsigned long long* nbatches; // batch count
+  PushDesc* desc;               // [batch][32]
+  long long* btotal;            // entries per batch
+  int2* chunks;                 // (batch, first flattened entry)
+  unsigned* barrier;            // grid barrier counter of this iteration
+};
+
 struct HookArgs {
   const uint32_t* ecol;   // oriented entries (headers + edges), padded to SPAN
   long long nspans;
@@ -82,6 +130,24 @@ struct HookArgs {
   int H;                  // hub slots (multiple of 4)
   int* hub_acc;           // column-side minima aimed at hubs
   const int* done;        // convergence flag (iteration number, 0 = running)
+  const int* mode;        // mode[iter]: 0 dense pull (this layout), 1 sparse push
+  int iter;
+  PushArgs push;
+};
+
+// Changed-gf ("delta") list written by the vertex pass: warp w owns
+// list[w*rcap, w*rcap + count[w]) so no global atomics are needed.
+// policy: 0 auto (sparse iff gf_changed < threshold*n, driver.py:51-61),
+// 1 dense only, 2 sparse only. mode[k] (k = 1-based iteration) is written by
+// the last block of iteration k-1: 0 dense product, 1 sparse push.
+struct DeltaOut {
+  int* list;
+  int* count;
+  long long rcap;
+  int* mode;
+  int policy;
+  double threshold;
+  long long n_total;      // global vertex count for the threshold rule
 };
 
 struct ShortcutArgs {
@@ -98,6 +164,7 @@ struct ShortcutArgs {
   int* done;
   int iter;               // 1-based iteration number
   int max_iter;           // stop flag raised when reached without converging
+  DeltaOut dl;            // changed-gf list for a following sparse iteration
 };
 
 // ---- emission of one hook contribution -------------------------------------
@@ -141,6 +208,119 @@ __device__ __forceinline__ int gather_gf(uint32_t c, uint32_t s_base, const int*
   return v;
 }
 
+// ---- sparse iteration: push over the changed-gf list --------------------------
+// Iteration k >= 2 only needs the directed entries (u -> v) with gf[v]
+// changed in iteration k-1: every other contribution is dominated by the
+// previous iteration's aggressive hook (f_{k-1}[u] <= min_{v in N(u)} gf_{k-2}[v],
+// and gf[F[u]] <= f_{k-1}[u]). So v pushes gf[v] to each neighbour u of the
+// symmetric CSR: N[u] <-min, N[F[u]] <-min, with the usual filters. This is
+// the reference's SpMSpV (kernels.py:71-102) without the mngf accumulator.
+
+
+constexpr int PUSH_CHUNK = 256;  // entries per chunk (8 per lane)
+
+// Phase 1: one warp per delta region, batches of 32 vertices.
+__device__ __forceinline__ void push_plan(const PushArgs& a) {
+  const int lane = threadIdx.x & 31;
+  const long long nw = (long long)gridDim.x * (blockDim.x >> 5);
+  unsigned long long work = 0;
+  for (long long r = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < a.nregions;
+       r += nw) {
+    const int cnt = a.count[r];
+    const int* reg = a.list + r * a.rcap;
+    for (int b = 0; b < cnt; b += 32) {
+      long long deg = 0, start = 0;
+      int gv = INF;
+      if (b + lane < cnt) {
+        const int v = reg[b + lane];
+        if (v >= a.row_begin && v < a.row_end) {
+          start = a.off[v] - a.col_base;
+          deg = a.off[v + 1] - a.off[v];
+          gv = ldg(a.G + v);
+        }
+      }
+      long long incl = deg;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const long long y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      const long long T = __shfl_sync(0xffffffffu, incl, 31);
+      if (T == 0) continue;
+      work += (unsigned long long)T;
+      unsigned long long bid = 0;
+      const long long nck = (T + PUSH_CHUNK - 1) / PUSH_CHUNK;
+      unsigned long long cbase = 0;
+      if (lane == 0) {
+        bid = atomicAdd(a.nbatches, 1ull);
+        cbase = atomicAdd(a.nchunks, (unsigned long long)nck);
+      }
+      bid = __shfl_sync(0xffffffffu, bid, 0);
+      cbase = __shfl_sync(0xffffffffu, cbase, 0);
+      PushDesc d;
+      d.start = start; d.excl = incl - deg; d.val = gv; d.pad = 0;
+      a.desc[bid * 32 + lane] = d;
+      if (lane == 0) a.btotal[bid] = T;
+      for (long long q = lane; q < nck; q += 32)
+        a.chunks[cbase + q] = make_int2((int)bid, (int)(q * PUSH_CHUNK));
+    }
+  }
+  if (lane == 0 && work) atomicAdd(a.flops, work);  // lane-uniform
+}
+
+// Phase 2: one warp per chunk; 8 entries per lane with every load batched
+// (columns, gf of the neighbours, then parents and their gf for the ones
+// that pass the filter) so each lane keeps 8 independent requests in flight.
+__device__ __forceinline__ void push_run(const PushArgs& a, long long* w_start, long long* w_excl,
+                                         int* w_val) {
+  const int lane = threadIdx.x & 31;
+  const unsigned long long total = *(volatile unsigned long long*)a.nchunks;
+  const long long nw = (long long)gridDim.x * (blockDim.x >> 5);
+  constexpr int PER = PUSH_CHUNK / 32;
+  for (long long q = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+       q < (long long)total; q += nw) {
+    const int2 ck = a.chunks[q];
+    const PushDesc d = a.desc[(long long)ck.x * 32 + lane];
+    w_start[lane] = d.start;
+    w_excl[lane] = d.excl;
+    w_val[lane] = d.val;
+    const long long T = a.btotal[ck.x];
+    const long long hi = min(T, (long long)ck.y + PUSH_CHUNK);
+    __syncwarp();
+    int u[PER], val[PER], t[PER], gt[PER];
+    int o = 0;
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {
+      const long long e = (long long)ck.y + lane + 32 * j;
+      u[j] = -1;
+      if (e < hi) {
+        while (o < 31 && w_excl[o + 1] <= e) ++o;   // owner of entry e (monotone)
+        u[j] = ldg(a.cols + w_start[o] + (e - w_excl[o]));
+        val[j] = w_val[o];
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < PER; ++j) gt[j] = u[j] >= 0 ? ldg(a.G + u[j]) : INF;
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {
+      t[j] = -1;
+      if (u[j] >= 0 && val[j] < gt[j]) {
+        red_min(a.N + u[j], val[j]);
+        t[j] = ldg(a.F + u[j]);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {
+      if (t[j] == u[j]) t[j] = -1;
+      gt[j] = t[j] >= 0 ? ldg(a.G + t[j]) : INF;
+    }
+#pragma unroll
+    for (int j = 0; j < PER; ++j)
+      if (t[j] >= 0 && val[j] < gt[j]) red_min(a.N + t[j], val[j]);
+    __syncwarp();
+  }
+}
+
 // ---- phase H: hooking over the oriented layout ------------------------------
 //
 // Warp task = SPAN consecutive entries; lane l of a step owns entries
@@ -160,6 +340,32 @@ __device__ __forceinline__ int gather_gf(uint32_t c, uint32_t s_base, const int*
 __global__ void __launch_bounds__(HOOK_THREADS, 1) k_hook(HookArgs a) {
   extern __shared__ int s_hub[];
   if (*(volatile const int*)a.done) return;
+  if (a.mode[a.iter] == 1) {
+    // sparse iteration: push from the vertices whose gf changed
+    __shared__ long long s_start[HOOK_THREADS];
+    __shared__ long long s_excl[HOOK_THREADS];
+    __shared__ int s_val[HOOK_THREADS];
+    const int wib = threadIdx.x >> 5;
+    DBG_T(0);
+    push_plan(a.push);
+    // grid barrier: every CTA is resident (one persistent CTA per SM)
+    __syncthreads();
+    DBG_T(1);
+    if (threadIdx.x == 0) {
+      __threadfence();
+      atomicAdd(a.push.barrier, 1u);
+      while (*(volatile unsigned*)a.push.barrier < gridDim.x) __nanosleep(64);
+      __threadfence();
+    }
+    __syncthreads();
+    DBG_T(2);
+    push_run(a.push, s_start + wib * 32, s_excl + wib * 32, s_val + wib * 32);
+#ifdef FSV_DEBUG_TIMING
+    __syncthreads();
+    DBG_T(3);
+#endif
+    return;
+  }
   for (int i = threadIdx.x; i < (a.H >> 2); i += blockDim.x)
     reinterpret_cast<int4*>(s_hub)[i] = reinterpret_cast<const int4*>(a.G_hub)[i];
   __syncthreads();
@@ -308,8 +514,9 @@ __global__ void __launch_bounds__(HOOK_THREADS, 1) k_hook(HookArgs a) {
 
 __global__ void k_hubfix(int* __restrict__ hub_acc, const int* __restrict__ hub_id, int H,
                          const int* __restrict__ F, const int* __restrict__ G, int* __restrict__ N,
-                         const int* done) {
+                         const int* done, const int* mode, int iter) {
   if (*(volatile const int*)done) return;
+  if (mode[iter] != 0) return;
   for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < H; s += gridDim.x * blockDim.x) {
     const int acc = hub_acc[s];
     if (acc == INF) continue;
@@ -327,7 +534,8 @@ __global__ void k_hubfix(int* __restrict__ hub_acc, const int* __restrict__ hub_
 template <int NT>
 __device__ __forceinline__ void finish_counters(const unsigned (&c)[5], unsigned* partials,
                                                 unsigned long long* cnt, unsigned int* ticket,
-                                                int* done, int iter, int max_iter) {
+                                                int* done, int iter, int max_iter,
+                                                const DeltaOut& dl) {
   __shared__ unsigned s_part[NT / 32][5];
   __shared__ bool s_last;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -371,6 +579,11 @@ __device__ __forceinline__ void finish_counters(const unsigned (&c)[5], unsigned
     if (threadIdx.x == C_GF) {
       if (sum == 0ull) atomicExch(done, iter);
       else if (max_iter > 0 && iter >= max_iter) atomicExch(done, -iter);
+      // product choice for the next iteration (choose_kernel, driver.py:51-61)
+      int m = 0;
+      if (dl.policy == 2) m = 1;
+      else if (dl.policy == 0) m = ((double)sum < dl.threshold * (double)dl.n_total) ? 1 : 0;
+      dl.mode[iter + 1] = m;
     }
   }
   if (threadIdx.x == 0) *ticket = 0u;
@@ -378,21 +591,64 @@ __device__ __forceinline__ void finish_counters(const unsigned (&c)[5], unsigned
 
 // ---- phase G: grandparents, counters, next N init ---------------------------
 
-__device__ __forceinline__ void shortcut_group(long long i, const int4* N4, const int* __restrict__ N,
-                                               int4* F4, int4* G4, unsigned (&c)[5]) {
-  const int4 nu = N4[i];
-  const int4 go = G4[i];
-  const int4 fo = F4[i];
-  int4 gg;
-  gg.x = ldg(N + nu.x); gg.y = ldg(N + nu.y); gg.z = ldg(N + nu.z); gg.w = ldg(N + nu.w);
-  const int u = (int)(i << 2);
-  c[C_GF] += (gg.x != go.x) + (gg.y != go.y) + (gg.z != go.z) + (gg.w != go.w);
-  c[C_F] += (nu.x != fo.x) + (nu.y != fo.y) + (nu.z != fo.z) + (nu.w != fo.w);
-  c[C_NONSTAR] += (gg.x != nu.x) + (gg.y != nu.y) + (gg.z != nu.z) + (gg.w != nu.w);
-  c[C_ROOTS] += (nu.x == u) + (nu.y == u + 1) + (nu.z == u + 2) + (nu.w == u + 3);
-  c[C_VIOL] += (nu.x > fo.x) + (nu.y > fo.y) + (nu.z > fo.z) + (nu.w > fo.w);
-  G4[i] = gg;
-  F4[i] = gg;
+// Append the vertices u0+j (j < 4, bit j of m4) to this warp's delta region.
+__device__ __forceinline__ void delta_append(unsigned m4, int u0, int* region, int& wo) {
+  const unsigned lt = (1u << (threadIdx.x & 31)) - 1u;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const bool on = (m4 >> j) & 1u;
+    const unsigned b = __ballot_sync(0xffffffffu, on);
+    if (on) region[wo + __popc(b & lt)] = u0 + j;
+    wo += __popc(b);
+  }
+}
+
+// Vertex pass of iteration k >= 2 over groups of 4 consecutive vertices
+// (int4 index i): gf' = N[N], counters, next N init, delta append. Loads of
+// both groups a thread owns are issued before any store or ballot so their
+// latencies overlap. `valid` = false lanes only take part in the ballots.
+struct SGroup {
+  int4 nu, go, fo, gg;
+};
+
+__device__ __forceinline__ void sgroup_load(bool valid, long long i, const int4* N4,
+                                            const int* __restrict__ N, const int4* F4,
+                                            const int4* G4, SGroup& g) {
+  if (valid) {
+    g.nu = N4[i];
+    g.go = G4[i];
+    g.fo = F4[i];
+    g.gg.x = ldg(N + g.nu.x); g.gg.y = ldg(N + g.nu.y);
+    g.gg.z = ldg(N + g.nu.z); g.gg.w = ldg(N + g.nu.w);
+  }
+}
+
+__device__ __forceinline__ void sgroup_commit(bool valid, long long i, const SGroup& g, int4* F4,
+                                              int4* G4, unsigned (&c)[5], int* region, int& wo) {
+  unsigned m4 = 0;
+  if (valid) {
+    const int u = (int)(i << 2);
+    const int4 nu = g.nu, go = g.go, fo = g.fo, gg = g.gg;
+    c[C_GF] += (gg.x != go.x) + (gg.y != go.y) + (gg.z != go.z) + (gg.w != go.w);
+    c[C_F] += (nu.x != fo.x) + (nu.y != fo.y) + (nu.z != fo.z) + (nu.w != fo.w);
+    c[C_NONSTAR] += (gg.x != nu.x) + (gg.y != nu.y) + (gg.z != nu.z) + (gg.w != nu.w);
+    c[C_ROOTS] += (nu.x == u) + (nu.y == u + 1) + (nu.z == u + 2) + (nu.w == u + 3);
+    c[C_VIOL] += (nu.x > fo.x) + (nu.y > fo.y) + (nu.z > fo.z) + (nu.w > fo.w);
+    G4[i] = gg;
+    F4[i] = gg;
+    m4 = (gg.x != go.x) | ((gg.y != go.y) << 1) | ((gg.z != go.z) << 2) | ((gg.w != go.w) << 3);
+  }
+  delta_append(m4, (int)(i << 2), region, wo);
+}
+
+// Scalar tail (n % 4 vertices), run by warp 0 lanes 0..2 after the vector part.
+template <typename Fn>
+__device__ __forceinline__ void tail_append(long long n4, long long n, Fn&& one, int* region, int& wo) {
+  const long long u = (n4 << 2) + (threadIdx.x & 31);
+  const bool ch = (u < n) ? one(u) : false;
+  const unsigned b = __ballot_sync(0xffffffffu, ch);
+  if (ch) region[wo + __popc(b & ((1u << (threadIdx.x & 31)) - 1u))] = (int)u;
+  wo += __popc(b);
 }
 
 __global__ void __launch_bounds__(SC_THREADS) k_shortcut(ShortcutArgs a) {
@@ -400,75 +656,113 @@ __global__ void __launch_bounds__(SC_THREADS) k_shortcut(ShortcutArgs a) {
   unsigned c[5] = {0u, 0u, 0u, 0u, 0u};
   const long long stride = (long long)gridDim.x * blockDim.x;
   const long long t0 = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
   const long long n4 = a.n >> 2;
   const int* __restrict__ N = a.N;
   int4* F4 = reinterpret_cast<int4*>(a.F);
   int4* G4 = reinterpret_cast<int4*>(a.G);
   const int4* N4 = reinterpret_cast<const int4*>(a.N);
-  long long i = t0;
-  for (; i + stride < n4; i += 2 * stride) {   // two independent groups in flight
-    shortcut_group(i, N4, N, F4, G4, c);
-    shortcut_group(i + stride, N4, N, F4, G4, c);
+  // warp gw handles groups [wb, wb+32) of every stride: its delta region is private
+  const long long gwarp = t0 >> 5;
+  int* region = a.dl.list + gwarp * a.dl.rcap;
+  int wo = 0;
+  for (long long wb = t0 - lane; wb < n4; wb += 2 * stride) {   // warp-uniform bound
+    const long long i0 = wb + lane, i1 = wb + stride + lane;     // two groups in flight
+    SGroup g0, g1;
+    sgroup_load(i0 < n4, i0, N4, N, F4, G4, g0);
+    sgroup_load(i1 < n4, i1, N4, N, F4, G4, g1);
+    sgroup_commit(i0 < n4, i0, g0, F4, G4, c, region, wo);
+    sgroup_commit(i1 < n4, i1, g1, F4, G4, c, region, wo);
   }
-  if (i < n4) shortcut_group(i, N4, N, F4, G4, c);
-  for (long long u = (n4 << 2) + t0; u < a.n; u += stride) {
-    const int nu = N[u], go = a.G[u], fo = a.F[u];
-    const int gg = ldg(N + nu);
-    c[C_GF] += gg != go; c[C_F] += nu != fo; c[C_NONSTAR] += gg != nu;
-    c[C_ROOTS] += nu == (int)u; c[C_VIOL] += nu > fo;
-    a.G[u] = gg; a.F[u] = gg;
-  }
+  if (gwarp == 0)
+    tail_append(n4, a.n, [&](long long u) {
+      const int nu = N[u], go = a.G[u], fo = a.F[u];
+      const int gg = ldg(N + nu);
+      c[C_GF] += gg != go; c[C_F] += nu != fo; c[C_NONSTAR] += gg != nu;
+      c[C_ROOTS] += nu == (int)u; c[C_VIOL] += nu > fo;
+      a.G[u] = gg; a.F[u] = gg;
+      return gg != go;
+    }, region, wo);
+  if (lane == 0) a.dl.count[gwarp] = wo;
   for (long long s = t0; s < a.H; s += stride) {
     const int h = ldg(a.hub_id + s);
     a.G_hub[s] = ldg(N + ldg(N + h));
   }
-  finish_counters<SC_THREADS>(c, a.partials, a.cnt, a.ticket, a.done, a.iter, a.max_iter);
+  finish_counters<SC_THREADS>(c, a.partials, a.cnt, a.ticket, a.done, a.iter, a.max_iter, a.dl);
 }
 
 // ---- iteration 1 in closed form ---------------------------------------------
 // f_1[u] = min(u, min neighbour) = f1[u]; gf_1 = f1[f1]. Writes Y = f_1,
 // G = gf_1 and X = gf_1 (the N init of iteration 2).
-__global__ void __launch_bounds__(SC_THREADS) k_first(const int* __restrict__ f1, int* Y, int* G,
-                                                      int* X, long long n, const int* __restrict__ hub_id,
-                                                      int* G_hub, int H, unsigned long long* cnt,
-                                                      unsigned* partials, unsigned int* ticket,
-                                                      int* done, int max_iter) {
+struct FirstArgs {
+  const int* f1;
+  int* Y;
+  int* G;
+  int* X;
+  long long n;
+  const int* hub_id;
+  int* G_hub;
+  int H;
+  unsigned long long* cnt;
+  unsigned* partials;
+  unsigned int* ticket;
+  int* done;
+  int max_iter;
+  DeltaOut dl;
+};
+
+__global__ void __launch_bounds__(SC_THREADS) k_first(FirstArgs a) {
   unsigned c[5] = {0u, 0u, 0u, 0u, 0u};
   const long long stride = (long long)gridDim.x * blockDim.x;
   const long long t0 = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  const long long n4 = n >> 2;
+  const int lane = threadIdx.x & 31;
+  const long long n4 = a.n >> 2;
+  const int* __restrict__ f1 = a.f1;
   const int4* f14 = reinterpret_cast<const int4*>(f1);
-  for (long long i = t0; i < n4; i += stride) {
-    const int4 a = f14[i];
-    int4 gg;
-    gg.x = ldg(f1 + a.x); gg.y = ldg(f1 + a.y); gg.z = ldg(f1 + a.z); gg.w = ldg(f1 + a.w);
-    const int u = (int)(i << 2);
-    c[C_GF] += (gg.x != u) + (gg.y != u + 1) + (gg.z != u + 2) + (gg.w != u + 3);
-    c[C_F] += (a.x != u) + (a.y != u + 1) + (a.z != u + 2) + (a.w != u + 3);
-    c[C_NONSTAR] += (gg.x != a.x) + (gg.y != a.y) + (gg.z != a.z) + (gg.w != a.w);
-    c[C_ROOTS] += (a.x == u) + (a.y == u + 1) + (a.z == u + 2) + (a.w == u + 3);
-    c[C_VIOL] += (a.x > u) + (a.y > u + 1) + (a.z > u + 2) + (a.w > u + 3);
-    reinterpret_cast<int4*>(Y)[i] = a;
-    reinterpret_cast<int4*>(G)[i] = gg;
-    reinterpret_cast<int4*>(X)[i] = gg;
+  const long long gwarp = t0 >> 5;
+  int* region = a.dl.list + gwarp * a.dl.rcap;
+  int wo = 0;
+  for (long long wb = t0 - lane; wb < n4; wb += stride) {
+    const long long i = wb + lane;
+    unsigned m4 = 0;
+    if (i < n4) {
+      const int4 f = f14[i];
+      int4 gg;
+      gg.x = ldg(f1 + f.x); gg.y = ldg(f1 + f.y); gg.z = ldg(f1 + f.z); gg.w = ldg(f1 + f.w);
+      const int u = (int)(i << 2);
+      c[C_GF] += (gg.x != u) + (gg.y != u + 1) + (gg.z != u + 2) + (gg.w != u + 3);
+      c[C_F] += (f.x != u) + (f.y != u + 1) + (f.z != u + 2) + (f.w != u + 3);
+      c[C_NONSTAR] += (gg.x != f.x) + (gg.y != f.y) + (gg.z != f.z) + (gg.w != f.w);
+      c[C_ROOTS] += (f.x == u) + (f.y == u + 1) + (f.z == u + 2) + (f.w == u + 3);
+      c[C_VIOL] += (f.x > u) + (f.y > u + 1) + (f.z > u + 2) + (f.w > u + 3);
+      reinterpret_cast<int4*>(a.Y)[i] = f;
+      reinterpret_cast<int4*>(a.G)[i] = gg;
+      reinterpret_cast<int4*>(a.X)[i] = gg;
+      m4 = (gg.x != u) | ((gg.y != u + 1) << 1) | ((gg.z != u + 2) << 2) | ((gg.w != u + 3) << 3);
+    }
+    delta_append(m4, (int)(i << 2), region, wo);
   }
-  for (long long u = (n4 << 2) + t0; u < n; u += stride) {
-    const int a = f1[u];
-    const int gg = ldg(f1 + a);
-    c[C_GF] += gg != (int)u; c[C_F] += a != (int)u; c[C_NONSTAR] += gg != a;
-    c[C_ROOTS] += a == (int)u; c[C_VIOL] += a > (int)u;
-    Y[u] = a; G[u] = gg; X[u] = gg;
+  if (gwarp == 0)
+    tail_append(n4, a.n, [&](long long u) {
+      const int f = f1[u];
+      const int gg = ldg(f1 + f);
+      c[C_GF] += gg != (int)u; c[C_F] += f != (int)u; c[C_NONSTAR] += gg != f;
+      c[C_ROOTS] += f == (int)u; c[C_VIOL] += f > (int)u;
+      a.Y[u] = f; a.G[u] = gg; a.X[u] = gg;
+      return gg != (int)u;
+    }, region, wo);
+  if (lane == 0) a.dl.count[gwarp] = wo;
+  for (long long s = t0; s < a.H; s += stride) {
+    const int h = ldg(a.hub_id + s);
+    a.G_hub[s] = ldg(f1 + ldg(f1 + h));
   }
-  for (long long s = t0; s < H; s += stride) {
-    const int h = ldg(hub_id + s);
-    G_hub[s] = ldg(f1 + ldg(f1 + h));
-  }
-  finish_counters<SC_THREADS>(c, partials, cnt, ticket, done, 1, max_iter);
+  finish_counters<SC_THREADS>(c, a.partials, a.cnt, a.ticket, a.done, 1, a.max_iter, a.dl);
 }
 
 // ---- solve-start initialisation ----------------------------------------------
 __global__ void k_solve_init(int* X, int* Y, int* G, long long n, int* hub_acc, int H,
-                             unsigned long long* cnt, long long ncnt, int* done, unsigned* ticket) {
+                             unsigned long long* cnt, long long ncnt, int* done, unsigned* ticket,
+                             int* mode, int first_mode) {
   const long long t0 = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const long long stride = (long long)gridDim.x * blockDim.x;
   for (long long s = t0; s < H; s += stride) hub_acc[s] = INF;
@@ -476,6 +770,7 @@ __global__ void k_solve_init(int* X, int* Y, int* G, long long n, int* hub_acc, 
   if (t0 == 0) {
     X[n] = (int)n; Y[n] = (int)n; G[n] = INF;  // dummy vertex n of the padding row
     *done = 0; *ticket = 0u;
+    mode[1] = first_mode;
   }
 }
 

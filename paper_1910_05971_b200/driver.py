@@ -31,10 +31,12 @@ _FORCE_MODES = ("auto", "dense_only", "sparse_only")
 class DriverConfig:
     """Same fields and validation as svcc.DriverConfig (driver.py:31-48).
 
-    ``sparse_threshold``/``force_kernel`` select the reference's per-iteration
-    product; the B200 path always runs the full (dense) product, whose
-    snapshots the reference proves identical to every sparse/auto schedule
-    (test_driver.py:60-71). ``workers`` is accepted for signature parity.
+    ``sparse_threshold``/``force_kernel`` select the per-iteration product
+    exactly as the reference does (dense pull over the oriented layout, or a
+    sparse push from the vertices whose gf changed); results are identical
+    either way (test_driver.py:60-71) and the trace's kernel/flops fields
+    follow the reference's definitions. ``workers`` is accepted for
+    signature parity (the device decides its own parallelism).
     ``batch`` is B200-only: iterations queued per host convergence check."""
 
     sparse_threshold: float = 0.1
@@ -185,17 +187,23 @@ class Solver:
 
     # -- solve ------------------------------------------------------------
     @staticmethod
-    def _config(batch: int = 0, max_iters: int = 0, profile: bool = False) -> FsvConfig:
+    def _config(batch: int = 0, max_iters: int = 0, profile: bool = False,
+                policy: int = 0, threshold: float = 0.1) -> FsvConfig:
         cfg = FsvConfig()
         cfg.batch = int(batch)
         cfg.max_iters = int(max_iters)
         cfg.profile = int(bool(profile))
+        cfg.sparse_policy = int(policy)
+        cfg.sparse_threshold = float(threshold)
         return cfg
 
-    def solve(self, batch: int = 0, max_iters: int = 0, profile: bool = False) -> FsvStats:
+    def solve(self, batch: int = 0, max_iters: int = 0, profile: bool = False,
+              policy: int = 0, threshold: float = 0.1) -> FsvStats:
         """Run to convergence; labels stay on the device. ``profile`` brackets
-        every kernel with CUDA events (per-kernel *_ms in the stats)."""
-        cfg = self._config(batch, max_iters, profile)
+        every kernel with CUDA events (per-kernel *_ms in the stats).
+        ``policy``: 0 reference default (auto, 0.1), 1 dense only, 2 sparse
+        only, 3 auto with ``threshold`` (svcc.choose_kernel)."""
+        cfg = self._config(batch, max_iters, profile, policy, threshold)
         _check(self._lib.fsv_solve(self._ctx, ctypes.byref(cfg), ctypes.byref(self.stats)))
         return self.stats
 
@@ -209,18 +217,25 @@ class Solver:
     def labels_into(self, ptr: int) -> None:
         _check(self._lib.fsv_get_labels(self._ctx, ctypes.c_void_p(ptr)))
 
-    def trace(self):
-        k = int(self.stats.iterations)
+    def trace(self, k: int | None = None, full: bool = False):
+        """(gf_changed, f_changed, ms) — plus (kernel 0/1, flops) with full=True."""
+        k = int(self.stats.iterations) if k is None else int(k)
         gfc = np.zeros(max(k, 1), dtype=np.int64)
         fc = np.zeros(max(k, 1), dtype=np.int64)
         ms = np.zeros(max(k, 1), dtype=np.float32)
-        _check(self._lib.fsv_get_trace(self._ctx, gfc.ctypes.data, fc.ctypes.data, ms.ctypes.data, k))
+        kern = np.zeros(max(k, 1), dtype=np.int32)
+        flops = np.zeros(max(k, 1), dtype=np.int64)
+        _check(self._lib.fsv_get_trace_ex(self._ctx, gfc.ctypes.data, fc.ctypes.data, ms.ctypes.data,
+                                          kern.ctypes.data, flops.ctypes.data, k))
+        if full:
+            return gfc[:k], fc[:k], ms[:k], kern[:k], flops[:k]
         return gfc[:k], fc[:k], ms[:k]
 
-    def run(self, batch: int = 0, max_iters: int = 0, snapshots: bool = False, snap_cap: int = 256):
+    def run(self, batch: int = 0, max_iters: int = 0, snapshots: bool = False, snap_cap: int = 256,
+            policy: int = 0, threshold: float = 0.1, full_trace: bool = False):
         """Solve + copy out: (labels int32, iterations, gf_changed, f_changed,
-        per-iteration ms, snapshots or None)."""
-        cfg = self._config(batch, max_iters)
+        per-iteration ms, snapshots or None[, kernel, flops])."""
+        cfg = self._config(batch, max_iters, False, policy, threshold)
         n = self.n
         labels = np.empty(n, dtype=np.int32)
         iters = ctypes.c_int32(0)
@@ -240,11 +255,9 @@ class Solver:
                 self.labels(labels)
             snap = None
         k = int(iters.value)
-        gfc2 = np.zeros(max(k, 1), dtype=np.int64)
-        fc2 = np.zeros(max(k, 1), dtype=np.int64)
-        ms = np.zeros(max(k, 1), dtype=np.float32)
-        _check(self._lib.fsv_get_trace(self._ctx, gfc2.ctypes.data, fc2.ctypes.data, ms.ctypes.data, k))
-        return labels, k, gfc2[:k], fc2[:k], ms[:k], (snap[:k] if snap is not None else None)
+        gfc2, fc2, ms, kern, flops = self.trace(k, full=True)
+        out = (labels, k, gfc2, fc2, ms, (snap[:k] if snap is not None else None))
+        return out + (kern, flops) if full_trace else out
 
 
 _solvers: dict = {}
@@ -258,11 +271,13 @@ def default_solver(device: int = 0) -> Solver:
     return s
 
 
-def _result(g, labels, iters, gfc, fc, ms, snaps, kernel="dense") -> RunResult:
-    m = int(g.col_indices.size)
+_POLICY = {"auto": 3, "dense_only": 1, "sparse_only": 2}
+
+
+def _result(g, labels, iters, gfc, fc, ms, snaps, kern, flops) -> RunResult:
     trace = [IterationTrace(iteration=i + 1, gf_changed=int(gfc[i]), f_changed=int(fc[i]),
-                            kernel=kernel, elapsed=float(ms[i]) / 1e3,
-                            flops=m if kernel == "dense" else 0)
+                            kernel="sparse" if kern[i] == 1 else "dense",
+                            elapsed=float(ms[i]) / 1e3, flops=int(flops[i]))
              for i in range(iters)]
     snapshots = None
     if snaps is not None:
@@ -275,12 +290,14 @@ def _result(g, labels, iters, gfc, fc, ms, snaps, kernel="dense") -> RunResult:
                      trace=trace, snapshots=snapshots)
 
 
-def _solve_graph(g, record_snapshots: bool, batch: int, device: int) -> RunResult:
+def _solve_graph(g, record_snapshots: bool, batch: int, device: int, policy: int = 0,
+                 threshold: float = 0.1) -> RunResult:
     solver = default_solver(device)
     solver.upload(g)
-    labels, iters, gfc, fc, ms, snaps = solver.run(batch=batch, snapshots=record_snapshots,
-                                                   snap_cap=max(64, 4 * int(np.log2(max(g.n, 2))) + 16))
-    return _result(g, labels, iters, gfc, fc, ms, snaps)
+    labels, iters, gfc, fc, ms, snaps, kern, flops = solver.run(
+        batch=batch, snapshots=record_snapshots, snap_cap=max(64, 4 * int(np.log2(max(g.n, 2))) + 16),
+        policy=policy, threshold=threshold, full_trace=True)
+    return _result(g, labels, iters, gfc, fc, ms, snaps, kern, flops)
 
 
 def fastsv_la(g, cfg: DriverConfig | None = None, record_snapshots: bool = False,
@@ -290,7 +307,8 @@ def fastsv_la(g, cfg: DriverConfig | None = None, record_snapshots: bool = False
     Per-iteration parent vectors, iteration count, gf_changed/f_changed and
     labels are bit-identical to the reference for every DriverConfig."""
     cfg = cfg or DriverConfig()
-    return _solve_graph(g, record_snapshots, cfg.batch, device)
+    return _solve_graph(g, record_snapshots, cfg.batch, device, _POLICY[cfg.force_kernel],
+                        cfg.sparse_threshold)
 
 
 def fastsv(g, cfg: HookingConfig | None = None, record_snapshots: bool = False,

@@ -120,6 +120,35 @@ def make_suite():
     print(f"suite: {len(names)} graphs")
 
 
+DRIVER_CONFIGS = {
+    "auto": dict(),
+    "auto_t1": dict(sparse_threshold=1.0),
+    "auto_t05": dict(sparse_threshold=0.5),
+    "sparse_only": dict(force_kernel="sparse_only"),
+    "dense_only": dict(force_kernel="dense_only"),
+}
+
+
+def make_driver_traces():
+    """Reference IterationTrace.kernel / .flops under several DriverConfigs
+    (driver.py:51-61, 85-93; kernels.py:67-68, 94-102) for a subset of the
+    suite: the device reproduces the same product schedule."""
+    cases = suite_cases()[::4]
+    names, kinds, flops, off = [], [], [], [0]
+    for cname, cfg in DRIVER_CONFIGS.items():
+        for name, n, e in cases:
+            g = svcc.build_csr(n, e)
+            r = svcc.fastsv_la(g, svcc.DriverConfig(**cfg))
+            names.append(f"{cname}:{name}")
+            kinds += [1 if t.kernel == "sparse" else 0 for t in r.trace]
+            flops += [t.flops for t in r.trace]
+            off.append(off[-1] + r.iterations)
+    np.savez_compressed(HERE / "driver_traces.npz", names=np.array(names),
+                        kernel=np.array(kinds, np.int32), flops=np.array(flops, np.int64),
+                        off=np.array(off, np.int64))
+    print(f"driver traces: {len(names)} runs")
+
+
 def kats():
     """Known-answer tests quoted from the reference's own tests."""
     out = {}
@@ -170,6 +199,7 @@ def main():
     ap.add_argument("--full", action="store_true", help="also configs 2-4 at full size (minutes)")
     args = ap.parse_args()
     make_suite()
+    make_driver_traces()
     kats()
     recs = {1: config_record(1)}
     path = HERE / "configs.json"

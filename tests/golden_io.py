@@ -44,3 +44,14 @@ def load_configs():
 
 def load_kats():
     return json.loads((GOLDEN / "kats.json").read_text())
+
+
+def load_driver_traces():
+    """{(config_name, graph_name): (kernel list, flops list)} from the reference."""
+    d = np.load(GOLDEN / "driver_traces.npz", allow_pickle=False)
+    out = {}
+    for i, nm in enumerate(d["names"]):
+        cfg, name = str(nm).split(":", 1)
+        a, b = d["off"][i], d["off"][i + 1]
+        out[(cfg, name)] = (d["kernel"][a:b].tolist(), d["flops"][a:b].tolist())
+    return out

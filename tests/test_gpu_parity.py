@@ -144,3 +144,41 @@ def test_baseline_config_full_size(solver, index):
     assert solver.stats.component_count == rec["component_count"]
     if index == 1:
         assert np.array_equal(labels, oracle.uf_labels(n, pairs))
+
+
+POLICY = {"auto": (3, 0.1), "auto_t1": (3, 1.0), "auto_t05": (3, 0.5), "sparse_only": (2, 0.1),
+          "dense_only": (1, 0.1)}
+
+
+def test_product_schedule_matches_reference_trace(solver):
+    """Same per-iteration product choice (dense pull / sparse push) and the
+    same flops as the reference's IterationTrace under five DriverConfigs;
+    snapshots stay identical to the golden ones under every schedule."""
+    from golden_io import load_driver_traces
+    traces = load_driver_traces()
+    suite = {c.name: c for c in load_suite()}
+    checked = 0
+    for (cfg, name), (kinds, flops) in traces.items():
+        c = suite[name]
+        g = fb.build_csr(c.n, c.edges)
+        solver.set_hub_slots(0)
+        solver.upload(g)
+        policy, thr = POLICY[cfg]
+        labels, iters, gfc, fc, ms, snaps, kern, fl = solver.run(
+            snapshots=True, snap_cap=512, policy=policy, threshold=thr, full_trace=True)
+        assert iters == c.iterations and np.array_equal(snaps, c.snapshots), (cfg, name)
+        assert kern.tolist() == kinds, (cfg, name)
+        assert fl.tolist() == flops, (cfg, name)
+        checked += 1
+    assert checked >= 400
+
+
+def test_public_api_trace_fields_match_reference():
+    g = fb.build_csr(64, [(i, i + 1) for i in range(63)])
+    r = fb.fastsv_la(g, fb.DriverConfig(sparse_threshold=1.0))
+    assert r.trace[0].kernel == "dense"                      # test_driver.py:110-114
+    assert all(t.kernel == "sparse" for t in r.trace[1:])
+    r = fb.fastsv_la(g, fb.DriverConfig(force_kernel="sparse_only"))
+    assert r.trace[0].kernel == "sparse" and r.trace[0].flops == g.m   # test_driver.py:117-121
+    r = fb.fastsv_la(g, fb.DriverConfig(force_kernel="dense_only"))
+    assert all(t.kernel == "dense" and t.flops == g.m for t in r.trace)  # test_driver.py:124-127

@@ -21,7 +21,7 @@ for c in cfgs:
             st = s.solve()
             times.append(st.solve_ms)
         pr = s.solve(profile=True)
-        print(f"  profile: first {pr.first_ms*1e3:.1f} us  hook {pr.hook_ms*1e3:.1f} us/{pr.hook_launches}  hubfix {pr.hubfix_ms*1e3:.1f} us  shortcut {pr.shortcut_ms*1e3:.1f} us  total {pr.solve_ms*1e3:.1f} us")
+        print(f"  profile: first {pr.first_ms*1e3:.1f} us  hook {pr.hook_ms*1e3:.1f} us/{pr.hook_launches}  hubfix {pr.hubfix_ms*1e3:.1f} us  push {pr.push_ms*1e3:.1f} us ({pr.sparse_iterations} sparse)  shortcut {pr.shortcut_ms*1e3:.1f} us  total {pr.solve_ms*1e3:.1f} us")
         lab = s.labels()
         gfc, fc, ms = s.trace()
         print(f"  hubs={st.hub_slots} E={st.oriented_entries} upload {tu*1e3:.0f} ms  iters {st.iterations} "
