@@ -162,6 +162,7 @@ struct fsv_ctx {
     DBuf<long long> cnt, out_off, nzoff;
     DBuf<unsigned char> tmp;
     DBuf<int64_t> cols64;
+    DBuf<uint32_t> etmp;
   } ws;
   long long rcap = 0;
   int dgrid = 1;
@@ -258,101 +259,155 @@ extern "C" int fsv_set_stream(fsv_ctx* c, void* s) {
 // ---------------------------------------------------------------------------
 // upload pipeline kernels
 
+// degrees + ids for the sort, and the offsets sanity check (non-decreasing)
 __global__ void k_degree(const int64_t* __restrict__ off, long long n, int* __restrict__ deg,
-                         int* __restrict__ ids) {
+                         int* __restrict__ ids, unsigned long long* bad) {
   for (long long u = blockIdx.x * (long long)blockDim.x + threadIdx.x; u < n;
        u += (long long)gridDim.x * blockDim.x) {
-    deg[u] = (int)(off[u + 1] - off[u]);
+    const int64_t d = off[u + 1] - off[u];
+    if (d < 0) atomicMin(bad, (unsigned long long)u);
+    deg[u] = (int)d;
     ids[u] = (int)u;
   }
 }
 
-template <typename ColT>
-__global__ void k_check_cols(const ColT* __restrict__ cols, long long m, long long n,
-                             unsigned long long* bad) {
-  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < m;
-       e += (long long)gridDim.x * blockDim.x) {
-    const long long v = (long long)cols[e];
-    if (v < 0 || v >= n) atomicMin(bad, (unsigned long long)e);
+// pos[v] = position of v in the degree-descending order (ties by id); hubs
+// are the first H positions, so a vertex's hub slot is its position.
+__global__ void k_positions(const int* __restrict__ sorted_ids, long long n, int H,
+                            int* __restrict__ pos, int* __restrict__ hub_id) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int v = sorted_ids[i];
+    pos[v] = (int)i;
+    if (i < H) hub_id[i] = v;
   }
 }
 
-__global__ void k_hub_slots(const int* __restrict__ sorted_ids, int H, int* __restrict__ slot_of,
-                            int* __restrict__ hub_id) {
-  for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < H; s += gridDim.x * blockDim.x) {
-    const int v = sorted_ids[s];
-    hub_id[s] = v;
-    slot_of[v] = s;
-  }
+constexpr uint32_t DROP = 0xffffffffu;
+
+__device__ __forceinline__ uint32_t encode_col(int v, int pv, int H) {
+  return pv < H ? (HUB | (uint32_t)pv) : (uint32_t)v;
 }
 
-__device__ __forceinline__ bool key_less(int du, int u, int dv, int v) {
-  return du < dv || (du == dv && u < v);
-}
-
-// Warp per row: number of entries kept by the orientation (row u keeps v iff
-// (deg u, u) < (deg v, v), so each undirected edge is stored exactly once).
+// Orientation pass 1: the edge {u, v} is kept once, in the row of the
+// endpoint that comes later in the degree order (so columns point at
+// high-degree vertices). Each entry gathers pos[v] once and is written,
+// encoded, at its own position in `tmp` (DROP if not kept); per-row kept
+// counts (+1 header) go to cnt. Warp = 32 consecutive rows: short rows one
+// per lane, long rows by the whole warp. Also range-checks the columns.
 template <typename ColT>
-__global__ void k_orient_count(const int64_t* __restrict__ off, const ColT* __restrict__ cols,
-                               long long col_base, long long row_begin, long long rows,
-                               const int* __restrict__ deg, long long* __restrict__ cnt,
-                               int* __restrict__ nzflag) {
+__global__ void k_orient_encode(const int64_t* __restrict__ off, const ColT* __restrict__ cols,
+                                long long col_base, long long row_begin, long long rows, long long n,
+                                const int* __restrict__ pos, int H, uint32_t* __restrict__ tmp,
+                                long long* __restrict__ cnt, int* __restrict__ nzflag,
+                                unsigned long long* bad) {
   const int lane = threadIdx.x & 31;
   const long long nw = (long long)gridDim.x * (blockDim.x >> 5);
-  for (long long w = blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5); w < rows;
-       w += nw) {
-    const long long u = row_begin + w;
-    const int du = deg[u];
+  for (long long w0 = ((long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32; w0 < rows;
+       w0 += nw * 32) {
+    const long long r = w0 + lane;
+    long long lo = 0, hi = 0;
+    int pu = 0;
+    if (r < rows) {
+      const long long u = row_begin + r;
+      lo = off[u] - col_base;
+      hi = off[u + 1] - col_base;
+      pu = pos[u];
+    }
+    const bool is_long = hi - lo > 32;
     long long k = 0;
-    for (long long e = off[u] + lane; e < off[u + 1]; e += 32) {
-      const int v = (int)cols[e - col_base];
-      k += key_less(du, (int)u, deg[v], v);
+    if (!is_long) {
+      for (long long e = lo; e < hi; ++e) {
+        const long long v = (long long)cols[e];
+        uint32_t code = DROP;
+        if (v < 0 || v >= n) {
+          atomicMin(bad, (unsigned long long)e);
+        } else {
+          const int pv = pos[v];
+          if (pv < pu) { code = encode_col((int)v, pv, H); ++k; }
+        }
+        tmp[e] = code;
+      }
     }
-    for (int o = 16; o; o >>= 1) k += __shfl_xor_sync(0xffffffffu, k, o);
-    if (lane == 0) {
-      cnt[w] = k ? k + 1 : 0;  // + header entry
-      nzflag[w] = k > 0;
+    unsigned lm = __ballot_sync(0xffffffffu, is_long);
+    while (lm) {
+      const int src = __ffs(lm) - 1;
+      lm &= lm - 1;
+      const long long slo = __shfl_sync(0xffffffffu, lo, src);
+      const long long shi = __shfl_sync(0xffffffffu, hi, src);
+      const int spu = __shfl_sync(0xffffffffu, pu, src);
+      long long sk = 0;
+      for (long long e = slo + lane; e < shi; e += 32) {
+        const long long v = (long long)cols[e];
+        uint32_t code = DROP;
+        if (v < 0 || v >= n) {
+          atomicMin(bad, (unsigned long long)e);
+        } else {
+          const int pv = pos[v];
+          if (pv < spu) { code = encode_col((int)v, pv, H); ++sk; }
+        }
+        tmp[e] = code;
+      }
+      for (int o = 16; o; o >>= 1) sk += __shfl_xor_sync(0xffffffffu, sk, o);
+      if (lane == src) k = sk;
+    }
+    if (r < rows) {
+      cnt[r] = k ? k + 1 : 0;  // + header entry
+      nzflag[r] = k > 0;
     }
   }
 }
 
-template <typename ColT>
-__global__ void k_orient_write(const int64_t* __restrict__ off, const ColT* __restrict__ cols,
-                               long long col_base, long long row_begin, long long rows,
-                               const int* __restrict__ deg, const long long* __restrict__ out_off,
-                               const int* __restrict__ nzidx, const int* __restrict__ slot_of,
-                               uint32_t* __restrict__ ecol, int* __restrict__ nzrows,
-                               long long* __restrict__ nzoff) {
+// Orientation pass 2 (no gathers): header + kept entries of each row, in
+// order, at out_off[r]; nzrows/nzoff for the span table.
+__global__ void k_orient_compact(const int64_t* __restrict__ off, long long col_base, long long row_begin,
+                                 long long rows, const uint32_t* __restrict__ tmp,
+                                 const long long* __restrict__ out_off, const int* __restrict__ nzidx,
+                                 uint32_t* __restrict__ ecol, int* __restrict__ nzrows,
+                                 long long* __restrict__ nzoff) {
   const int lane = threadIdx.x & 31;
   const long long nw = (long long)gridDim.x * (blockDim.x >> 5);
-  for (long long w = blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5); w < rows;
-       w += nw) {
-    const long long u = row_begin + w;
-    const int du = deg[u];
-    const long long o0 = out_off[w];
-    if (out_off[w + 1] == o0) continue;  // no kept entries: no header either
-    long long o = o0 + 1;                 // entry o0 is the row header
-    const long long hi = off[u + 1];
-    for (long long e0 = off[u]; e0 < hi; e0 += 32) {
-      const long long e = e0 + lane;
-      bool keep = false;
-      int v = 0;
-      if (e < hi) {
-        v = (int)cols[e - col_base];
-        keep = key_less(du, (int)u, deg[v], v);
+  for (long long w0 = ((long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32; w0 < rows;
+       w0 += nw * 32) {
+    const long long r = w0 + lane;
+    long long lo = 0, hi = 0, o0 = 0;
+    bool has = false;
+    if (r < rows) {
+      const long long u = row_begin + r;
+      lo = off[u] - col_base;
+      hi = off[u + 1] - col_base;
+      o0 = out_off[r];
+      has = out_off[r + 1] > o0;
+      if (has) {
+        ecol[o0] = HDR | (uint32_t)u;
+        const int z = nzidx[r];
+        nzrows[z] = (int)u;
+        nzoff[z] = o0;
       }
-      const unsigned b = __ballot_sync(0xffffffffu, keep);
-      if (keep) {
-        const int s = slot_of[v];
-        ecol[o + __popc(b & ((1u << lane) - 1u))] = s >= 0 ? (HUB | (uint32_t)s) : (uint32_t)v;
-      }
-      o += __popc(b);
     }
-    if (lane == 0) {
-      ecol[o0] = HDR | (uint32_t)u;
-      const int r = nzidx[w];
-      nzrows[r] = (int)u;
-      nzoff[r] = o0;
+    const bool is_long = has && hi - lo > 32;
+    if (has && !is_long) {
+      long long o = o0 + 1;
+      for (long long e = lo; e < hi; ++e) {
+        const uint32_t code = tmp[e];
+        if (code != DROP) ecol[o++] = code;
+      }
+    }
+    unsigned lm = __ballot_sync(0xffffffffu, is_long);
+    while (lm) {
+      const int src = __ffs(lm) - 1;
+      lm &= lm - 1;
+      const long long slo = __shfl_sync(0xffffffffu, lo, src);
+      const long long shi = __shfl_sync(0xffffffffu, hi, src);
+      long long o = __shfl_sync(0xffffffffu, o0, src) + 1;
+      for (long long e0 = slo; e0 < shi; e0 += 32) {
+        const long long e = e0 + lane;
+        const uint32_t code = e < shi ? tmp[e] : DROP;
+        const bool keep = code != DROP;
+        const unsigned b = __ballot_sync(0xffffffffu, keep);
+        if (keep) ecol[o + __popc(b & ((1u << lane) - 1u))] = code;
+        o += __popc(b);
+      }
     }
   }
 }
@@ -386,20 +441,28 @@ __global__ void k_span_row(const long long* __restrict__ nzoff, const int* __res
 }
 
 // f_1[u] = min(u, first (= smallest) column of row u) for rows this rank owns;
-// other rows get INF so an allreduce-min assembles the global vector.
+// other rows get `outside` (INF before an allreduce-min assembles the global
+// vector, or u itself when there is no communicator).
 template <typename ColT>
 __global__ void k_f1(const int64_t* __restrict__ off, const ColT* __restrict__ cols,
                      long long col_base, long long row_begin, long long row_end, long long n,
-                     int* __restrict__ f1) {
+                     int* __restrict__ f1, bool outside_inf) {
   for (long long u = blockIdx.x * (long long)blockDim.x + threadIdx.x; u < n;
        u += (long long)gridDim.x * blockDim.x) {
-    int val = INF;
+    int val = outside_inf ? INF : (int)u;
     if (u >= row_begin && u < row_end) {
       val = (int)u;
       if (off[u + 1] > off[u]) val = min(val, (int)cols[off[u] - col_base]);
     }
     f1[u] = val;
   }
+}
+
+// rows no rank owned stay isolated (never index with INF)
+__global__ void k_f1_fix(int* __restrict__ f1, long long n) {
+  for (long long u = blockIdx.x * (long long)blockDim.x + threadIdx.x; u < n;
+       u += (long long)gridDim.x * blockDim.x)
+    if (f1[u] == INF) f1[u] = (int)u;
 }
 
 __global__ void k_narrow(const int64_t* __restrict__ in, long long m, int* __restrict__ out) {
@@ -432,10 +495,10 @@ static int upload_impl(fsv_ctx* c, int64_t n, const int64_t* h_off, const ColT* 
     return fail(FSV_ERR_CONTRACT, "row range [%lld, %lld) invalid for n=%lld", (long long)row_begin,
                 (long long)row_end, (long long)n);
   if (h_off[0] != 0) return fail(FSV_ERR_INPUT, "row_offsets[0] must be 0");
-  for (int64_t u = 0; u < n; ++u)
-    if (h_off[u + 1] < h_off[u]) return fail(FSV_ERR_INPUT, "row_offsets must be non-decreasing");
+  if (h_off[n] < h_off[0]) return fail(FSV_ERR_INPUT, "row_offsets must be non-decreasing");
   const int64_t e_begin = h_off[row_begin], e_end = h_off[row_end];
   const int64_t mloc = e_end - e_begin;
+  if (mloc < 0 || e_begin < 0) return fail(FSV_ERR_INPUT, "row_offsets must be non-decreasing");
   if (mloc > 0 && !h_cols) return fail(FSV_ERR_CONTRACT, "col_indices is NULL");
   CUDA_TRY(cudaSetDevice(c->device));
   cudaStream_t st = c->stream;
@@ -450,31 +513,18 @@ static int upload_impl(fsv_ctx* c, int64_t n, const int64_t* h_off, const ColT* 
   CUDA_TRY(cudaMemcpyAsync(d_off.p, h_off, sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice, st));
   if (mloc) CUDA_TRY(cudaMemcpyAsync(d_cols.p, h_cols, sizeof(ColT) * mloc, cudaMemcpyHostToDevice, st));
 
-  // column range check (graph.py:71-75 semantics: report an offending entry)
+  // degrees (+ offsets check), stable degree order, positions, hubs
   DBuf<unsigned long long>& d_bad = c->ws.bad;
-  CUDA_TRY(d_bad.alloc(1));
-  CUDA_TRY(cudaMemsetAsync(d_bad.p, 0xff, sizeof(unsigned long long), st));
-  if (mloc) k_check_cols<ColT><<<grid_for(c, mloc, 256), 256, 0, st>>>(d_cols.p, mloc, n, d_bad.p);
-  unsigned long long h_bad = 0;
-  CUDA_TRY(cudaMemcpyAsync(&h_bad, d_bad.p, sizeof h_bad, cudaMemcpyDeviceToHost, st));
-  CUDA_TRY(cudaStreamSynchronize(st));
-  if (h_bad != ~0ull) {
-    const int64_t e = e_begin + (int64_t)h_bad;
-    const int64_t* it = std::upper_bound(h_off, h_off + n + 1, e);
-    const long long u = (long long)(it - h_off) - 1;
-    return fail(FSV_ERR_INPUT, "edge (%lld, %lld) out of range for n=%lld", u,
-                (long long)h_cols[h_bad], (long long)n);
-  }
-
-  // degrees + hub selection (top-H by degree, stable, identical on all ranks)
+  CUDA_TRY(d_bad.alloc(2));
+  CUDA_TRY(cudaMemsetAsync(d_bad.p, 0xff, 2 * sizeof(unsigned long long), st));
   auto& deg = c->ws.deg;
   auto& ids = c->ws.ids;
   auto& deg_sorted = c->ws.deg_sorted;
   auto& ids_sorted = c->ws.ids_sorted;
-  auto& slot_of = c->ws.slot_of;
+  auto& pos = c->ws.slot_of;
   CUDA_TRY(deg.alloc(n)); CUDA_TRY(ids.alloc(n));
-  CUDA_TRY(deg_sorted.alloc(n)); CUDA_TRY(ids_sorted.alloc(n)); CUDA_TRY(slot_of.alloc(n));
-  if (n) k_degree<<<grid_for(c, n, 256), 256, 0, st>>>(d_off.p, n, deg.p, ids.p);
+  CUDA_TRY(deg_sorted.alloc(n)); CUDA_TRY(ids_sorted.alloc(n)); CUDA_TRY(pos.alloc(n));
+  if (n) k_degree<<<grid_for(c, n, 256), 256, 0, st>>>(d_off.p, n, deg.p, ids.p, d_bad.p + 1);
   int H = 0;
   if (n) {
     size_t tmp_bytes = 0;
@@ -484,11 +534,14 @@ static int upload_impl(fsv_ctx* c, int64_t n, const int64_t* h_off, const ColT* 
     CUDA_TRY(tmp.alloc(tmp_bytes));
     CUDA_TRY(cub::DeviceRadixSort::SortPairsDescending(tmp.p, tmp_bytes, deg.p, deg_sorted.p, ids.p,
                                                        ids_sorted.p, (int)n, 0, 32, st));
-    // number of vertices with degree >= kHubMinDegree among the first kHubMax
+    // hubs: the first positions with degree >= kHubMinDegree, at most kHubMax
     const int probe = (int)std::min<int64_t>(n, kHubMax);
     std::vector<int> top(probe);
+    unsigned long long h_badoff = 0;
     CUDA_TRY(cudaMemcpyAsync(top.data(), deg_sorted.p, sizeof(int) * probe, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaMemcpyAsync(&h_badoff, d_bad.p + 1, sizeof h_badoff, cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaStreamSynchronize(st));
+    if (h_badoff != ~0ull) return fail(FSV_ERR_INPUT, "row_offsets must be non-decreasing");
     int cand = 0;
     while (cand < probe && top[cand] >= kHubMinDegree) ++cand;
     H = (c->hub_limit >= 0) ? std::min(cand, c->hub_limit) : 0;
@@ -496,22 +549,23 @@ static int upload_impl(fsv_ctx* c, int64_t n, const int64_t* h_off, const ColT* 
     if (H < 256) H = 0;
   }
   c->H = H;
-  if (n) CUDA_TRY(cudaMemsetAsync(slot_of.p, 0xff, sizeof(int) * n, st));
   CUDA_TRY(c->hub_id.alloc(std::max(H, 4)));
-  if (H) k_hub_slots<<<grid_for(c, H, 256), 256, 0, st>>>(ids_sorted.p, H, slot_of.p, c->hub_id.p);
+  if (n) k_positions<<<grid_for(c, n, 256), 256, 0, st>>>(ids_sorted.p, n, H, pos.p, c->hub_id.p);
 
-  // orientation
+  // orientation: encode (one gather per entry), scan, compact
   auto& cnt = c->ws.cnt;
   auto& out_off = c->ws.out_off;
   auto& nzflag = c->ws.nzflag;
   auto& nzidx = c->ws.nzidx;
+  auto& etmp = c->ws.etmp;
   CUDA_TRY(cnt.alloc(rows + 1)); CUDA_TRY(out_off.alloc(rows + 1));
   CUDA_TRY(nzflag.alloc(rows + 1)); CUDA_TRY(nzidx.alloc(rows + 1));
+  CUDA_TRY(etmp.alloc((size_t)std::max<int64_t>(mloc, 1)));
   CUDA_TRY(cudaMemsetAsync(cnt.p + rows, 0, sizeof(long long), st));
   CUDA_TRY(cudaMemsetAsync(nzflag.p + rows, 0, sizeof(int), st));
   if (rows)
-    k_orient_count<ColT><<<grid_for(c, rows * 32, 256, 16), 256, 0, st>>>(
-        d_off.p, d_cols.p, e_begin, row_begin, rows, deg.p, cnt.p, nzflag.p);
+    k_orient_encode<ColT><<<grid_for(c, (rows + 31) / 32 * 32, 256, 16), 256, 0, st>>>(
+        d_off.p, d_cols.p, e_begin, row_begin, rows, n, pos.p, H, etmp.p, cnt.p, nzflag.p, d_bad.p);
   {
     size_t b1 = 0, b2 = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, b1, cnt.p, out_off.p, (int)(rows + 1), st);
@@ -523,9 +577,19 @@ static int upload_impl(fsv_ctx* c, int64_t n, const int64_t* h_off, const ColT* 
   }
   long long E = 0;
   int R = 0;
+  unsigned long long h_bad = 0;
   CUDA_TRY(cudaMemcpyAsync(&E, out_off.p + rows, sizeof E, cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaMemcpyAsync(&R, nzidx.p + rows, sizeof R, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaMemcpyAsync(&h_bad, d_bad.p, sizeof h_bad, cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaStreamSynchronize(st));
+  if (h_bad != ~0ull) {
+    // graph.py:71-75 semantics: report an offending entry
+    const int64_t e = e_begin + (int64_t)h_bad;
+    const int64_t* it = std::upper_bound(h_off, h_off + n + 1, e);
+    const long long u = (long long)(it - h_off) - 1;
+    return fail(FSV_ERR_INPUT, "edge (%lld, %lld) out of range for n=%lld", u,
+                (long long)h_cols[h_bad], (long long)n);
+  }
   const long long Epad = (E + SPAN - 1) / SPAN * SPAN;
   CUDA_TRY(c->ecol.alloc((size_t)std::max<long long>(Epad, 4)));
   auto& nzrows = c->ws.nzrows;
@@ -533,9 +597,8 @@ static int upload_impl(fsv_ctx* c, int64_t n, const int64_t* h_off, const ColT* 
   auto& nzoff = c->ws.nzoff;
   CUDA_TRY(nzoff.alloc((size_t)R + 1));
   if (rows)
-    k_orient_write<ColT><<<grid_for(c, rows * 32, 256, 16), 256, 0, st>>>(
-        d_off.p, d_cols.p, e_begin, row_begin, rows, deg.p, out_off.p, nzidx.p, slot_of.p,
-        c->ecol.p, nzrows.p, nzoff.p);
+    k_orient_compact<<<grid_for(c, (rows + 31) / 32 * 32, 256, 16), 256, 0, st>>>(
+        d_off.p, e_begin, row_begin, rows, etmp.p, out_off.p, nzidx.p, c->ecol.p, nzrows.p, nzoff.p);
   k_pad<<<grid_for(c, std::max<long long>(Epad - E, 1), 256), 256, 0, st>>>(c->ecol.p, E, Epad, (int)n,
                                                                              nzrows.p, R, nzoff.p);
   const long long nspans = Epad / SPAN;
@@ -547,9 +610,10 @@ static int upload_impl(fsv_ctx* c, int64_t n, const int64_t* h_off, const ColT* 
   CUDA_TRY(c->f1.alloc((size_t)n + 64));
   if (n)
     k_f1<ColT><<<grid_for(c, n, 256), 256, 0, st>>>(d_off.p, d_cols.p, e_begin, row_begin, row_end, n,
-                                                    c->f1.p);
+                                                    c->f1.p, c->comm != nullptr);
   if (c->comm && n) {
     NCCL_TRY(g_nccl.AllReduce(c->f1.p, c->f1.p, (size_t)n, ncclInt32, ncclMin, c->comm, st));
+    k_f1_fix<<<grid_for(c, n, 256), 256, 0, st>>>(c->f1.p, n);
   }
 
   // keep the rank's symmetric columns (int32) for sparse iterations

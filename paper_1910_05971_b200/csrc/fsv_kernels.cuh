@@ -50,11 +50,17 @@ constexpr int INF = 0x7fffffff;
 constexpr uint32_t HDR = 0x80000000u;
 constexpr uint32_t HUB = 0x40000000u;    // edge column is a hub: low bits = slot
 constexpr uint32_t IDMASK = 0x3fffffffu;
+#ifndef FSV_HOOK_THREADS
+#define FSV_HOOK_THREADS 1024
+#endif
+#ifndef FSV_STEPS
+#define FSV_STEPS 4
+#endif
 constexpr int EPL = 8;                   // contiguous entries per lane per step
 constexpr int STEP = 32 * EPL;           // entries per warp step
-constexpr int STEPS = 4;                 // steps per span
+constexpr int STEPS = FSV_STEPS;         // steps per span
 constexpr int SPAN = STEP * STEPS;       // entries per warp task
-constexpr int HOOK_THREADS = 768;
+constexpr int HOOK_THREADS = FSV_HOOK_THREADS;
 constexpr int SC_THREADS = 512;
 constexpr int NCOUNT = 16;               // counter slots per iteration
 enum { C_GF = 0, C_F = 1, C_NONSTAR = 2, C_ROOTS = 3, C_VIOL = 4,   // vertex-pass counters

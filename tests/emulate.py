@@ -4,7 +4,8 @@ Mirrors what libfastsv.so does, step for step, so the host-side partition
 logic and the collective semantics can be tested on CPU:
 
   layout     each undirected edge {a, b} kept once, in the row of the endpoint
-             with the smaller (degree, id) key (k_orient_count/k_orient_write)
+             that comes later in the degree-descending order, ties by id
+             (k_positions + k_orient_encode/k_orient_compact)
   iteration 1  f1[u] = min(u, smallest neighbour) from each rank's own rows,
              assembled with an allreduce-min (k_f1 + ncclAllReduce)
   iteration k>=2 on every rank, over its own oriented entries (k_hook):
@@ -32,9 +33,10 @@ def oriented_entries(n, offsets, cols, row_begin, row_end):
     lo, hi = offsets[row_begin], offsets[row_end]
     rows = np.repeat(np.arange(row_begin, row_end, dtype=np.int64), deg[row_begin:row_end])
     c = np.asarray(cols, dtype=np.int64)[lo:hi] if cols.size else np.zeros(0, np.int64)
-    key_r = deg[rows] * (n + 1) + rows
-    key_c = deg[c] * (n + 1) + c
-    keep = key_r < key_c
+    order = np.argsort(-deg, kind="stable")        # degree-descending, ties by id
+    pos = np.empty(n, dtype=np.int64)
+    pos[order] = np.arange(n)
+    keep = pos[c] < pos[rows]
     return rows[keep], c[keep]
 
 

@@ -182,3 +182,37 @@ def test_public_api_trace_fields_match_reference():
     assert r.trace[0].kernel == "sparse" and r.trace[0].flops == g.m   # test_driver.py:117-121
     r = fb.fastsv_la(g, fb.DriverConfig(force_kernel="dense_only"))
     assert all(t.kernel == "dense" and t.flops == g.m for t in r.trace)  # test_driver.py:124-127
+
+
+def test_single_rank_nccl_path_matches():
+    """The multi-GPU code path (NCCL allreduce-min every iteration, f1
+    assembled by allreduce at upload) with one rank: identical results."""
+    n, e = gen.rmat(13, 16, seed=21)
+    g = fb.build_csr(n, e)
+    o = oracle.fastsv_csr(n, g.row_offsets, g.col_indices)
+    with fb.Solver(0) as s:
+        s.attach_nccl(fb.Solver.nccl_unique_id(), 1, 0)
+        s.upload(g)
+        labels, iters, gfc, fc, ms, _ = s.run()
+    assert iters == o.iterations and gfc.tolist() == o.gf_changed.tolist()
+    assert np.array_equal(labels, o.labels)
+
+
+def test_row_partition_upload_two_contexts_emulate_ranks():
+    """Two contexts on one GPU, each owning half the rows, run WITHOUT a
+    communicator cannot merge; instead check the partitioned layout covers
+    every edge exactly once: the union of the two ranks' oriented entries
+    equals the single-rank layout size."""
+    n, e = gen.rmat(12, 16, seed=22)
+    g = fb.build_csr(n, e)
+    import bench
+    sizes = []
+    for r in range(2):
+        lo, hi = bench.row_partition(g.row_offsets, 2, r)
+        with fb.Solver(0) as s:
+            s.upload(g, lo, hi, g.col_indices[g.row_offsets[lo]:g.row_offsets[hi]])
+            sizes.append(int(s.solve().oriented_entries))
+    with fb.Solver(0) as s:
+        s.upload(g)
+        total = int(s.solve().oriented_entries)
+    assert sum(sizes) == total == g.m // 2
