@@ -190,6 +190,16 @@ struct fsv_ctx {
   int labels_ready = 0;
   int host_syncs = 0, launches = 0;
   int hub_limit = kHubMax;
+  // device loop control + CUDA-graph (conditional WHILE) of the iteration loop
+  DBuf<int> iterbuf;
+  DBuf<unsigned long long> tstamp;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t graph_exec = nullptr;
+  cudaGraphConditionalHandle graph_cond = 0;
+  bool graph_dirty = true;
+  int graph_key_policy = -1, graph_key_cap = -1;
+  double graph_key_thr = -1.0;
+  bool use_graph = true;
   int sc_grid = 296;  // resident blocks of the vertex-pass kernels
   // multi-GPU
   ncclComm_t comm = nullptr;
@@ -243,6 +253,9 @@ extern "C" int fsv_destroy(fsv_ctx* c) {
   cudaSetDevice(c->device);
   cudaStreamSynchronize(c->stream);
   for (auto e : c->events) cudaEventDestroy(e);
+  for (auto e : c->pev) cudaEventDestroy(e);
+  if (c->graph_exec) cudaGraphExecDestroy(c->graph_exec);
+  if (c->graph) cudaGraphDestroy(c->graph);
   if (c->comm && g_nccl.CommDestroy) g_nccl.CommDestroy(c->comm);
   if (c->h_done) cudaFreeHost(c->h_done);
   if (c->own_stream) cudaStreamDestroy(c->own_stream);
@@ -504,6 +517,7 @@ static int upload_impl(fsv_ctx* c, int64_t n, const int64_t* h_off, const ColT* 
   cudaStream_t st = c->stream;
   c->ready = false;
   c->labels_ready = 0;
+  c->graph_dirty = true;
 
   const long long rows = row_end - row_begin;
   DBuf<int64_t>& d_off = c->csr_off;
@@ -642,6 +656,8 @@ static int upload_impl(fsv_ctx* c, int64_t n, const int64_t* h_off, const ColT* 
     CUDA_TRY(c->dlist.alloc((size_t)(warps * c->rcap)));
     CUDA_TRY(c->dcount.alloc((size_t)warps));
     CUDA_TRY(c->mode.alloc((size_t)kTraceCap + 2));
+    CUDA_TRY(c->iterbuf.alloc(4));
+    CUDA_TRY(c->tstamp.alloc((size_t)kTraceCap + 2));
     const long long max_batches = n / 32 + warps + 2;
     CUDA_TRY(c->pdesc.alloc((size_t)(max_batches * 32)));
     CUDA_TRY(c->pbtotal.alloc((size_t)max_batches));
@@ -715,8 +731,22 @@ static inline void pmark(fsv_ctx* c, int k, int slot) {
   if (c->profile) cudaEventRecord(c->pev[(size_t)k * kPev + slot], c->stream);
 }
 
-static int launch_iteration(fsv_ctx* c, int k, int max_iter) {
+static LoopCtl loop_ctl(fsv_ctx* c, int graph) {
+  LoopCtl l;
+  l.iterp = c->iterbuf.p;
+  l.cnt_base = c->cnt.p;
+  l.tstamp = c->tstamp.p;
+  l.cond = (unsigned long long)c->graph_cond;
+  l.graph = graph;
+  return l;
+}
+
+// Queue iteration k (host loop), or, with graph = true, one half of the
+// graph body whose buffer parity is that of k (the iteration number itself
+// is read by the kernels from device memory).
+static int launch_iteration(fsv_ctx* c, int k, int max_iter, bool graph = false) {
   cudaStream_t st = c->stream;
+  const LoopCtl lc = loop_ctl(c, graph ? 1 : 0);
   if (c->profile) {
     int rc = ensure_pevents(c, (size_t)(k + 1) * kPev);
     if (rc) return rc;
@@ -739,6 +769,7 @@ static int launch_iteration(fsv_ctx* c, int k, int max_iter) {
     p.flops = slot + C_FLOPS; p.nchunks = slot + C_CHUNKS; p.nbatches = slot + C_BATCHES;
     p.barrier = reinterpret_cast<unsigned*>(slot + C_BARRIER); p.chunks = c->chunks.p;
     p.desc = c->pdesc.p; p.btotal = c->pbtotal.p;
+    a.lc = lc;
     // persistent, one CTA per SM; cooperative launch guarantees co-residency
     // for the grid barrier of the sparse (push) path
     pmark(c, k, 0);
@@ -751,7 +782,8 @@ static int launch_iteration(fsv_ctx* c, int k, int max_iter) {
   if (c->H) {
     pmark(c, k, 2);
     k_hubfix<<<grid_for(c, c->H, 256), 256, 0, st>>>(c->hub_acc.p, c->hub_id.p, c->H, F, c->G.p, N,
-                                                       c->done.p, c->mode.p, k);
+                                                       c->done.p, c->mode.p, k,
+                                                       graph ? c->iterbuf.p : nullptr);
     pmark(c, k, 3);
     ++c->launches;
   }
@@ -766,10 +798,48 @@ static int launch_iteration(fsv_ctx* c, int k, int max_iter) {
   s.partials = c->partials.p;
   s.dl = delta_out(c);
   s.iter = k; s.max_iter = max_iter;
+  s.lc = lc;
   pmark(c, k, 6);
   k_shortcut<<<vertex_grid(c), SC_THREADS, 0, st>>>(s);
   pmark(c, k, 7);
   ++c->launches;
+  return FSV_OK;
+}
+
+// Builds (or reuses) the CUDA graph of the iteration loop: one conditional
+// WHILE node whose body is an even and an odd iteration (buffer parity).
+static int ensure_graph(fsv_ctx* c, int cap) {
+  if (!c->graph_dirty && c->graph_exec && c->graph_key_policy == c->policy &&
+      c->graph_key_thr == c->threshold && c->graph_key_cap == cap)
+    return FSV_OK;
+  if (c->graph_exec) { cudaGraphExecDestroy(c->graph_exec); c->graph_exec = nullptr; }
+  if (c->graph) { cudaGraphDestroy(c->graph); c->graph = nullptr; }
+  CUDA_TRY(cudaGraphCreate(&c->graph, 0));
+  CUDA_TRY(cudaGraphConditionalHandleCreate(&c->graph_cond, c->graph, 1, cudaGraphCondAssignDefault));
+  cudaGraphNodeParams cp = {};
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = c->graph_cond;
+  cp.conditional.type = cudaGraphCondTypeWhile;
+  cp.conditional.size = 1;
+  cudaGraphNode_t node;
+  CUDA_TRY(cudaGraphAddNode(&node, c->graph, nullptr, 0, &cp));
+  cudaGraph_t body = cp.conditional.phGraph_out[0];
+  const bool prof = c->profile;
+  c->profile = false;
+  CUDA_TRY(cudaStreamBeginCaptureToGraph(c->stream, body, nullptr, nullptr, 0,
+                                         cudaStreamCaptureModeRelaxed));
+  int rc = launch_iteration(c, 2, cap, true);
+  if (!rc) rc = launch_iteration(c, 3, cap, true);
+  cudaGraph_t captured = body;
+  const cudaError_t ec = cudaStreamEndCapture(c->stream, &captured);
+  c->profile = prof;
+  if (rc) return rc;
+  CUDA_TRY(ec);
+  CUDA_TRY(cudaGraphInstantiate(&c->graph_exec, c->graph, 0));
+  c->graph_dirty = false;
+  c->graph_key_policy = c->policy;
+  c->graph_key_thr = c->threshold;
+  c->graph_key_cap = cap;
   return FSV_OK;
 }
 
@@ -807,10 +877,13 @@ static int solve_impl(fsv_ctx* c, const fsv_config* cfg, int32_t* snapshots, int
   c->hook_launches = 0;
   if (c->profile && (rc = ensure_pevents(c, 2 * kPev))) return rc;
 
+  // graph mode: the whole iteration loop is one conditional-WHILE graph launch
+  const bool graph_mode = c->use_graph && !snapshots && !c->profile && !c->comm && d.batch == 0;
+  if (graph_mode && (rc = ensure_graph(c, cap))) return rc;
   CUDA_TRY(cudaEventRecord(c->events[0], st));
   k_solve_init<<<grid_for(c, std::max<long long>(c->H, (long long)cap * NCOUNT), 256), 256, 0, st>>>(
       c->X.p, c->Y.p, c->G.p, c->n, c->hub_acc.p, c->H, c->cnt.p, (long long)cap * NCOUNT, c->done.p,
-      c->ticket.p, c->mode.p, c->policy == 2 ? 1 : 0);
+      c->ticket.p, c->mode.p, c->policy == 2 ? 1 : 0, c->tstamp.p);
   pmark(c, 1, 6);
   {
     FirstArgs fa;
@@ -818,6 +891,7 @@ static int solve_impl(fsv_ctx* c, const fsv_config* cfg, int32_t* snapshots, int
     fa.hub_id = c->hub_id.p; fa.G_hub = c->G_hub.p; fa.H = c->H; fa.cnt = c->cnt.p;
     fa.partials = c->partials.p; fa.ticket = c->ticket.p; fa.done = c->done.p; fa.max_iter = cap;
     fa.dl = delta_out(c);
+    fa.lc = loop_ctl(c, graph_mode ? 2 : 0);
     k_first<<<vertex_grid(c), SC_THREADS, 0, st>>>(fa);
   }
   pmark(c, 1, 7);
@@ -830,8 +904,24 @@ static int solve_impl(fsv_ctx* c, const fsv_config* cfg, int32_t* snapshots, int
   }
   int launched = 1;  // iterations queued so far (k_first is iteration 1)
   int done = 0;
+  if (graph_mode) {
+    CUDA_TRY(cudaGraphLaunch(c->graph_exec, st));
+    CUDA_TRY(cudaMemcpyAsync(c->h_done, c->done.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    ++c->host_syncs;
+    done = *c->h_done;
+    if (done == 0) return fail(FSV_ERR_RUNTIME, "graph loop ended without convergence");
+    {
+      // kernels the graph ran: each body pass is two iterations' worth
+      const int it = done > 0 ? done : -done;
+      const int passes = std::max(1, it / 2);
+      c->launches += passes * 2 * (2 + (c->H ? 1 : 0));
+    }
+    if (done > 0 && (rc = ensure_events(c, (size_t)done + 1))) return rc;
+    if (done > 0) CUDA_TRY(cudaEventRecord(c->events[done], st));
+  }
   bool first_round = true;
-  for (;;) {
+  while (!graph_mode) {
     // the first round also holds iteration 1, so it queues batch-1 more
     const int more = first_round ? batch - 1 : batch;
     first_round = false;
@@ -847,8 +937,7 @@ static int solve_impl(fsv_ctx* c, const fsv_config* cfg, int32_t* snapshots, int
     ++c->host_syncs;
     done = *c->h_done;
     if (snapshots && (done == 0 || done == launched)) {
-      // batch == 1: iteration `launched` has committed f_k; copy it unless the
-      // flag says an earlier iteration converged (cannot happen with batch 1)
+      // batch == 1: iteration `launched` has committed f_k
       if (launched > 1) {
         if (launched > snap_cap) return fail(FSV_ERR_CONTRACT, "more than %d iterations ran", snap_cap);
         if ((rc = copy_snapshot(c, launched, snapshots + (size_t)(launched - 1) * c->n))) return rc;
@@ -869,8 +958,12 @@ static int solve_impl(fsv_ctx* c, const fsv_config* cfg, int32_t* snapshots, int
   c->h_mode.assign((size_t)iters + 1, 0);
   CUDA_TRY(cudaMemcpy(c->h_mode.data(), c->mode.p, sizeof(int) * (iters + 1), cudaMemcpyDeviceToHost));
   c->iter_ms.assign(iters, 0.f);
-  for (int k = 1; k <= iters; ++k)
-    CUDA_TRY(cudaEventElapsedTime(&c->iter_ms[k - 1], c->events[k - 1], c->events[k]));
+  {
+    std::vector<unsigned long long> ts((size_t)iters + 1, 0ull);
+    CUDA_TRY(cudaMemcpy(ts.data(), c->tstamp.p, sizeof(unsigned long long) * (iters + 1),
+                        cudaMemcpyDeviceToHost));
+    for (int k = 1; k <= iters; ++k) c->iter_ms[k - 1] = (float)((double)(ts[k] - ts[k - 1]) * 1e-6);
+  }
   CUDA_TRY(cudaEventElapsedTime(&c->solve_ms, c->events[0], c->events[iters]));
   if (c->profile) {
     auto span = [&](int k, int a, int b) {

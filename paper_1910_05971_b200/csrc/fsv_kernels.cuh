@@ -91,6 +91,36 @@ __device__ __forceinline__ void red_min(int* p, int v) {
 
 // ---- argument blocks --------------------------------------------------------
 
+// Device-side loop control. Graph mode runs the iteration loop inside a
+// CUDA-graph conditional WHILE node: kernels read the iteration number from
+// *iterp, the vertex pass's last block advances it and sets the condition.
+struct LoopCtl {
+  int* iterp;                        // graph mode: current iteration (>= 2)
+  unsigned long long* cnt_base;      // counters of iteration 1 (NCOUNT per iteration)
+  unsigned long long* tstamp;        // per-iteration end time (%globaltimer, ns)
+  unsigned long long cond;           // cudaGraphConditionalHandle
+  int graph;                         // 0 host loop, 1 inside the graph, 2 k_first before it
+};
+
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__device__ __forceinline__ int loop_iter(const LoopCtl& lc, int iter) {
+  return lc.graph == 1 ? *(volatile const int*)lc.iterp : iter;
+}
+
+// Early exit after convergence: in graph mode the loop condition must drop.
+__device__ __forceinline__ bool converged_exit(const int* done, const LoopCtl& lc) {
+  if (*(volatile const int*)done) {
+    if (lc.graph == 1 && blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(lc.cond, 0u);
+    return true;
+  }
+  return false;
+}
+
 // Sparse iteration (push). Phase 1 turns the delta list into batches of 32
 // vertices (descriptor per vertex: row start, exclusive prefix of degrees
 // within the batch, gf) and cuts each batch's flattened entry range into
@@ -139,6 +169,7 @@ struct HookArgs {
   const int* mode;        // mode[iter]: 0 dense pull (this layout), 1 sparse push
   int iter;
   PushArgs push;
+  LoopCtl lc;
 };
 
 // Changed-gf ("delta") list written by the vertex pass: warp w owns
@@ -171,6 +202,7 @@ struct ShortcutArgs {
   int iter;               // 1-based iteration number
   int max_iter;           // stop flag raised when reached without converging
   DeltaOut dl;            // changed-gf list for a following sparse iteration
+  LoopCtl lc;
 };
 
 // ---- emission of one hook contribution -------------------------------------
@@ -346,6 +378,16 @@ __device__ __forceinline__ void push_run(const PushArgs& a, long long* w_start, 
 __global__ void __launch_bounds__(HOOK_THREADS, 1) k_hook(HookArgs a) {
   extern __shared__ int s_hub[];
   if (*(volatile const int*)a.done) return;
+  if (a.lc.graph == 1) {
+    const int it = loop_iter(a.lc, a.iter);
+    unsigned long long* slot = a.lc.cnt_base + (size_t)(it - 1) * NCOUNT;
+    a.iter = it;
+    a.push.iter = it;
+    a.push.flops = slot + C_FLOPS;
+    a.push.nchunks = slot + C_CHUNKS;
+    a.push.nbatches = slot + C_BATCHES;
+    a.push.barrier = reinterpret_cast<unsigned*>(slot + C_BARRIER);
+  }
   if (a.mode[a.iter] == 1) {
     // sparse iteration: push from the vertices whose gf changed
     __shared__ long long s_start[HOOK_THREADS];
@@ -520,8 +562,9 @@ __global__ void __launch_bounds__(HOOK_THREADS, 1) k_hook(HookArgs a) {
 
 __global__ void k_hubfix(int* __restrict__ hub_acc, const int* __restrict__ hub_id, int H,
                          const int* __restrict__ F, const int* __restrict__ G, int* __restrict__ N,
-                         const int* done, const int* mode, int iter) {
+                         const int* done, const int* mode, int iter, const int* iterp) {
   if (*(volatile const int*)done) return;
+  if (iterp) iter = *(volatile const int*)iterp;
   if (mode[iter] != 0) return;
   for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < H; s += gridDim.x * blockDim.x) {
     const int acc = hub_acc[s];
@@ -541,7 +584,7 @@ template <int NT>
 __device__ __forceinline__ void finish_counters(const unsigned (&c)[5], unsigned* partials,
                                                 unsigned long long* cnt, unsigned int* ticket,
                                                 int* done, int iter, int max_iter,
-                                                const DeltaOut& dl) {
+                                                const DeltaOut& dl, const LoopCtl& lc) {
   __shared__ unsigned s_part[NT / 32][5];
   __shared__ bool s_last;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -583,8 +626,13 @@ __device__ __forceinline__ void finish_counters(const unsigned (&c)[5], unsigned
     for (int i = 0; i < NT / 32; ++i) sum += s_acc[i][threadIdx.x];
     cnt[threadIdx.x] = sum;
     if (threadIdx.x == C_GF) {
+      bool stop = true;
       if (sum == 0ull) atomicExch(done, iter);
       else if (max_iter > 0 && iter >= max_iter) atomicExch(done, -iter);
+      else stop = false;
+      lc.tstamp[iter] = global_ns();
+      if (lc.graph) *lc.iterp = iter + 1;                       // 2: iteration 1 before the graph
+      if (lc.graph == 1) cudaGraphSetConditional(lc.cond, stop ? 0u : 1u);
       // product choice for the next iteration (choose_kernel, driver.py:51-61)
       int m = 0;
       if (dl.policy == 2) m = 1;
@@ -658,7 +706,11 @@ __device__ __forceinline__ void tail_append(long long n4, long long n, Fn&& one,
 }
 
 __global__ void __launch_bounds__(SC_THREADS) k_shortcut(ShortcutArgs a) {
-  if (*(volatile const int*)a.done) return;
+  if (converged_exit(a.done, a.lc)) return;
+  if (a.lc.graph == 1) {
+    a.iter = loop_iter(a.lc, a.iter);
+    a.cnt = a.lc.cnt_base + (size_t)(a.iter - 1) * NCOUNT;
+  }
   unsigned c[5] = {0u, 0u, 0u, 0u, 0u};
   const long long stride = (long long)gridDim.x * blockDim.x;
   const long long t0 = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -694,7 +746,7 @@ __global__ void __launch_bounds__(SC_THREADS) k_shortcut(ShortcutArgs a) {
     const int h = ldg(a.hub_id + s);
     a.G_hub[s] = ldg(N + ldg(N + h));
   }
-  finish_counters<SC_THREADS>(c, a.partials, a.cnt, a.ticket, a.done, a.iter, a.max_iter, a.dl);
+  finish_counters<SC_THREADS>(c, a.partials, a.cnt, a.ticket, a.done, a.iter, a.max_iter, a.dl, a.lc);
 }
 
 // ---- iteration 1 in closed form ---------------------------------------------
@@ -715,6 +767,7 @@ struct FirstArgs {
   int* done;
   int max_iter;
   DeltaOut dl;
+  LoopCtl lc;
 };
 
 __global__ void __launch_bounds__(SC_THREADS) k_first(FirstArgs a) {
@@ -762,13 +815,13 @@ __global__ void __launch_bounds__(SC_THREADS) k_first(FirstArgs a) {
     const int h = ldg(a.hub_id + s);
     a.G_hub[s] = ldg(f1 + ldg(f1 + h));
   }
-  finish_counters<SC_THREADS>(c, a.partials, a.cnt, a.ticket, a.done, 1, a.max_iter, a.dl);
+  finish_counters<SC_THREADS>(c, a.partials, a.cnt, a.ticket, a.done, 1, a.max_iter, a.dl, a.lc);
 }
 
 // ---- solve-start initialisation ----------------------------------------------
 __global__ void k_solve_init(int* X, int* Y, int* G, long long n, int* hub_acc, int H,
                              unsigned long long* cnt, long long ncnt, int* done, unsigned* ticket,
-                             int* mode, int first_mode) {
+                             int* mode, int first_mode, unsigned long long* tstamp) {
   const long long t0 = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const long long stride = (long long)gridDim.x * blockDim.x;
   for (long long s = t0; s < H; s += stride) hub_acc[s] = INF;
@@ -777,6 +830,7 @@ __global__ void k_solve_init(int* X, int* Y, int* G, long long n, int* hub_acc, 
     X[n] = (int)n; Y[n] = (int)n; G[n] = INF;  // dummy vertex n of the padding row
     *done = 0; *ticket = 0u;
     mode[1] = first_mode;
+    tstamp[0] = global_ns();
   }
 }
 
