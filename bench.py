@@ -161,8 +161,9 @@ def run_reference(args, world, rank):
         "impl": "reference", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": step * 1e3, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "int64", "data": "synthetic (seeded generator, BASELINE config)",
-        "config": {"workload": f"config{args.config}", "n": n, "edges": edges, "m_dir": g.m,
-                   "iterations": iters},
+        "config": {"workload": f"config{args.config} (BASELINE.json configs[{args.config - 1}])",
+                   "n": n, "edges": edges, "m_dir": g.m, "iterations": iters,
+                   "parallelism": "host threads (reference CPU path)"},
         "cpu_baseline": {"value": val, "unit": "edges/s", "cores": cores, "kind": "port",
                          "sample": f"full solve of config {args.config} per step (numpy port of "
                                    "svcc.fastsv_la, auto kernel choice, workers=cores)"},
