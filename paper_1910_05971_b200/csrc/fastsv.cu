@@ -131,7 +131,7 @@ struct DBuf {
   ~DBuf() { free(); }
 };
 
-static constexpr int kHubMax = 49152;     // 192 KB of shared memory
+static constexpr int kHubMax = 57344;     // 224 KB of shared memory (the opt-in maximum is 227 KB)
 static constexpr int kHubMinDegree = 32;  // below this a hub slot buys nothing
 static constexpr int kTraceCap = 4096;    // iteration cap of the counter array
 
@@ -239,7 +239,7 @@ extern "C" int fsv_create(int device, fsv_ctx** out) {
     c->sc_grid = std::max(1, per_sm) * c->sm_count;
   }
   cudaError_t e = cudaFuncSetAttribute(k_hook, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       kHubMax * (int)sizeof(int));
+                                       std::max(kHubMax * (int)sizeof(int), PUSH_SCRATCH_BYTES));
   if (e != cudaSuccess) {
     delete c;
     return fail(FSV_ERR_RUNTIME, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
@@ -457,7 +457,7 @@ __global__ void k_span_row(const long long* __restrict__ nzoff, const int* __res
 // other rows get `outside` (INF before an allreduce-min assembles the global
 // vector, or u itself when there is no communicator).
 template <typename ColT>
-__global__ void k_f1(const int64_t* __restrict__ off, const ColT* __restrict__ cols,
+__global__ void k_f1(const int64_t* __restrict__ off, const ColT* __restrict__ cols,  // (ColT = int)
                      long long col_base, long long row_begin, long long row_end, long long n,
                      int* __restrict__ f1, bool outside_inf) {
   for (long long u = blockIdx.x * (long long)blockDim.x + threadIdx.x; u < n;
@@ -620,15 +620,8 @@ static int upload_impl(fsv_ctx* c, int64_t n, const int64_t* h_off, const ColT* 
   if (nspans)
     k_span_row<<<grid_for(c, nspans, 256), 256, 0, st>>>(nzoff.p, nzrows.p, R + 1, nspans, c->span_row.p);
 
-  // closed-form first iteration
+  // f_1 is computed by every solve (k_f1 in solve_impl), not cached here
   CUDA_TRY(c->f1.alloc((size_t)n + 64));
-  if (n)
-    k_f1<ColT><<<grid_for(c, n, 256), 256, 0, st>>>(d_off.p, d_cols.p, e_begin, row_begin, row_end, n,
-                                                    c->f1.p, c->comm != nullptr);
-  if (c->comm && n) {
-    NCCL_TRY(g_nccl.AllReduce(c->f1.p, c->f1.p, (size_t)n, ncclInt32, ncclMin, c->comm, st));
-    k_f1_fix<<<grid_for(c, n, 256), 256, 0, st>>>(c->f1.p, n);
-  }
 
   // keep the rank's symmetric columns (int32) for sparse iterations
   if constexpr (sizeof(ColT) != 4) {
@@ -774,8 +767,9 @@ static int launch_iteration(fsv_ctx* c, int k, int max_iter, bool graph = false)
     // for the grid barrier of the sparse (push) path
     pmark(c, k, 0);
     void* kargs[] = {&a};
+    const size_t dyn = std::max<size_t>((size_t)c->H * sizeof(int), PUSH_SCRATCH_BYTES);
     CUDA_TRY(cudaLaunchCooperativeKernel((const void*)k_hook, dim3(c->sm_count), dim3(HOOK_THREADS),
-                                         kargs, (size_t)c->H * sizeof(int), st));
+                                         kargs, dyn, st));
     pmark(c, k, 1);
     ++c->launches;
   }
@@ -885,6 +879,19 @@ static int solve_impl(fsv_ctx* c, const fsv_config* cfg, int32_t* snapshots, int
       c->X.p, c->Y.p, c->G.p, c->n, c->hub_acc.p, c->H, c->cnt.p, (long long)cap * NCOUNT, c->done.p,
       c->ticket.p, c->mode.p, c->policy == 2 ? 1 : 0, c->tstamp.p);
   pmark(c, 1, 6);
+  // iteration 1 in closed form: f_1[u] = min(u, smallest neighbour) from the
+  // resident CSR rows (first column of each sorted row), every solve
+  if (c->n) {
+    k_f1<int><<<grid_for(c, c->n, 256, 64), 256, 0, st>>>(c->csr_off.p, c->csr_cols.p, c->col_base,
+                                                      c->row_begin, c->row_end, c->n, c->f1.p,
+                                                      c->comm != nullptr);
+    ++c->launches;
+    if (c->comm) {
+      NCCL_TRY(g_nccl.AllReduce(c->f1.p, c->f1.p, (size_t)c->n, ncclInt32, ncclMin, c->comm, st));
+      k_f1_fix<<<grid_for(c, c->n, 256), 256, 0, st>>>(c->f1.p, c->n);
+      ++c->launches;
+    }
+  }
   {
     FirstArgs fa;
     fa.f1 = c->f1.p; fa.Y = c->Y.p; fa.G = c->G.p; fa.X = c->X.p; fa.n = c->n;

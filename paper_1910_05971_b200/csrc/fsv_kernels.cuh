@@ -61,6 +61,7 @@ constexpr int STEP = 32 * EPL;           // entries per warp step
 constexpr int STEPS = FSV_STEPS;         // steps per span
 constexpr int SPAN = STEP * STEPS;       // entries per warp task
 constexpr int HOOK_THREADS = FSV_HOOK_THREADS;
+constexpr int PUSH_SCRATCH_BYTES = HOOK_THREADS * 20;  // s_start, s_excl (8 B) + s_val (4 B)
 constexpr int SC_THREADS = 512;
 constexpr int NCOUNT = 16;               // counter slots per iteration
 enum { C_GF = 0, C_F = 1, C_NONSTAR = 2, C_ROOTS = 3, C_VIOL = 4,   // vertex-pass counters
@@ -389,10 +390,11 @@ __global__ void __launch_bounds__(HOOK_THREADS, 1) k_hook(HookArgs a) {
     a.push.barrier = reinterpret_cast<unsigned*>(slot + C_BARRIER);
   }
   if (a.mode[a.iter] == 1) {
-    // sparse iteration: push from the vertices whose gf changed
-    __shared__ long long s_start[HOOK_THREADS];
-    __shared__ long long s_excl[HOOK_THREADS];
-    __shared__ int s_val[HOOK_THREADS];
+    // sparse iteration: push from the vertices whose gf changed; the push
+    // scratch aliases the (unused) hub table in dynamic shared memory
+    long long* s_start = reinterpret_cast<long long*>(s_hub);
+    long long* s_excl = s_start + HOOK_THREADS;
+    int* s_val = reinterpret_cast<int*>(s_excl + HOOK_THREADS);
     const int wib = threadIdx.x >> 5;
     DBG_T(0);
     push_plan(a.push);
