@@ -471,6 +471,34 @@ __global__ void k_f1(const int64_t* __restrict__ off, const ColT* __restrict__ c
   }
 }
 
+// In-solve f_1 for the full single-rank row range: 4 vertices per thread,
+// offsets as two 16-byte loads, the four first-column loads in flight together.
+__global__ void k_f1_solve(const int64_t* __restrict__ off, const int* __restrict__ cols, long long n,
+                           int* __restrict__ f1) {
+  const long long n4 = n >> 2;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i <= n4;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long u0 = i << 2;
+    if (u0 + 4 <= n) {
+      const longlong2 a = *reinterpret_cast<const longlong2*>(off + u0);   // off[u0], off[u0+1]
+      const longlong2 b = *reinterpret_cast<const longlong2*>(off + u0 + 2);
+      const long long e4 = off[u0 + 4];
+      const long long o[5] = {a.x, a.y, b.x, b.y, e4};
+      int4 r;
+      int* rp = reinterpret_cast<int*>(&r);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int c = o[j + 1] > o[j] ? __ldg(cols + o[j]) : INF;
+        rp[j] = min((int)(u0 + j), c);
+      }
+      *reinterpret_cast<int4*>(f1 + u0) = r;
+    } else {
+      for (long long u = u0; u < n; ++u)
+        f1[u] = off[u + 1] > off[u] ? min((int)u, cols[off[u]]) : (int)u;
+    }
+  }
+}
+
 // rows no rank owned stay isolated (never index with INF)
 __global__ void k_f1_fix(int* __restrict__ f1, long long n) {
   for (long long u = blockIdx.x * (long long)blockDim.x + threadIdx.x; u < n;
@@ -881,7 +909,11 @@ static int solve_impl(fsv_ctx* c, const fsv_config* cfg, int32_t* snapshots, int
   pmark(c, 1, 6);
   // iteration 1 in closed form: f_1[u] = min(u, smallest neighbour) from the
   // resident CSR rows (first column of each sorted row), every solve
-  if (c->n) {
+  if (c->n && !c->comm && c->row_begin == 0 && c->row_end == c->n) {
+    k_f1_solve<<<grid_for(c, c->n / 4 + 1, 256, 32), 256, 0, st>>>(c->csr_off.p, c->csr_cols.p, c->n,
+                                                                   c->f1.p);
+    ++c->launches;
+  } else if (c->n) {
     k_f1<int><<<grid_for(c, c->n, 256, 64), 256, 0, st>>>(c->csr_off.p, c->csr_cols.p, c->col_base,
                                                       c->row_begin, c->row_end, c->n, c->f1.p,
                                                       c->comm != nullptr);
