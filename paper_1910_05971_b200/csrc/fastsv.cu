@@ -21,6 +21,7 @@
 #include <algorithm>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -140,6 +141,8 @@ struct fsv_ctx {
   int sm_count = 148;
   cudaStream_t own_stream = nullptr;
   cudaStream_t stream = nullptr;
+  cudaStream_t copy_stream = nullptr;            // upload: column chunks H2D
+  std::vector<cudaEvent_t> chunk_ev;             // one per column chunk
   // graph layout
   bool ready = false;
   int64_t n = 0, m_dir = 0, E = 0, Epad = 0;
@@ -163,6 +166,9 @@ struct fsv_ctx {
     DBuf<unsigned char> tmp;
     DBuf<int64_t> cols64;
     DBuf<uint32_t> etmp;
+    DBuf<int4> pieces;
+    DBuf<long long> hrow;
+    DBuf<unsigned long long> hkept, hcursor;
   } ws;
   long long rcap = 0;
   int dgrid = 1;
@@ -233,6 +239,10 @@ extern "C" int fsv_create(int device, fsv_ctx** out) {
     return fail(FSV_ERR_RUNTIME, "stream/pinned allocation failed");
   }
   c->stream = c->own_stream;
+  if (cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking) != cudaSuccess) {
+    delete c;
+    return fail(FSV_ERR_RUNTIME, "copy stream creation failed");
+  }
   {
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_shortcut, SC_THREADS, 0);
@@ -258,6 +268,8 @@ extern "C" int fsv_destroy(fsv_ctx* c) {
   if (c->graph) cudaGraphDestroy(c->graph);
   if (c->comm && g_nccl.CommDestroy) g_nccl.CommDestroy(c->comm);
   if (c->h_done) cudaFreeHost(c->h_done);
+  for (auto e : c->chunk_ev) cudaEventDestroy(e);
+  if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
   if (c->own_stream) cudaStreamDestroy(c->own_stream);
   delete c;
   return FSV_OK;
@@ -297,6 +309,8 @@ __global__ void k_positions(const int* __restrict__ sorted_ids, long long n, int
 }
 
 constexpr uint32_t DROP = 0xffffffffu;
+constexpr long long HUGE_ROW = 4096;  // rows longer than this are cut into pieces
+constexpr long long PIECE = 4096;     // entries per piece
 
 __device__ __forceinline__ uint32_t encode_col(int v, int pv, int H) {
   return pv < H ? (HUB | (uint32_t)pv) : (uint32_t)v;
@@ -327,19 +341,31 @@ __global__ void k_orient_encode(const int64_t* __restrict__ off, const ColT* __r
       hi = off[u + 1] - col_base;
       pu = pos[u];
     }
+    const bool huge = hi - lo > HUGE_ROW;        // cut into pieces (k_piece_encode)
+    if (huge) hi = lo;
     const bool is_long = hi - lo > 32;
     long long k = 0;
     if (!is_long) {
-      for (long long e = lo; e < hi; ++e) {
-        const long long v = (long long)cols[e];
-        uint32_t code = DROP;
-        if (v < 0 || v >= n) {
-          atomicMin(bad, (unsigned long long)e);
-        } else {
-          const int pv = pos[v];
-          if (pv < pu) { code = encode_col((int)v, pv, H); ++k; }
+      // 4 entries of the lane's row in flight (column loads, then pos gathers)
+      for (long long e = lo; e < hi; e += 4) {
+        long long v[4];
+        int pv[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) v[q] = e + q < hi ? (long long)cols[e + q] : 0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) pv[q] = (e + q < hi && v[q] >= 0 && v[q] < n) ? pos[v[q]] : INF;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          if (e + q >= hi) break;
+          uint32_t code = DROP;
+          if (v[q] < 0 || v[q] >= n) {
+            atomicMin(bad, (unsigned long long)(e + q));
+          } else if (pv[q] < pu) {
+            code = encode_col((int)v[q], pv[q], H);
+            ++k;
+          }
+          tmp[e + q] = code;
         }
-        tmp[e] = code;
       }
     }
     unsigned lm = __ballot_sync(0xffffffffu, is_long);
@@ -364,9 +390,117 @@ __global__ void k_orient_encode(const int64_t* __restrict__ off, const ColT* __r
       for (int o = 16; o; o >>= 1) sk += __shfl_xor_sync(0xffffffffu, sk, o);
       if (lane == src) k = sk;
     }
-    if (r < rows) {
+    if (r < rows && !huge) {
       cnt[r] = k ? k + 1 : 0;  // + header entry
       nzflag[r] = k > 0;
+    }
+  }
+}
+
+// Pieces of rows longer than HUGE_ROW: one warp per piece (listed by the
+// host), 8 entries per lane in flight; kept counts summed per row.
+__global__ void k_find_huge(const int64_t* __restrict__ off, long long row_begin, long long rows,
+                            long long* __restrict__ hrow, int4* __restrict__ pieces,
+                            unsigned long long* ctr) {
+  for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < rows;
+       r += (long long)gridDim.x * blockDim.x) {
+    const long long u = row_begin + r;
+    const long long d = off[u + 1] - off[u];
+    if (d <= HUGE_ROW) continue;
+    const int np = (int)((d + PIECE - 1) / PIECE);
+    const int h = (int)atomicAdd(ctr, 1ull);
+    const unsigned long long b = atomicAdd(ctr + 1, (unsigned long long)np);
+    hrow[h] = r;
+    for (int j = 0; j < np; ++j) pieces[b + j] = make_int4((int)u, j, j + 1, h);
+  }
+}
+
+template <typename ColT>
+__global__ void k_piece_encode(const int4* __restrict__ pieces, const unsigned long long* npieces_p,
+                               const int64_t* __restrict__ off,
+                               const ColT* __restrict__ cols, long long col_base, long long n,
+                               const int* __restrict__ pos, int H, uint32_t* __restrict__ tmp,
+                               unsigned long long* __restrict__ row_kept, unsigned long long* bad) {
+  const int lane = threadIdx.x & 31;
+  const long long nw = (long long)gridDim.x * (blockDim.x >> 5);
+  const long long npieces = (long long)*npieces_p;
+  for (long long q = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); q < npieces; q += nw) {
+    const int4 pc = pieces[q];                      // (row u, piece start, piece end, huge-row index)
+    const int u = pc.x;
+    const long long base = off[u] - col_base;
+    const long long lo = base + (long long)pc.y * PIECE, hi = min(base + (long long)pc.z * PIECE,
+                                                                  off[u + 1] - col_base);
+    const int pu = pos[u];
+    unsigned long long k = 0;
+    for (long long e0 = lo; e0 < hi; e0 += 8 * 32) {
+      long long v[8];
+      int pv[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const long long e = e0 + lane + 32 * j;
+        v[j] = e < hi ? (long long)cols[e] : -2;
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) pv[j] = (v[j] >= 0 && v[j] < n) ? pos[v[j]] : INF;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const long long e = e0 + lane + 32 * j;
+        if (e >= hi) continue;
+        uint32_t code = DROP;
+        if (v[j] < 0 || v[j] >= n) atomicMin(bad, (unsigned long long)e);
+        else if (pv[j] < pu) { code = encode_col((int)v[j], pv[j], H); ++k; }
+        tmp[e] = code;
+      }
+    }
+    for (int o = 16; o; o >>= 1) k += __shfl_xor_sync(0xffffffffu, k, o);
+    if (lane == 0 && k) atomicAdd(row_kept + pc.w, k);
+  }
+}
+
+// Huge rows: per-row counts from the pieces (+ header), and the output
+// cursor for k_piece_compact; `hrow[i]` = (row - row_begin) of huge row i.
+__global__ void k_huge_rows(const long long* __restrict__ hrow, const unsigned long long* nh_p,
+                            const unsigned long long* row_kept, long long* __restrict__ cnt,
+                            int* __restrict__ nzflag) {
+  const long long nh = (long long)*nh_p;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < nh;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long k = (long long)row_kept[i];
+    cnt[hrow[i]] = k ? k + 1 : 0;
+    nzflag[hrow[i]] = k > 0;
+  }
+}
+
+__global__ void k_piece_compact(const int4* __restrict__ pieces, const unsigned long long* npieces_p,
+                                const int64_t* __restrict__ off,
+                                long long col_base, const uint32_t* __restrict__ tmp,
+                                const long long* __restrict__ hrow, const long long* __restrict__ out_off,
+                                unsigned long long* __restrict__ cursor, uint32_t* __restrict__ ecol) {
+  const int lane = threadIdx.x & 31;
+  const long long nw = (long long)gridDim.x * (blockDim.x >> 5);
+  const long long npieces = (long long)*npieces_p;
+  for (long long q = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); q < npieces; q += nw) {
+    const int4 pc = pieces[q];
+    const int u = pc.x;
+    const long long base = off[u] - col_base;
+    const long long lo = base + (long long)pc.y * PIECE, hi = min(base + (long long)pc.z * PIECE,
+                                                                  off[u + 1] - col_base);
+    // count kept, reserve a contiguous slot range of the row, write in order
+    unsigned long long k = 0;
+    for (long long e = lo + lane; e < hi; e += 32) k += tmp[e] != DROP;
+    for (int o = 16; o; o >>= 1) k += __shfl_xor_sync(0xffffffffu, k, o);
+    unsigned long long o0 = 0;
+    if (lane == 0 && k) o0 = atomicAdd(cursor + pc.w, k);
+    o0 = __shfl_sync(0xffffffffu, o0, 0);
+    const long long dst = out_off[hrow[pc.w]] + 1 + (long long)o0;
+    long long o = 0;
+    for (long long e0 = lo; e0 < hi; e0 += 32) {
+      const long long e = e0 + lane;
+      const uint32_t code = e < hi ? tmp[e] : DROP;
+      const bool keep = code != DROP;
+      const unsigned b = __ballot_sync(0xffffffffu, keep);
+      if (keep) ecol[dst + o + __popc(b & ((1u << lane) - 1u))] = code;
+      o += __popc(b);
     }
   }
 }
@@ -398,12 +532,17 @@ __global__ void k_orient_compact(const int64_t* __restrict__ off, long long col_
         nzoff[z] = o0;
       }
     }
+    if (hi - lo > HUGE_ROW) hi = lo;     // entries placed by k_piece_compact
     const bool is_long = has && hi - lo > 32;
     if (has && !is_long) {
       long long o = o0 + 1;
-      for (long long e = lo; e < hi; ++e) {
-        const uint32_t code = tmp[e];
-        if (code != DROP) ecol[o++] = code;
+      for (long long e = lo; e < hi; e += 4) {
+        uint32_t code[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) code[q] = e + q < hi ? tmp[e + q] : DROP;
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (code[q] != DROP) ecol[o++] = code[q];
       }
     }
     unsigned lm = __ballot_sync(0xffffffffu, is_long);
@@ -548,12 +687,66 @@ static int upload_impl(fsv_ctx* c, int64_t n, const int64_t* h_off, const ColT* 
   c->graph_dirty = true;
 
   const long long rows = row_end - row_begin;
+  const bool udbg = getenv("FSV_UPLOAD_DEBUG") != nullptr;
+  cudaEvent_t uev[8];
+  if (udbg) for (auto& e : uev) cudaEventCreate(&e);
+  auto umark = [&](int i) { if (udbg) cudaEventRecord(uev[i], st); };
+  umark(0);
+  std::vector<cudaEvent_t> dbg_copy_ev, dbg_enc_ev;
   DBuf<int64_t>& d_off = c->csr_off;
   DBuf<ColT>& d_cols = cols_buffer<ColT>(c);
   CUDA_TRY(d_off.alloc((size_t)n + 1));
   CUDA_TRY(d_cols.alloc((size_t)mloc));
   CUDA_TRY(cudaMemcpyAsync(d_off.p, h_off, sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice, st));
-  if (mloc) CUDA_TRY(cudaMemcpyAsync(d_cols.p, h_cols, sizeof(ColT) * mloc, cudaMemcpyHostToDevice, st));
+  // columns go up in row-aligned chunks on the copy stream, so the degree
+  // sort and the orientation of earlier chunks overlap the transfer
+  std::vector<int64_t> chunk_rows;  // row boundaries, chunk k = [chunk_rows[k], chunk_rows[k+1])
+  {
+    int K = mloc >= ((int64_t)1 << 24) ? 8 : 1;
+    if (const char* env = getenv("FSV_UPLOAD_CHUNKS")) K = std::max(1, std::min(64, atoi(env)));
+    chunk_rows.push_back(row_begin);
+    for (int k = 1; k < K; ++k) {
+      const int64_t target = e_begin + mloc * k / K;
+      int64_t r = std::lower_bound(h_off + row_begin, h_off + row_end, target) - h_off;
+      r = std::max<int64_t>(r, chunk_rows.back());
+      chunk_rows.push_back(std::min<int64_t>(r, row_end));
+    }
+    chunk_rows.push_back(row_end);
+    while (c->chunk_ev.size() < (size_t)K) {
+      cudaEvent_t e;
+      CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      c->chunk_ev.push_back(e);
+    }
+    cudaEvent_t off_ready = c->chunk_ev[0];
+    CUDA_TRY(cudaEventRecord(off_ready, st));              // d_off allocation/reuse ordering
+    CUDA_TRY(cudaStreamWaitEvent(c->copy_stream, off_ready, 0));
+    for (int k = 0; k < K; ++k) {
+      const int64_t lo = h_off[chunk_rows[k]] - e_begin, hi = h_off[chunk_rows[k + 1]] - e_begin;
+      if (hi > lo)
+        CUDA_TRY(cudaMemcpyAsync(d_cols.p + lo, h_cols + lo, sizeof(ColT) * (hi - lo),
+                                 cudaMemcpyHostToDevice, c->copy_stream));
+      CUDA_TRY(cudaEventRecord(c->chunk_ev[k], c->copy_stream));
+      if (udbg) {
+        cudaEvent_t e; cudaEventCreate(&e); cudaEventRecord(e, c->copy_stream);
+        dbg_copy_ev.push_back(e);
+      }
+    }
+  }
+  // rows longer than HUGE_ROW are cut into PIECE-entry pieces so no single
+  // warp walks a whole hub row; the list is built on the device from the
+  // offsets (which arrive first), counts stay on the device
+  const long long max_huge = mloc / HUGE_ROW + 1;
+  const long long max_pieces = mloc / PIECE + max_huge + 1;
+  CUDA_TRY(c->ws.pieces.alloc((size_t)max_pieces));
+  CUDA_TRY(c->ws.hrow.alloc((size_t)max_huge));
+  CUDA_TRY(c->ws.hkept.alloc((size_t)max_huge + 2));   // [0..max_huge) kept, then 2 counters
+  CUDA_TRY(c->ws.hcursor.alloc((size_t)max_huge));
+  CUDA_TRY(cudaMemsetAsync(c->ws.hkept.p, 0, sizeof(unsigned long long) * (max_huge + 2), st));
+  CUDA_TRY(cudaMemsetAsync(c->ws.hcursor.p, 0, sizeof(unsigned long long) * max_huge, st));
+  unsigned long long* huge_ctr = c->ws.hkept.p + max_huge;      // [0] huge rows, [1] pieces
+  if (rows)
+    k_find_huge<<<grid_for(c, rows, 256), 256, 0, st>>>(d_off.p, row_begin, rows, c->ws.hrow.p,
+                                                        c->ws.pieces.p, huge_ctr);
 
   // degrees (+ offsets check), stable degree order, positions, hubs
   DBuf<unsigned long long>& d_bad = c->ws.bad;
@@ -593,6 +786,7 @@ static int upload_impl(fsv_ctx* c, int64_t n, const int64_t* h_off, const ColT* 
   c->H = H;
   CUDA_TRY(c->hub_id.alloc(std::max(H, 4)));
   if (n) k_positions<<<grid_for(c, n, 256), 256, 0, st>>>(ids_sorted.p, n, H, pos.p, c->hub_id.p);
+  umark(1);
 
   // orientation: encode (one gather per entry), scan, compact
   auto& cnt = c->ws.cnt;
@@ -605,9 +799,25 @@ static int upload_impl(fsv_ctx* c, int64_t n, const int64_t* h_off, const ColT* 
   CUDA_TRY(etmp.alloc((size_t)std::max<int64_t>(mloc, 1)));
   CUDA_TRY(cudaMemsetAsync(cnt.p + rows, 0, sizeof(long long), st));
   CUDA_TRY(cudaMemsetAsync(nzflag.p + rows, 0, sizeof(int), st));
-  if (rows)
-    k_orient_encode<ColT><<<grid_for(c, (rows + 31) / 32 * 32, 256, 16), 256, 0, st>>>(
-        d_off.p, d_cols.p, e_begin, row_begin, rows, n, pos.p, H, etmp.p, cnt.p, nzflag.p, d_bad.p);
+  umark(2);
+  for (size_t k = 0; k + 1 < chunk_rows.size(); ++k) {
+    const long long r0 = chunk_rows[k], nr = chunk_rows[k + 1] - chunk_rows[k];
+    CUDA_TRY(cudaStreamWaitEvent(st, c->chunk_ev[k], 0));
+    if (nr)
+      k_orient_encode<ColT><<<grid_for(c, (nr + 31) / 32 * 32, 256, 16), 256, 0, st>>>(
+          d_off.p, d_cols.p, e_begin, r0, nr, n, pos.p, H, etmp.p, cnt.p + (r0 - row_begin),
+          nzflag.p + (r0 - row_begin), d_bad.p);
+    if (udbg) {
+      cudaEvent_t e; cudaEventCreate(&e); cudaEventRecord(e, st);
+      dbg_enc_ev.push_back(e);
+    }
+  }
+  if (rows) {
+    k_piece_encode<ColT><<<c->sm_count * 16, 256, 0, st>>>(
+        c->ws.pieces.p, huge_ctr + 1, d_off.p, d_cols.p, e_begin, n, pos.p, H, etmp.p, c->ws.hkept.p, d_bad.p);
+    k_huge_rows<<<c->sm_count * 2, 256, 0, st>>>(c->ws.hrow.p, huge_ctr, c->ws.hkept.p, cnt.p, nzflag.p);
+  }
+  umark(3);
   {
     size_t b1 = 0, b2 = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, b1, cnt.p, out_off.p, (int)(rows + 1), st);
@@ -638,15 +848,21 @@ static int upload_impl(fsv_ctx* c, int64_t n, const int64_t* h_off, const ColT* 
   CUDA_TRY(nzrows.alloc((size_t)R + 1));
   auto& nzoff = c->ws.nzoff;
   CUDA_TRY(nzoff.alloc((size_t)R + 1));
+  umark(4);
   if (rows)
     k_orient_compact<<<grid_for(c, (rows + 31) / 32 * 32, 256, 16), 256, 0, st>>>(
         d_off.p, e_begin, row_begin, rows, etmp.p, out_off.p, nzidx.p, c->ecol.p, nzrows.p, nzoff.p);
+  if (rows)
+    k_piece_compact<<<c->sm_count * 16, 256, 0, st>>>(
+        c->ws.pieces.p, huge_ctr + 1, d_off.p, e_begin, etmp.p, c->ws.hrow.p, out_off.p, c->ws.hcursor.p,
+        c->ecol.p);
   k_pad<<<grid_for(c, std::max<long long>(Epad - E, 1), 256), 256, 0, st>>>(c->ecol.p, E, Epad, (int)n,
                                                                              nzrows.p, R, nzoff.p);
   const long long nspans = Epad / SPAN;
   CUDA_TRY(c->span_row.alloc((size_t)std::max<long long>(nspans, 1)));
   if (nspans)
     k_span_row<<<grid_for(c, nspans, 256), 256, 0, st>>>(nzoff.p, nzrows.p, R + 1, nspans, c->span_row.p);
+  umark(5);
 
   // f_1 is computed by every solve (k_f1 in solve_impl), not cached here
   CUDA_TRY(c->f1.alloc((size_t)n + 64));
@@ -685,8 +901,25 @@ static int upload_impl(fsv_ctx* c, int64_t n, const int64_t* h_off, const ColT* 
     CUDA_TRY(c->chunks.alloc((size_t)(mloc / PUSH_CHUNK + max_batches + 64)));
   }
   CUDA_TRY(c->cnt.alloc((size_t)kTraceCap * NCOUNT));
+  umark(6);
   CUDA_TRY(cudaStreamSynchronize(st));
   CUDA_TRY(cudaGetLastError());
+  if (udbg) {
+    const char* names[] = {"degrees+sort+positions", "(wait cols) ", "encode", "scans+readback", "compact+pad+spans",
+                           "tail (narrow, allocs)"};
+    for (int i = 0; i < 6; ++i) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, uev[i], uev[i + 1]);
+      fprintf(stderr, "[upload] %-24s %8.3f ms\n", names[i], ms);
+    }
+    for (size_t k = 0; k < dbg_copy_ev.size(); ++k) {
+      float a = 0.f, b = 0.f;
+      cudaEventElapsedTime(&a, uev[0], dbg_copy_ev[k]);
+      if (k < dbg_enc_ev.size()) cudaEventElapsedTime(&b, uev[0], dbg_enc_ev[k]);
+      fprintf(stderr, "[upload] chunk %zu copied at %8.3f ms, encoded at %8.3f ms\n", k, a, b);
+    }
+    for (auto& e : uev) cudaEventDestroy(e);
+  }
 
   c->n = n;
   c->m_dir = h_off[n];
