@@ -134,6 +134,9 @@ struct DBuf {
 
 static constexpr int kHubMax = 57344;     // 224 KB of shared memory (the opt-in maximum is 227 KB)
 static constexpr int kHubMinDegree = 32;  // below this a hub slot buys nothing
+static constexpr long long kTierMinN = 1LL << 23;   // rank tier only when the vectors overflow L2
+static constexpr int kTierMinDegree = 8;
+static constexpr long long kTierMax = 8LL << 20;    // 32 MB of gf + 32 MB of accumulators
 static constexpr int kTraceCap = 4096;    // iteration cap of the counter array
 
 struct fsv_ctx {
@@ -146,7 +149,7 @@ struct fsv_ctx {
   // graph layout
   bool ready = false;
   int64_t n = 0, m_dir = 0, E = 0, Epad = 0;
-  int R = 0, H = 0;
+  int R = 0, H = 0, HT = 0;   // shared-memory hub slots, all tier slots
   DBuf<uint32_t> ecol;
   DBuf<int> span_row, hub_id, f1;
   // full symmetric CSR of this rank's rows, for sparse (push) iterations
@@ -248,8 +251,11 @@ extern "C" int fsv_create(int device, fsv_ctx** out) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_shortcut, SC_THREADS, 0);
     c->sc_grid = std::max(1, per_sm) * c->sm_count;
   }
-  cudaError_t e = cudaFuncSetAttribute(k_hook, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  cudaError_t e = cudaFuncSetAttribute(k_hook<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        std::max(kHubMax * (int)sizeof(int), PUSH_SCRATCH_BYTES));
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(k_hook<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             std::max(kHubMax * (int)sizeof(int), PUSH_SCRATCH_BYTES));
   if (e != cudaSuccess) {
     delete c;
     return fail(FSV_ERR_RUNTIME, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
@@ -306,6 +312,17 @@ __global__ void k_positions(const int* __restrict__ sorted_ids, long long n, int
     pos[v] = (int)i;
     if (i < H) hub_id[i] = v;
   }
+}
+
+// number of leading entries >= thr in a descending array (one warp, binary search)
+__global__ void k_count_ge(const int* __restrict__ sorted_desc, long long n, int thr, long long* out) {
+  if (threadIdx.x != 0) return;
+  long long lo = 0, hi = n;
+  while (lo < hi) {
+    const long long mid = (lo + hi) >> 1;
+    if (sorted_desc[mid] >= thr) lo = mid + 1; else hi = mid;
+  }
+  *out = lo;
 }
 
 constexpr uint32_t DROP = 0xffffffffu;
@@ -783,9 +800,24 @@ static int upload_impl(fsv_ctx* c, int64_t n, const int64_t* h_off, const ColT* 
     H &= ~3;
     if (H < 256) H = 0;
   }
+  // L2 rank tier: when the vectors overflow L2 and the degrees are skewed,
+  // the next most connected vertices (degree >= kTierMinDegree, at most
+  // kTierMax) also get a compact slot, gathered from the L2-resident G_hub
+  int HT = H;
+  long long tier_min_n = kTierMinN;
+  if (const char* env = getenv("FSV_TIER_MIN_N")) tier_min_n = atoll(env);   // tests force the tier
+  if (H && n >= tier_min_n && c->hub_limit >= 0) {
+    k_count_ge<<<1, 32, 0, st>>>(deg_sorted.p, n, kTierMinDegree, reinterpret_cast<long long*>(d_bad.p + 1));
+    long long cnt_ge = 0;
+    CUDA_TRY(cudaMemcpyAsync(&cnt_ge, d_bad.p + 1, sizeof cnt_ge, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    const long long t = std::min<long long>(cnt_ge, kTierMax) & ~3LL;
+    if (t > H) HT = (int)t;
+  }
   c->H = H;
-  CUDA_TRY(c->hub_id.alloc(std::max(H, 4)));
-  if (n) k_positions<<<grid_for(c, n, 256), 256, 0, st>>>(ids_sorted.p, n, H, pos.p, c->hub_id.p);
+  c->HT = HT;
+  CUDA_TRY(c->hub_id.alloc(std::max(HT, 4)));
+  if (n) k_positions<<<grid_for(c, n, 256), 256, 0, st>>>(ids_sorted.p, n, HT, pos.p, c->hub_id.p);
   umark(1);
 
   // orientation: encode (one gather per entry), scan, compact
@@ -805,7 +837,7 @@ static int upload_impl(fsv_ctx* c, int64_t n, const int64_t* h_off, const ColT* 
     CUDA_TRY(cudaStreamWaitEvent(st, c->chunk_ev[k], 0));
     if (nr)
       k_orient_encode<ColT><<<grid_for(c, (nr + 31) / 32 * 32, 256, 16), 256, 0, st>>>(
-          d_off.p, d_cols.p, e_begin, r0, nr, n, pos.p, H, etmp.p, cnt.p + (r0 - row_begin),
+          d_off.p, d_cols.p, e_begin, r0, nr, n, pos.p, HT, etmp.p, cnt.p + (r0 - row_begin),
           nzflag.p + (r0 - row_begin), d_bad.p);
     if (udbg) {
       cudaEvent_t e; cudaEventCreate(&e); cudaEventRecord(e, st);
@@ -814,7 +846,7 @@ static int upload_impl(fsv_ctx* c, int64_t n, const int64_t* h_off, const ColT* 
   }
   if (rows) {
     k_piece_encode<ColT><<<c->sm_count * 16, 256, 0, st>>>(
-        c->ws.pieces.p, huge_ctr + 1, d_off.p, d_cols.p, e_begin, n, pos.p, H, etmp.p, c->ws.hkept.p, d_bad.p);
+        c->ws.pieces.p, huge_ctr + 1, d_off.p, d_cols.p, e_begin, n, pos.p, HT, etmp.p, c->ws.hkept.p, d_bad.p);
     k_huge_rows<<<c->sm_count * 2, 256, 0, st>>>(c->ws.hrow.p, huge_ctr, c->ws.hkept.p, cnt.p, nzflag.p);
   }
   umark(3);
@@ -880,7 +912,7 @@ static int upload_impl(fsv_ctx* c, int64_t n, const int64_t* h_off, const ColT* 
   // solve buffers: n + dummy vertex, padded for 16-byte vector access
   const size_t nv = ((size_t)n + 1 + 63) / 64 * 64;
   CUDA_TRY(c->X.alloc(nv)); CUDA_TRY(c->Y.alloc(nv)); CUDA_TRY(c->G.alloc(nv));
-  CUDA_TRY(c->G_hub.alloc(std::max(H, 4))); CUDA_TRY(c->hub_acc.alloc(std::max(H, 4)));
+  CUDA_TRY(c->G_hub.alloc(std::max(HT, 4))); CUDA_TRY(c->hub_acc.alloc(std::max(HT, 4)));
   CUDA_TRY(c->done.alloc(1)); CUDA_TRY(c->ticket.alloc(1));
   CUDA_TRY(c->partials.alloc((size_t)c->sc_grid * 8));
   {
@@ -1011,7 +1043,8 @@ static int launch_iteration(fsv_ctx* c, int k, int max_iter, bool graph = false)
   {
     HookArgs a;
     a.ecol = c->ecol.p; a.nspans = nspans; a.span_row = c->span_row.p;
-    a.F = F; a.G = c->G.p; a.N = N; a.G_hub = c->G_hub.p; a.H = c->H; a.hub_acc = c->hub_acc.p;
+    a.F = F; a.G = c->G.p; a.N = N; a.G_hub = c->G_hub.p; a.H = c->H; a.HT = c->HT;
+    a.hub_acc = c->hub_acc.p;
     a.done = c->done.p; a.mode = c->mode.p; a.iter = k;
     PushArgs& p = a.push;
     p.list = c->dlist.p; p.count = c->dcount.p; p.rcap = c->rcap;
@@ -1029,14 +1062,14 @@ static int launch_iteration(fsv_ctx* c, int k, int max_iter, bool graph = false)
     pmark(c, k, 0);
     void* kargs[] = {&a};
     const size_t dyn = std::max<size_t>((size_t)c->H * sizeof(int), PUSH_SCRATCH_BYTES);
-    CUDA_TRY(cudaLaunchCooperativeKernel((const void*)k_hook, dim3(c->sm_count), dim3(HOOK_THREADS),
-                                         kargs, dyn, st));
+    const void* fn = c->HT > c->H ? (const void*)k_hook<true> : (const void*)k_hook<false>;
+    CUDA_TRY(cudaLaunchCooperativeKernel(fn, dim3(c->sm_count), dim3(HOOK_THREADS), kargs, dyn, st));
     pmark(c, k, 1);
     ++c->launches;
   }
-  if (c->H) {
+  if (c->HT) {
     pmark(c, k, 2);
-    k_hubfix<<<grid_for(c, c->H, 256), 256, 0, st>>>(c->hub_acc.p, c->hub_id.p, c->H, F, c->G.p, N,
+    k_hubfix<<<grid_for(c, c->HT, 256), 256, 0, st>>>(c->hub_acc.p, c->hub_id.p, c->HT, F, c->G.p, N,
                                                        c->done.p, c->mode.p, k,
                                                        graph ? c->iterbuf.p : nullptr);
     pmark(c, k, 3);
@@ -1049,7 +1082,7 @@ static int launch_iteration(fsv_ctx* c, int k, int max_iter, bool graph = false)
   }
   ShortcutArgs s;
   s.F = F; s.G = c->G.p; s.N = N; s.n = c->n; s.hub_id = c->hub_id.p; s.G_hub = c->G_hub.p;
-  s.H = c->H; s.cnt = c->cnt.p + (size_t)(k - 1) * NCOUNT; s.ticket = c->ticket.p; s.done = c->done.p;
+  s.H = c->HT; s.cnt = c->cnt.p + (size_t)(k - 1) * NCOUNT; s.ticket = c->ticket.p; s.done = c->done.p;
   s.partials = c->partials.p;
   s.dl = delta_out(c);
   s.iter = k; s.max_iter = max_iter;
@@ -1136,8 +1169,8 @@ static int solve_impl(fsv_ctx* c, const fsv_config* cfg, int32_t* snapshots, int
   const bool graph_mode = c->use_graph && !snapshots && !c->profile && !c->comm && d.batch == 0;
   if (graph_mode && (rc = ensure_graph(c, cap))) return rc;
   CUDA_TRY(cudaEventRecord(c->events[0], st));
-  k_solve_init<<<grid_for(c, std::max<long long>(c->H, (long long)cap * NCOUNT), 256), 256, 0, st>>>(
-      c->X.p, c->Y.p, c->G.p, c->n, c->hub_acc.p, c->H, c->cnt.p, (long long)cap * NCOUNT, c->done.p,
+  k_solve_init<<<grid_for(c, std::max<long long>(c->HT, (long long)cap * NCOUNT), 256), 256, 0, st>>>(
+      c->X.p, c->Y.p, c->G.p, c->n, c->hub_acc.p, c->HT, c->cnt.p, (long long)cap * NCOUNT, c->done.p,
       c->ticket.p, c->mode.p, c->policy == 2 ? 1 : 0, c->tstamp.p);
   pmark(c, 1, 6);
   // iteration 1 in closed form: f_1[u] = min(u, smallest neighbour) from the
@@ -1160,7 +1193,7 @@ static int solve_impl(fsv_ctx* c, const fsv_config* cfg, int32_t* snapshots, int
   {
     FirstArgs fa;
     fa.f1 = c->f1.p; fa.Y = c->Y.p; fa.G = c->G.p; fa.X = c->X.p; fa.n = c->n;
-    fa.hub_id = c->hub_id.p; fa.G_hub = c->G_hub.p; fa.H = c->H; fa.cnt = c->cnt.p;
+    fa.hub_id = c->hub_id.p; fa.G_hub = c->G_hub.p; fa.H = c->HT; fa.cnt = c->cnt.p;
     fa.partials = c->partials.p; fa.ticket = c->ticket.p; fa.done = c->done.p; fa.max_iter = cap;
     fa.dl = delta_out(c);
     fa.lc = loop_ctl(c, graph_mode ? 2 : 0);
@@ -1187,7 +1220,7 @@ static int solve_impl(fsv_ctx* c, const fsv_config* cfg, int32_t* snapshots, int
       // kernels the graph ran: each body pass is two iterations' worth
       const int it = done > 0 ? done : -done;
       const int passes = std::max(1, it / 2);
-      c->launches += passes * 2 * (2 + (c->H ? 1 : 0));
+      c->launches += passes * 2 * (2 + (c->HT ? 1 : 0));
     }
     if (done > 0 && (rc = ensure_events(c, (size_t)done + 1))) return rc;
     if (done > 0) CUDA_TRY(cudaEventRecord(c->events[done], st));
@@ -1252,7 +1285,7 @@ static int solve_impl(fsv_ctx* c, const fsv_config* cfg, int32_t* snapshots, int
       } else {
         c->push_ms += hk;
       }
-      if (c->H) c->hubfix_ms += span(k, 2, 3);
+      if (c->HT) c->hubfix_ms += span(k, 2, 3);
       if (c->comm && c->n) c->allreduce_ms += span(k, 8, 9);
       c->shortcut_ms += span(k, 6, 7);
     }
@@ -1275,7 +1308,7 @@ static void fill_stats(fsv_ctx* c, fsv_stats* s) {
   s->n = c->n;
   s->m_dir = c->m_dir;
   s->oriented_entries = c->E - c->R;  // edges only (headers excluded)
-  s->hub_slots = c->H;
+  s->hub_slots = c->HT;
   s->host_syncs = c->host_syncs;
   s->kernel_launches = c->launches;
   s->solve_ms = c->solve_ms;

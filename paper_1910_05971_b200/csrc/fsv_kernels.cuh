@@ -163,9 +163,10 @@ struct HookArgs {
   const int* F;           // f_k
   const int* G;           // gf_k
   int* N;                 // f_{k+1}, pre-initialised to gf_k
-  const int* G_hub;       // gf_k of hub slots (compact)
-  int H;                  // hub slots (multiple of 4)
-  int* hub_acc;           // column-side minima aimed at hubs
+  const int* G_hub;       // gf_k of all tier slots, degree-rank order (compact)
+  int H;                  // shared-memory slots (multiple of 4)
+  int HT;                 // all tier slots: [0,H) shared memory, [H,HT) the L2 rank tier
+  int* hub_acc;           // column-side minima aimed at tier slots
   const int* done;        // convergence flag (iteration number, 0 = running)
   const int* mode;        // mode[iter]: 0 dense pull (this layout), 1 sparse push
   int iter;
@@ -195,7 +196,7 @@ struct ShortcutArgs {
   long long n;
   const int* hub_id;
   int* G_hub;
-  int H;
+  int H;                  // tier slots refreshed here (all of them)
   unsigned long long* cnt;  // this iteration's NCOUNT counters
   unsigned* partials;       // per-block partial counters [grid][8]
   unsigned int* ticket;
@@ -360,6 +361,24 @@ __device__ __forceinline__ void push_run(const PushArgs& a, long long* w_start, 
   }
 }
 
+// Rank-tier gather: hub slots below H from shared memory, the rest of the
+// tier from the compact (L2-resident) G_hub, non-tier columns from G.
+__device__ __forceinline__ int gather_gf_tier(uint32_t c, uint32_t s_base, const int* __restrict__ G,
+                                              const int* __restrict__ G_hub, uint32_t H) {
+  int v;
+  const uint32_t x = c & IDMASK;
+  const bool hub = (c & HUB) != 0;
+  const bool sm = hub && x < H;
+  const int* gp = hub ? G_hub + x : G + x;
+  asm("{\n\t.reg .pred p;\n\t"
+      "setp.ne.u32 p, %1, 0;\n\t"
+      "@p  ld.shared.b32 %0, [%2];\n\t"
+      "@!p ld.global.nc.b32 %0, [%3];\n\t}"
+      : "=r"(v)
+      : "r"((uint32_t)sm), "r"(s_base + (x << 2)), "l"(gp));
+  return v;
+}
+
 // ---- phase H: hooking over the oriented layout ------------------------------
 //
 // Warp task = SPAN consecutive entries; lane l of a step owns entries
@@ -376,6 +395,7 @@ __device__ __forceinline__ void push_run(const PushArgs& a, long long* w_start, 
 // differs and no carried minimum is pending, the whole step is a no-op apart
 // from carry bookkeeping — the common case once components have converged.
 
+template <bool TIER>
 __global__ void __launch_bounds__(HOOK_THREADS, 1) k_hook(HookArgs a) {
   extern __shared__ int s_hub[];
   if (*(volatile const int*)a.done) return;
@@ -446,7 +466,9 @@ __global__ void __launch_bounds__(HOOK_THREADS, 1) k_hook(HookArgs a) {
       }
       int val[EPL];
 #pragma unroll
-      for (int j = 0; j < EPL; ++j) val[j] = gather_gf(c[j], s_base, G);
+      for (int j = 0; j < EPL; ++j)
+        val[j] = TIER ? gather_gf_tier(c[j], s_base, G, a.G_hub, (uint32_t)a.H)
+                      : gather_gf(c[j], s_base, G);
       // last header of this lane
       int lu = -1, lgu = INF;
 #pragma unroll

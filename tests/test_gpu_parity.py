@@ -232,3 +232,23 @@ def test_graph_loop_and_host_loop_agree(solver):
     assert a[1] == b[1] and a[2].tolist() == b[2].tolist() and np.array_equal(a[0], b[0])
     assert st_graph[0] == 1
     assert all(ms > 0 for ms in a[4])
+
+
+def test_rank_tier_path(solver, monkeypatch):
+    """The L2 rank tier (degree-ranked compact gf beyond the shared-memory
+    slots; on by default only when the vectors overflow L2) forced on small
+    skewed graphs with a small shared-memory table: identical results."""
+    monkeypatch.setenv("FSV_TIER_MIN_N", "0")
+    for seed, scale in ((41, 12), (42, 13), (43, 14)):
+        n, e = gen.rmat(scale, 16, seed=seed)
+        g = fb.build_csr(n, e)
+        o = oracle.fastsv_csr(n, g.row_offsets, g.col_indices, snapshots=True)
+        solver.set_hub_slots(256)
+        solver.upload(g)
+        st = solver.solve()
+        assert st.hub_slots > 256           # the tier is in use
+        for policy in (0, 1):
+            labels, iters, gfc, fc, ms, snaps = solver.run(snapshots=True, snap_cap=64, policy=policy)
+            assert iters == o.iterations and gfc.tolist() == o.gf_changed.tolist()
+            assert np.array_equal(snaps, o.snapshots)
+    solver.set_hub_slots(0)
