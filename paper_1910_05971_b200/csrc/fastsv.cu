@@ -14,6 +14,7 @@
 #include "fsv_kernels.cuh"
 
 #include <cub/cub.cuh>
+#include <cuda/std/functional>
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <nccl.h>
@@ -132,7 +133,8 @@ struct DBuf {
   ~DBuf() { free(); }
 };
 
-static constexpr int kHubMax = 57344;     // 224 KB of shared memory (the opt-in maximum is 227 KB)
+// hub table + hot accumulators within the 227 KB opt-in shared memory
+static constexpr int kHubMax = (SMEM_OPTIN_INTS - HOT_ACC) / 1024 * 1024;
 static constexpr int kHubMinDegree = 32;  // below this a hub slot buys nothing
 static constexpr long long kTierMinN = 1LL << 23;   // rank tier only when the vectors overflow L2
 static constexpr int kTierMinDegree = 8;
@@ -151,6 +153,7 @@ struct fsv_ctx {
   int64_t n = 0, m_dir = 0, E = 0, Epad = 0;
   int R = 0, H = 0, HT = 0;   // shared-memory hub slots, all tier slots
   DBuf<uint32_t> ecol;
+  uint32_t* ecolp = nullptr;   // layout start inside ecol
   DBuf<int> span_row, hub_id, f1;
   // full symmetric CSR of this rank's rows, for sparse (push) iterations
   DBuf<int64_t> csr_off;
@@ -165,18 +168,24 @@ struct fsv_ctx {
   struct {
     DBuf<unsigned long long> bad;
     DBuf<int> deg, ids, deg_sorted, ids_sorted, slot_of, nzflag, nzidx, nzrows;
-    DBuf<long long> cnt, out_off, nzoff;
+    DBuf<long long> cnt, out_off, nzoff, carry_e;
+    DBuf<int> carry_r;
     DBuf<unsigned char> tmp;
     DBuf<int64_t> cols64;
     DBuf<uint32_t> etmp;
     DBuf<int4> pieces;
     DBuf<long long> hrow;
-    DBuf<unsigned long long> hkept, hcursor;
+    DBuf<unsigned long long> hkept;
+    DBuf<int> piece_kept;
   } ws;
   long long rcap = 0;
   int dgrid = 1;
   // solve state
-  DBuf<int> X, Y, G, G_hub, hub_acc, done;
+  DBuf<int> vec, G_hub, hub_acc, done;
+  int* hacc = nullptr;   // vec: slab holding X, Y, G
+  int* X = nullptr;
+  int* Y = nullptr;
+  int* G = nullptr;
   DBuf<unsigned long long> cnt;
   DBuf<unsigned int> ticket;
   DBuf<unsigned> partials;
@@ -252,10 +261,10 @@ extern "C" int fsv_create(int device, fsv_ctx** out) {
     c->sc_grid = std::max(1, per_sm) * c->sm_count;
   }
   cudaError_t e = cudaFuncSetAttribute(k_hook<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       std::max(kHubMax * (int)sizeof(int), PUSH_SCRATCH_BYTES));
+                                       std::max((kHubMax + HOT_ACC) * (int)sizeof(int), PUSH_SCRATCH_BYTES));
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(k_hook<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             std::max(kHubMax * (int)sizeof(int), PUSH_SCRATCH_BYTES));
+                             std::max((kHubMax + HOT_ACC) * (int)sizeof(int), PUSH_SCRATCH_BYTES));
   if (e != cudaSuccess) {
     delete c;
     return fail(FSV_ERR_RUNTIME, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
@@ -326,8 +335,14 @@ __global__ void k_count_ge(const int* __restrict__ sorted_desc, long long n, int
 }
 
 constexpr uint32_t DROP = 0xffffffffu;
-constexpr long long HUGE_ROW = 4096;  // rows longer than this are cut into pieces
-constexpr long long PIECE = 4096;     // entries per piece
+#ifndef FSV_HUGE_ROW
+#define FSV_HUGE_ROW 512
+#endif
+#ifndef FSV_PIECE
+#define FSV_PIECE 1024
+#endif
+constexpr long long HUGE_ROW = FSV_HUGE_ROW;  // rows longer than this are cut into pieces
+constexpr long long PIECE = FSV_PIECE;        // entries per piece
 
 __device__ __forceinline__ uint32_t encode_col(int v, int pv, int H) {
   return pv < H ? (HUB | (uint32_t)pv) : (uint32_t)v;
@@ -393,16 +408,26 @@ __global__ void k_orient_encode(const int64_t* __restrict__ off, const ColT* __r
       const long long shi = __shfl_sync(0xffffffffu, hi, src);
       const int spu = __shfl_sync(0xffffffffu, pu, src);
       long long sk = 0;
-      for (long long e = slo + lane; e < shi; e += 32) {
-        const long long v = (long long)cols[e];
-        uint32_t code = DROP;
-        if (v < 0 || v >= n) {
-          atomicMin(bad, (unsigned long long)e);
-        } else {
-          const int pv = pos[v];
-          if (pv < spu) { code = encode_col((int)v, pv, H); ++sk; }
+      // 8 entries per lane in flight (column loads, then pos gathers)
+      for (long long e0 = slo; e0 < shi; e0 += 8 * 32) {
+        long long v[8];
+        int pv[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const long long e = e0 + lane + 32 * j;
+          v[j] = e < shi ? (long long)cols[e] : -2;
         }
-        tmp[e] = code;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) pv[j] = (v[j] >= 0 && v[j] < n) ? pos[v[j]] : INF;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const long long e = e0 + lane + 32 * j;
+          if (e >= shi) continue;
+          uint32_t code = DROP;
+          if (v[j] < 0 || v[j] >= n) atomicMin(bad, (unsigned long long)e);
+          else if (pv[j] < spu) { code = encode_col((int)v[j], pv[j], H); ++sk; }
+          tmp[e] = code;
+        }
       }
       for (int o = 16; o; o >>= 1) sk += __shfl_xor_sync(0xffffffffu, sk, o);
       if (lane == src) k = sk;
@@ -434,16 +459,18 @@ __global__ void k_find_huge(const int64_t* __restrict__ off, long long row_begin
 
 template <typename ColT>
 __global__ void k_piece_encode(const int4* __restrict__ pieces, const unsigned long long* npieces_p,
-                               const int64_t* __restrict__ off,
+                               long long u0, long long u1, const int64_t* __restrict__ off,
                                const ColT* __restrict__ cols, long long col_base, long long n,
                                const int* __restrict__ pos, int H, uint32_t* __restrict__ tmp,
-                               unsigned long long* __restrict__ row_kept, unsigned long long* bad) {
+                               unsigned long long* __restrict__ row_kept, int* __restrict__ piece_kept,
+                               unsigned long long* bad) {
   const int lane = threadIdx.x & 31;
   const long long nw = (long long)gridDim.x * (blockDim.x >> 5);
   const long long npieces = (long long)*npieces_p;
   for (long long q = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); q < npieces; q += nw) {
     const int4 pc = pieces[q];                      // (row u, piece start, piece end, huge-row index)
     const int u = pc.x;
+    if (u < u0 || u >= u1) continue;                // another chunk's row
     const long long base = off[u] - col_base;
     const long long lo = base + (long long)pc.y * PIECE, hi = min(base + (long long)pc.z * PIECE,
                                                                   off[u + 1] - col_base);
@@ -470,54 +497,65 @@ __global__ void k_piece_encode(const int4* __restrict__ pieces, const unsigned l
       }
     }
     for (int o = 16; o; o >>= 1) k += __shfl_xor_sync(0xffffffffu, k, o);
-    if (lane == 0 && k) atomicAdd(row_kept + pc.w, k);
+    if (lane == 0) {
+      piece_kept[q] = (int)k;
+      if (k) atomicAdd(row_kept + pc.w, k);
+    }
   }
 }
 
 // Huge rows: per-row counts from the pieces (+ header), and the output
 // cursor for k_piece_compact; `hrow[i]` = (row - row_begin) of huge row i.
 __global__ void k_huge_rows(const long long* __restrict__ hrow, const unsigned long long* nh_p,
-                            const unsigned long long* row_kept, long long* __restrict__ cnt,
-                            int* __restrict__ nzflag) {
+                            long long r0, long long r1, const unsigned long long* row_kept,
+                            long long* __restrict__ cnt, int* __restrict__ nzflag) {
   const long long nh = (long long)*nh_p;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < nh;
        i += (long long)gridDim.x * blockDim.x) {
+    if (hrow[i] < r0 || hrow[i] >= r1) continue;
     const long long k = (long long)row_kept[i];
     cnt[hrow[i]] = k ? k + 1 : 0;
     nzflag[hrow[i]] = k > 0;
   }
 }
 
+// Pieces of a huge row are consecutive in the piece list (piece j of the
+// row at index q has its predecessors at q-j .. q-1), so each piece's output
+// offset is the row offset plus its predecessors' kept counts: the row keeps
+// its column order, deterministically.
 __global__ void k_piece_compact(const int4* __restrict__ pieces, const unsigned long long* npieces_p,
-                                const int64_t* __restrict__ off,
+                                long long u0, long long u1, const int64_t* __restrict__ off,
                                 long long col_base, const uint32_t* __restrict__ tmp,
                                 const long long* __restrict__ hrow, const long long* __restrict__ out_off,
-                                unsigned long long* __restrict__ cursor, uint32_t* __restrict__ ecol) {
+                                const int* __restrict__ piece_kept, uint32_t* __restrict__ ecol) {
   const int lane = threadIdx.x & 31;
   const long long nw = (long long)gridDim.x * (blockDim.x >> 5);
   const long long npieces = (long long)*npieces_p;
   for (long long q = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); q < npieces; q += nw) {
     const int4 pc = pieces[q];
     const int u = pc.x;
+    if (u < u0 || u >= u1) continue;
     const long long base = off[u] - col_base;
     const long long lo = base + (long long)pc.y * PIECE, hi = min(base + (long long)pc.z * PIECE,
                                                                   off[u + 1] - col_base);
-    // count kept, reserve a contiguous slot range of the row, write in order
-    unsigned long long k = 0;
-    for (long long e = lo + lane; e < hi; e += 32) k += tmp[e] != DROP;
-    for (int o = 16; o; o >>= 1) k += __shfl_xor_sync(0xffffffffu, k, o);
-    unsigned long long o0 = 0;
-    if (lane == 0 && k) o0 = atomicAdd(cursor + pc.w, k);
-    o0 = __shfl_sync(0xffffffffu, o0, 0);
-    const long long dst = out_off[hrow[pc.w]] + 1 + (long long)o0;
-    long long o = 0;
-    for (long long e0 = lo; e0 < hi; e0 += 32) {
-      const long long e = e0 + lane;
-      const uint32_t code = e < hi ? tmp[e] : DROP;
-      const bool keep = code != DROP;
-      const unsigned b = __ballot_sync(0xffffffffu, keep);
-      if (keep) ecol[dst + o + __popc(b & ((1u << lane) - 1u))] = code;
-      o += __popc(b);
+    long long before = 0;
+    for (long long i = q - pc.y + lane; i < q; i += 32) before += piece_kept[i];
+    for (int o = 16; o; o >>= 1) before += __shfl_xor_sync(0xffffffffu, before, o);
+    long long o = out_off[hrow[pc.w]] + 1 + before;
+    for (long long e0 = lo; e0 < hi; e0 += 8 * 32) {
+      uint32_t code[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const long long e = e0 + lane + 32 * j;
+        code[j] = e < hi ? tmp[e] : DROP;
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const bool keep = code[j] != DROP;
+        const unsigned b = __ballot_sync(0xffffffffu, keep);
+        if (keep) ecol[o + __popc(b & ((1u << lane) - 1u))] = code[j];
+        o += __popc(b);
+      }
     }
   }
 }
@@ -569,16 +607,41 @@ __global__ void k_orient_compact(const int64_t* __restrict__ off, long long col_
       const long long slo = __shfl_sync(0xffffffffu, lo, src);
       const long long shi = __shfl_sync(0xffffffffu, hi, src);
       long long o = __shfl_sync(0xffffffffu, o0, src) + 1;
-      for (long long e0 = slo; e0 < shi; e0 += 32) {
-        const long long e = e0 + lane;
-        const uint32_t code = e < shi ? tmp[e] : DROP;
-        const bool keep = code != DROP;
-        const unsigned b = __ballot_sync(0xffffffffu, keep);
-        if (keep) ecol[o + __popc(b & ((1u << lane) - 1u))] = code;
-        o += __popc(b);
+      for (long long e0 = slo; e0 < shi; e0 += 8 * 32) {
+        uint32_t code[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const long long e = e0 + lane + 32 * j;
+          code[j] = e < shi ? tmp[e] : DROP;
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const bool keep = code[j] != DROP;
+          const unsigned b = __ballot_sync(0xffffffffu, keep);
+          if (keep) ecol[o + __popc(b & ((1u << lane) - 1u))] = code[j];
+          o += __popc(b);
+        }
       }
     }
   }
+}
+
+// Chains the per-chunk scans: after chunk k's exclusive scans of rows
+// [r0, r1) (seeded with carry[k]), the totals up to r1 become carry[k+1]
+// and the out_off/nzidx entries at r1 (read by the compaction of chunk k).
+__global__ void k_chunk_carry(const long long* __restrict__ cnt, const int* __restrict__ nzflag,
+                              long long* __restrict__ out_off, int* __restrict__ nzidx, long long r0,
+                              long long r1, long long* carry_e, int* carry_r, int k) {
+  long long e = carry_e[k];
+  int z = carry_r[k];
+  if (r1 > r0) {
+    e = out_off[r1 - 1] + cnt[r1 - 1];
+    z = nzidx[r1 - 1] + nzflag[r1 - 1];
+  }
+  carry_e[k + 1] = e;
+  carry_r[k + 1] = z;
+  out_off[r1] = e;
+  nzidx[r1] = z;
 }
 
 __global__ void k_pad(uint32_t* ecol, long long E, long long Epad, int n, int* nzrows, int R,
@@ -719,11 +782,20 @@ static int upload_impl(fsv_ctx* c, int64_t n, const int64_t* h_off, const ColT* 
   // sort and the orientation of earlier chunks overlap the transfer
   std::vector<int64_t> chunk_rows;  // row boundaries, chunk k = [chunk_rows[k], chunk_rows[k+1])
   {
-    int K = mloc >= ((int64_t)1 << 24) ? 8 : 1;
-    if (const char* env = getenv("FSV_UPLOAD_CHUNKS")) K = std::max(1, std::min(64, atoi(env)));
+    // eighths of the entries, the last eighth cut geometrically (1/16, 1/32,
+    // 1/64, 1/64) so the work trailing the final copy is small
+    std::vector<int64_t> cut;  // chunk ends in 1/64ths of mloc
+    if (mloc >= ((int64_t)1 << 24)) cut = {8, 16, 24, 32, 40, 48, 56, 60, 62, 63, 64};
+    else cut = {64};
+    if (const char* env = getenv("FSV_UPLOAD_CHUNKS")) {   // dev: K equal chunks
+      const int k_eq = std::max(1, std::min(64, atoi(env)));
+      cut.clear();
+      for (int k = 1; k <= k_eq; ++k) cut.push_back(64 * k / k_eq);
+    }
+    const int K = (int)cut.size();
     chunk_rows.push_back(row_begin);
-    for (int k = 1; k < K; ++k) {
-      const int64_t target = e_begin + mloc * k / K;
+    for (int k = 0; k + 1 < K; ++k) {
+      const int64_t target = e_begin + (int64_t)((__int128)mloc * cut[k] / 64);
       int64_t r = std::lower_bound(h_off + row_begin, h_off + row_end, target) - h_off;
       r = std::max<int64_t>(r, chunk_rows.back());
       chunk_rows.push_back(std::min<int64_t>(r, row_end));
@@ -757,9 +829,8 @@ static int upload_impl(fsv_ctx* c, int64_t n, const int64_t* h_off, const ColT* 
   CUDA_TRY(c->ws.pieces.alloc((size_t)max_pieces));
   CUDA_TRY(c->ws.hrow.alloc((size_t)max_huge));
   CUDA_TRY(c->ws.hkept.alloc((size_t)max_huge + 2));   // [0..max_huge) kept, then 2 counters
-  CUDA_TRY(c->ws.hcursor.alloc((size_t)max_huge));
+  CUDA_TRY(c->ws.piece_kept.alloc((size_t)max_pieces));
   CUDA_TRY(cudaMemsetAsync(c->ws.hkept.p, 0, sizeof(unsigned long long) * (max_huge + 2), st));
-  CUDA_TRY(cudaMemsetAsync(c->ws.hcursor.p, 0, sizeof(unsigned long long) * max_huge, st));
   unsigned long long* huge_ctr = c->ws.hkept.p + max_huge;      // [0] huge rows, [1] pieces
   if (rows)
     k_find_huge<<<grid_for(c, rows, 256), 256, 0, st>>>(d_off.p, row_begin, rows, c->ws.hrow.p,
@@ -778,12 +849,25 @@ static int upload_impl(fsv_ctx* c, int64_t n, const int64_t* h_off, const ColT* 
   CUDA_TRY(deg_sorted.alloc(n)); CUDA_TRY(ids_sorted.alloc(n)); CUDA_TRY(pos.alloc(n));
   if (n) k_degree<<<grid_for(c, n, 256), 256, 0, st>>>(d_off.p, n, deg.p, ids.p, d_bad.p + 1);
   int H = 0;
+  {
+    // one temp buffer for the sort and the per-chunk scans (no reallocation
+    // while the pipeline runs: cudaFree would synchronise the device)
+    size_t sort_bytes = 0, b1 = 0, b2 = 0;
+    long long max_nr = 1;
+    for (size_t k = 0; k + 1 < chunk_rows.size(); ++k)
+      max_nr = std::max<long long>(max_nr, chunk_rows[k + 1] - chunk_rows[k]);
+    if (n)
+      cub::DeviceRadixSort::SortPairsDescending(nullptr, sort_bytes, deg.p, deg_sorted.p, ids.p,
+                                                ids_sorted.p, (int)n, 0, 32, st);
+    cub::DeviceScan::ExclusiveScan(nullptr, b1, (long long*)nullptr, (long long*)nullptr, cuda::std::plus<>{},
+                                   cub::FutureValue<long long>(nullptr), (int)max_nr, st);
+    cub::DeviceScan::ExclusiveScan(nullptr, b2, (int*)nullptr, (int*)nullptr, cuda::std::plus<>{},
+                                   cub::FutureValue<int>(nullptr), (int)max_nr, st);
+    CUDA_TRY(c->ws.tmp.alloc(std::max(sort_bytes, std::max(b1, b2))));
+  }
   if (n) {
-    size_t tmp_bytes = 0;
-    cub::DeviceRadixSort::SortPairsDescending(nullptr, tmp_bytes, deg.p, deg_sorted.p, ids.p,
-                                              ids_sorted.p, (int)n, 0, 32, st);
+    size_t tmp_bytes = c->ws.tmp.n;
     auto& tmp = c->ws.tmp;
-    CUDA_TRY(tmp.alloc(tmp_bytes));
     CUDA_TRY(cub::DeviceRadixSort::SortPairsDescending(tmp.p, tmp_bytes, deg.p, deg_sorted.p, ids.p,
                                                        ids_sorted.p, (int)n, 0, 32, st));
     // hubs: the first positions with degree >= kHubMinDegree, at most kHubMax
@@ -820,50 +904,74 @@ static int upload_impl(fsv_ctx* c, int64_t n, const int64_t* h_off, const ColT* 
   if (n) k_positions<<<grid_for(c, n, 256), 256, 0, st>>>(ids_sorted.p, n, HT, pos.p, c->hub_id.p);
   umark(1);
 
-  // orientation: encode (one gather per entry), scan, compact
+  // orientation, chunk by chunk as the columns arrive: encode (one gather
+  // per entry), exclusive scans seeded with the running totals of the
+  // earlier chunks (device-side carry), compact into the final layout. Only
+  // the last chunk's work trails the transfer. ecol is sized by the bound
+  // E <= kept entries + headers <= mloc + rows until E is known.
   auto& cnt = c->ws.cnt;
   auto& out_off = c->ws.out_off;
   auto& nzflag = c->ws.nzflag;
   auto& nzidx = c->ws.nzidx;
   auto& etmp = c->ws.etmp;
+  auto& nzrows = c->ws.nzrows;
+  auto& nzoff = c->ws.nzoff;
+  const int K = (int)chunk_rows.size() - 1;
   CUDA_TRY(cnt.alloc(rows + 1)); CUDA_TRY(out_off.alloc(rows + 1));
   CUDA_TRY(nzflag.alloc(rows + 1)); CUDA_TRY(nzidx.alloc(rows + 1));
   CUDA_TRY(etmp.alloc((size_t)std::max<int64_t>(mloc, 1)));
-  CUDA_TRY(cudaMemsetAsync(cnt.p + rows, 0, sizeof(long long), st));
-  CUDA_TRY(cudaMemsetAsync(nzflag.p + rows, 0, sizeof(int), st));
+  CUDA_TRY(nzrows.alloc((size_t)rows + 1));
+  CUDA_TRY(nzoff.alloc((size_t)rows + 1));
+  {
+    long long epad = 0;   // dev: FSV_EPAD shifts the layout (placement sensitivity checks)
+    if (const char* e = getenv("FSV_EPAD")) epad = atoll(e);
+    CUDA_TRY(c->ecol.alloc((size_t)(mloc + rows + SPAN + epad)));
+    c->ecolp = c->ecol.p + epad;
+  }
+  CUDA_TRY(c->ws.carry_e.alloc((size_t)K + 1));
+  CUDA_TRY(c->ws.carry_r.alloc((size_t)K + 1));
+  CUDA_TRY(cudaMemsetAsync(c->ws.carry_e.p, 0, sizeof(long long), st));
+  CUDA_TRY(cudaMemsetAsync(c->ws.carry_r.p, 0, sizeof(int), st));
   umark(2);
-  for (size_t k = 0; k + 1 < chunk_rows.size(); ++k) {
-    const long long r0 = chunk_rows[k], nr = chunk_rows[k + 1] - chunk_rows[k];
+  for (int k = 0; k < K; ++k) {
+    const long long u0 = chunk_rows[k], u1 = chunk_rows[k + 1], nr = u1 - u0;
+    const long long r0 = u0 - row_begin, r1 = u1 - row_begin;
     CUDA_TRY(cudaStreamWaitEvent(st, c->chunk_ev[k], 0));
-    if (nr)
+    if (nr) {
       k_orient_encode<ColT><<<grid_for(c, (nr + 31) / 32 * 32, 256, 16), 256, 0, st>>>(
-          d_off.p, d_cols.p, e_begin, r0, nr, n, pos.p, HT, etmp.p, cnt.p + (r0 - row_begin),
-          nzflag.p + (r0 - row_begin), d_bad.p);
+          d_off.p, d_cols.p, e_begin, u0, nr, n, pos.p, HT, etmp.p, cnt.p + r0, nzflag.p + r0, d_bad.p);
+      k_piece_encode<ColT><<<c->sm_count * 16, 256, 0, st>>>(
+          c->ws.pieces.p, huge_ctr + 1, u0, u1, d_off.p, d_cols.p, e_begin, n, pos.p, HT, etmp.p,
+          c->ws.hkept.p, c->ws.piece_kept.p, d_bad.p);
+      k_huge_rows<<<c->sm_count * 2, 256, 0, st>>>(c->ws.hrow.p, huge_ctr, r0, r1, c->ws.hkept.p, cnt.p,
+                                                  nzflag.p);
+      size_t b = c->ws.tmp.n;
+      CUDA_TRY(cub::DeviceScan::ExclusiveScan(c->ws.tmp.p, b, cnt.p + r0, out_off.p + r0, cuda::std::plus<>{},
+                                              cub::FutureValue<long long>(c->ws.carry_e.p + k), (int)nr, st));
+      b = c->ws.tmp.n;
+      CUDA_TRY(cub::DeviceScan::ExclusiveScan(c->ws.tmp.p, b, nzflag.p + r0, nzidx.p + r0, cuda::std::plus<>{},
+                                              cub::FutureValue<int>(c->ws.carry_r.p + k), (int)nr, st));
+    }
+    k_chunk_carry<<<1, 1, 0, st>>>(cnt.p, nzflag.p, out_off.p, nzidx.p, r0, r1, c->ws.carry_e.p,
+                                   c->ws.carry_r.p, k);
+    if (nr) {
+      k_orient_compact<<<grid_for(c, (nr + 31) / 32 * 32, 256, 16), 256, 0, st>>>(
+          d_off.p, e_begin, u0, nr, etmp.p, out_off.p + r0, nzidx.p + r0, c->ecolp, nzrows.p, nzoff.p);
+      k_piece_compact<<<c->sm_count * 16, 256, 0, st>>>(
+          c->ws.pieces.p, huge_ctr + 1, u0, u1, d_off.p, e_begin, etmp.p, c->ws.hrow.p, out_off.p,
+          c->ws.piece_kept.p, c->ecolp);
+    }
     if (udbg) {
       cudaEvent_t e; cudaEventCreate(&e); cudaEventRecord(e, st);
       dbg_enc_ev.push_back(e);
     }
   }
-  if (rows) {
-    k_piece_encode<ColT><<<c->sm_count * 16, 256, 0, st>>>(
-        c->ws.pieces.p, huge_ctr + 1, d_off.p, d_cols.p, e_begin, n, pos.p, HT, etmp.p, c->ws.hkept.p, d_bad.p);
-    k_huge_rows<<<c->sm_count * 2, 256, 0, st>>>(c->ws.hrow.p, huge_ctr, c->ws.hkept.p, cnt.p, nzflag.p);
-  }
   umark(3);
-  {
-    size_t b1 = 0, b2 = 0;
-    cub::DeviceScan::ExclusiveSum(nullptr, b1, cnt.p, out_off.p, (int)(rows + 1), st);
-    cub::DeviceScan::ExclusiveSum(nullptr, b2, nzflag.p, nzidx.p, (int)(rows + 1), st);
-    auto& tmp = c->ws.tmp;
-    CUDA_TRY(tmp.alloc(std::max(b1, b2)));
-    CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp.p, b1, cnt.p, out_off.p, (int)(rows + 1), st));
-    CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp.p, b2, nzflag.p, nzidx.p, (int)(rows + 1), st));
-  }
   long long E = 0;
   int R = 0;
   unsigned long long h_bad = 0;
-  CUDA_TRY(cudaMemcpyAsync(&E, out_off.p + rows, sizeof E, cudaMemcpyDeviceToHost, st));
-  CUDA_TRY(cudaMemcpyAsync(&R, nzidx.p + rows, sizeof R, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaMemcpyAsync(&E, c->ws.carry_e.p + K, sizeof E, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaMemcpyAsync(&R, c->ws.carry_r.p + K, sizeof R, cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaMemcpyAsync(&h_bad, d_bad.p, sizeof h_bad, cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaStreamSynchronize(st));
   if (h_bad != ~0ull) {
@@ -875,20 +983,8 @@ static int upload_impl(fsv_ctx* c, int64_t n, const int64_t* h_off, const ColT* 
                 (long long)h_cols[h_bad], (long long)n);
   }
   const long long Epad = (E + SPAN - 1) / SPAN * SPAN;
-  CUDA_TRY(c->ecol.alloc((size_t)std::max<long long>(Epad, 4)));
-  auto& nzrows = c->ws.nzrows;
-  CUDA_TRY(nzrows.alloc((size_t)R + 1));
-  auto& nzoff = c->ws.nzoff;
-  CUDA_TRY(nzoff.alloc((size_t)R + 1));
   umark(4);
-  if (rows)
-    k_orient_compact<<<grid_for(c, (rows + 31) / 32 * 32, 256, 16), 256, 0, st>>>(
-        d_off.p, e_begin, row_begin, rows, etmp.p, out_off.p, nzidx.p, c->ecol.p, nzrows.p, nzoff.p);
-  if (rows)
-    k_piece_compact<<<c->sm_count * 16, 256, 0, st>>>(
-        c->ws.pieces.p, huge_ctr + 1, d_off.p, e_begin, etmp.p, c->ws.hrow.p, out_off.p, c->ws.hcursor.p,
-        c->ecol.p);
-  k_pad<<<grid_for(c, std::max<long long>(Epad - E, 1), 256), 256, 0, st>>>(c->ecol.p, E, Epad, (int)n,
+  k_pad<<<grid_for(c, std::max<long long>(Epad - E, 1), 256), 256, 0, st>>>(c->ecolp, E, Epad, (int)n,
                                                                              nzrows.p, R, nzoff.p);
   const long long nspans = Epad / SPAN;
   CUDA_TRY(c->span_row.alloc((size_t)std::max<long long>(nspans, 1)));
@@ -911,8 +1007,16 @@ static int upload_impl(fsv_ctx* c, int64_t n, const int64_t* h_off, const ColT* 
 
   // solve buffers: n + dummy vertex, padded for 16-byte vector access
   const size_t nv = ((size_t)n + 1 + 63) / 64 * 64;
-  CUDA_TRY(c->X.alloc(nv)); CUDA_TRY(c->Y.alloc(nv)); CUDA_TRY(c->G.alloc(nv));
-  CUDA_TRY(c->G_hub.alloc(std::max(HT, 4))); CUDA_TRY(c->hub_acc.alloc(std::max(HT, 4)));
+  CUDA_TRY(c->vec.alloc(3 * nv));
+  c->X = c->vec.p;
+  c->Y = c->X + nv;
+  c->G = c->Y + nv;
+  CUDA_TRY(c->G_hub.alloc(std::max(HT, 4))); {
+    long long hpad = 0;   // dev: FSV_HPAD shifts the hub accumulator (placement checks)
+    if (const char* e = getenv("FSV_HPAD")) hpad = atoll(e);
+    CUDA_TRY(c->hub_acc.alloc(std::max(HT, 4) + hpad));
+    c->hacc = c->hub_acc.p + hpad;
+  }
   CUDA_TRY(c->done.alloc(1)); CUDA_TRY(c->ticket.alloc(1));
   CUDA_TRY(c->partials.alloc((size_t)c->sc_grid * 8));
   {
@@ -937,7 +1041,7 @@ static int upload_impl(fsv_ctx* c, int64_t n, const int64_t* h_off, const ColT* 
   CUDA_TRY(cudaStreamSynchronize(st));
   CUDA_TRY(cudaGetLastError());
   if (udbg) {
-    const char* names[] = {"degrees+sort+positions", "(wait cols) ", "encode", "scans+readback", "compact+pad+spans",
+    const char* names[] = {"degrees+sort+positions", "(setup)", "chunks (encode..compact)", "readback", "pad+spans",
                            "tail (narrow, allocs)"};
     for (int i = 0; i < 6; ++i) {
       float ms = 0.f;
@@ -953,6 +1057,13 @@ static int upload_impl(fsv_ctx* c, int64_t n, const int64_t* h_off, const ColT* 
     for (auto& e : uev) cudaEventDestroy(e);
   }
 
+  if (udbg) {   // layout digest (FNV-1a over ecol, span_row)
+    std::vector<uint32_t> h((size_t)Epad);
+    cudaMemcpy(h.data(), c->ecolp, sizeof(uint32_t) * Epad, cudaMemcpyDeviceToHost);
+    uint64_t d = 1469598103934665603ull;
+    for (uint32_t x : h) { d ^= x; d *= 1099511628211ull; }
+    fprintf(stderr, "[upload] layout digest %016llx E=%lld R=%d\n", (unsigned long long)d, E, R);
+  }
   c->n = n;
   c->m_dir = h_off[n];
   c->E = E;
@@ -983,8 +1094,8 @@ extern "C" int fsv_upload_csr64(fsv_ctx* c, int64_t n, const int64_t* off, const
 
 // Buffers of iteration k >= 2: F = f_{k-1}, N = f_k (initialised to gf_{k-1}).
 // k_first leaves f_1 in Y and gf_1 in X, so even k reads F = Y, N = X.
-static inline int* bufF(fsv_ctx* c, int k) { return (k & 1) ? c->X.p : c->Y.p; }
-static inline int* bufN(fsv_ctx* c, int k) { return (k & 1) ? c->Y.p : c->X.p; }
+static inline int* bufF(fsv_ctx* c, int k) { return (k & 1) ? c->X : c->Y; }
+static inline int* bufN(fsv_ctx* c, int k) { return (k & 1) ? c->Y : c->X; }
 
 static constexpr int kPev = 10;  // profile events per iteration
 
@@ -1042,16 +1153,16 @@ static int launch_iteration(fsv_ctx* c, int k, int max_iter, bool graph = false)
   const long long nspans = c->Epad / SPAN;
   {
     HookArgs a;
-    a.ecol = c->ecol.p; a.nspans = nspans; a.span_row = c->span_row.p;
-    a.F = F; a.G = c->G.p; a.N = N; a.G_hub = c->G_hub.p; a.H = c->H; a.HT = c->HT;
-    a.hub_acc = c->hub_acc.p;
+    a.ecol = c->ecolp; a.nspans = nspans; a.span_row = c->span_row.p;
+    a.F = F; a.G = c->G; a.N = N; a.G_hub = c->G_hub.p; a.H = c->H; a.HT = c->HT;
+    a.hub_acc = c->hacc;
     a.done = c->done.p; a.mode = c->mode.p; a.iter = k;
     PushArgs& p = a.push;
     p.list = c->dlist.p; p.count = c->dcount.p; p.rcap = c->rcap;
     p.nregions = c->dgrid * (SC_THREADS / 32);
     p.off = c->csr_off.p; p.cols = c->csr_cols.p; p.col_base = c->col_base;
     p.row_begin = (int)c->row_begin; p.row_end = (int)c->row_end;
-    p.F = F; p.G = c->G.p; p.N = N; p.mode = c->mode.p; p.iter = k;
+    p.F = F; p.G = c->G; p.N = N; p.mode = c->mode.p; p.iter = k;
     unsigned long long* slot = c->cnt.p + (size_t)(k - 1) * NCOUNT;
     p.flops = slot + C_FLOPS; p.nchunks = slot + C_CHUNKS; p.nbatches = slot + C_BATCHES;
     p.barrier = reinterpret_cast<unsigned*>(slot + C_BARRIER); p.chunks = c->chunks.p;
@@ -1061,7 +1172,8 @@ static int launch_iteration(fsv_ctx* c, int k, int max_iter, bool graph = false)
     // for the grid barrier of the sparse (push) path
     pmark(c, k, 0);
     void* kargs[] = {&a};
-    const size_t dyn = std::max<size_t>((size_t)c->H * sizeof(int), PUSH_SCRATCH_BYTES);
+    const size_t dyn = std::max<size_t>((size_t)(c->H + std::min(c->H, HOT_ACC)) * sizeof(int),
+                                        PUSH_SCRATCH_BYTES);
     const void* fn = c->HT > c->H ? (const void*)k_hook<true> : (const void*)k_hook<false>;
     CUDA_TRY(cudaLaunchCooperativeKernel(fn, dim3(c->sm_count), dim3(HOOK_THREADS), kargs, dyn, st));
     pmark(c, k, 1);
@@ -1069,7 +1181,7 @@ static int launch_iteration(fsv_ctx* c, int k, int max_iter, bool graph = false)
   }
   if (c->HT) {
     pmark(c, k, 2);
-    k_hubfix<<<grid_for(c, c->HT, 256), 256, 0, st>>>(c->hub_acc.p, c->hub_id.p, c->HT, F, c->G.p, N,
+    k_hubfix<<<grid_for(c, c->HT, 256), 256, 0, st>>>(c->hacc, c->hub_id.p, c->HT, F, c->G, N,
                                                        c->done.p, c->mode.p, k,
                                                        graph ? c->iterbuf.p : nullptr);
     pmark(c, k, 3);
@@ -1081,7 +1193,7 @@ static int launch_iteration(fsv_ctx* c, int k, int max_iter, bool graph = false)
     pmark(c, k, 9);
   }
   ShortcutArgs s;
-  s.F = F; s.G = c->G.p; s.N = N; s.n = c->n; s.hub_id = c->hub_id.p; s.G_hub = c->G_hub.p;
+  s.F = F; s.G = c->G; s.N = N; s.n = c->n; s.hub_id = c->hub_id.p; s.G_hub = c->G_hub.p;
   s.H = c->HT; s.cnt = c->cnt.p + (size_t)(k - 1) * NCOUNT; s.ticket = c->ticket.p; s.done = c->done.p;
   s.partials = c->partials.p;
   s.dl = delta_out(c);
@@ -1133,7 +1245,7 @@ static int ensure_graph(fsv_ctx* c, int cap) {
 
 // Copies f_k (the committed parent vector of iteration k) to host.
 static int copy_snapshot(fsv_ctx* c, int k, int32_t* dst) {
-  const int* src = (k == 1) ? c->Y.p : bufN(c, k);
+  const int* src = (k == 1) ? c->Y : bufN(c, k);
   CUDA_TRY(cudaMemcpyAsync(dst, src, sizeof(int) * c->n, cudaMemcpyDeviceToHost, c->stream));
   return FSV_OK;
 }
@@ -1170,7 +1282,7 @@ static int solve_impl(fsv_ctx* c, const fsv_config* cfg, int32_t* snapshots, int
   if (graph_mode && (rc = ensure_graph(c, cap))) return rc;
   CUDA_TRY(cudaEventRecord(c->events[0], st));
   k_solve_init<<<grid_for(c, std::max<long long>(c->HT, (long long)cap * NCOUNT), 256), 256, 0, st>>>(
-      c->X.p, c->Y.p, c->G.p, c->n, c->hub_acc.p, c->HT, c->cnt.p, (long long)cap * NCOUNT, c->done.p,
+      c->X, c->Y, c->G, c->n, c->hacc, c->HT, c->cnt.p, (long long)cap * NCOUNT, c->done.p,
       c->ticket.p, c->mode.p, c->policy == 2 ? 1 : 0, c->tstamp.p);
   pmark(c, 1, 6);
   // iteration 1 in closed form: f_1[u] = min(u, smallest neighbour) from the
@@ -1192,7 +1304,7 @@ static int solve_impl(fsv_ctx* c, const fsv_config* cfg, int32_t* snapshots, int
   }
   {
     FirstArgs fa;
-    fa.f1 = c->f1.p; fa.Y = c->Y.p; fa.G = c->G.p; fa.X = c->X.p; fa.n = c->n;
+    fa.f1 = c->f1.p; fa.Y = c->Y; fa.G = c->G; fa.X = c->X; fa.n = c->n;
     fa.hub_id = c->hub_id.p; fa.G_hub = c->G_hub.p; fa.H = c->HT; fa.cnt = c->cnt.p;
     fa.partials = c->partials.p; fa.ticket = c->ticket.p; fa.done = c->done.p; fa.max_iter = cap;
     fa.dl = delta_out(c);
@@ -1335,7 +1447,7 @@ extern "C" int fsv_get_labels(fsv_ctx* c, int32_t* labels) {
   if (!c->n) return FSV_OK;
   if (!labels) return fail(FSV_ERR_CONTRACT, "labels is NULL");
   CUDA_TRY(cudaSetDevice(c->device));
-  CUDA_TRY(cudaMemcpyAsync(labels, c->G.p, sizeof(int) * c->n, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(cudaMemcpyAsync(labels, c->G, sizeof(int) * c->n, cudaMemcpyDeviceToHost, c->stream));
   CUDA_TRY(cudaStreamSynchronize(c->stream));
   return FSV_OK;
 }

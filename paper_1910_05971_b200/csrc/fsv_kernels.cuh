@@ -62,6 +62,15 @@ constexpr int STEPS = FSV_STEPS;         // steps per span
 constexpr int SPAN = STEP * STEPS;       // entries per warp task
 constexpr int HOOK_THREADS = FSV_HOOK_THREADS;
 constexpr int PUSH_SCRATCH_BYTES = HOOK_THREADS * 20;  // s_start, s_excl (8 B) + s_val (4 B)
+// Column-side minima aimed at the HOT_ACC most connected hubs are combined in
+// shared memory per CTA and flushed once at the end: a top hub can be the
+// target of ~1e5 reductions per iteration, which would otherwise serialise
+// on the one L2 slice that owns its line.
+#ifndef FSV_HOT_ACC
+#define FSV_HOT_ACC 2048
+#endif
+constexpr int HOT_ACC = FSV_HOT_ACC;
+constexpr int SMEM_OPTIN_INTS = 232448 / 4;   // 227 KB opt-in dynamic shared memory per CTA
 constexpr int SC_THREADS = 512;
 constexpr int NCOUNT = 16;               // counter slots per iteration
 enum { C_GF = 0, C_F = 1, C_NONSTAR = 2, C_ROOTS = 3, C_VIOL = 4,   // vertex-pass counters
@@ -88,6 +97,10 @@ __device__ __forceinline__ int ldg(const int* p) { return __ldg(p); }
 
 __device__ __forceinline__ void red_min(int* p, int v) {
   asm volatile("red.relaxed.gpu.global.min.s32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ void red_min_shared(uint32_t saddr, int v) {
+  asm volatile("red.shared.min.s32 [%0], %1;" :: "r"(saddr), "r"(v) : "memory");
 }
 
 // ---- argument blocks --------------------------------------------------------
@@ -436,10 +449,15 @@ __global__ void __launch_bounds__(HOOK_THREADS, 1) k_hook(HookArgs a) {
 #endif
     return;
   }
+  // s_hub[0, H): gf of the shared-memory hubs; s_hub[H, H + hot): this CTA's
+  // accumulator of the hottest hub slots
+  const int hot = min(a.H, HOT_ACC);
   for (int i = threadIdx.x; i < (a.H >> 2); i += blockDim.x)
     reinterpret_cast<int4*>(s_hub)[i] = reinterpret_cast<const int4*>(a.G_hub)[i];
+  for (int i = threadIdx.x; i < hot; i += blockDim.x) s_hub[a.H + i] = INF;
   __syncthreads();
   const uint32_t s_base = (uint32_t)__cvta_generic_to_shared(s_hub);
+  const uint32_t s_acc = s_base + 4u * (uint32_t)a.H;
 
   const int* __restrict__ F = a.F;
   const int* __restrict__ G = a.G;
@@ -536,7 +554,8 @@ __global__ void __launch_bounds__(HOOK_THREADS, 1) k_hook(HookArgs a) {
           t[j] = -1;
           if ((act >> j) & 1u) {
             if ((hubm >> j) & 1u) {
-              red_min(hub_acc + w[j], y[j]);
+              if (w[j] < hot) red_min_shared(s_acc + 4u * (uint32_t)w[j], y[j]);
+              else red_min(hub_acc + w[j], y[j]);
             } else {
               red_min(N + w[j], y[j]);
               t[j] = ldg(F + w[j]);
@@ -579,6 +598,11 @@ __global__ void __launch_bounds__(HOOK_THREADS, 1) k_hook(HookArgs a) {
     }
     // the run still open at the span end: partial minimum of row carry_u
     if (lane == 0 && carry_run < carry_gu) emit_row(carry_u, carry_gu, carry_run, F, G, N);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < hot; i += blockDim.x) {
+    const int v = s_hub[a.H + i];
+    if (v != INF) red_min(hub_acc + i, v);
   }
 }
 

@@ -10,5 +10,5 @@ g = fb.build_csr(n, pairs)
 s = fb.Solver(0)
 s.upload(g)
 for _ in range(reps):
-    st = s.solve()
+    st = s.solve(profile=len(sys.argv) > 3)
 print("iters", st.iterations, "ms", st.solve_ms)

@@ -3,6 +3,9 @@ import os, sys
 from pathlib import Path
 sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 import numpy as np, torch
+from paper_1910_05971_b200 import _native
+if len(sys.argv) > 1:
+    _native.LIB_FASTSV_PATH = Path(sys.argv[1]).resolve()
 import paper_1910_05971_b200 as fb
 from paper_1910_05971_b200 import generators as gen
 n, pairs = gen.baseline_graph(2)
@@ -26,4 +29,4 @@ d_off = torch.empty_like(off, device="cuda"); d_cols = torch.empty_like(cols, de
 def cp():
     d_off.copy_(off, non_blocking=True); d_cols.copy_(cols, non_blocking=True)
 h2d = timed(cp)
-print(f"chunks={os.environ.get('FSV_UPLOAD_CHUNKS','default')} upload {up:.2f} ms  solve {sol:.3f} ms  pure H2D {h2d:.2f} ms")
+print(f"{Path(sys.argv[1]).stem if len(sys.argv) > 1 else ''} chunks={os.environ.get('FSV_UPLOAD_CHUNKS','default')} upload {up:.2f} ms  solve {sol:.3f} ms  pure H2D {h2d:.2f} ms")
