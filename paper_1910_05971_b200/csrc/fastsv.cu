@@ -181,7 +181,7 @@ struct fsv_ctx {
   long long rcap = 0;
   int dgrid = 1;
   // solve state
-  DBuf<int> vec, G_hub, hub_acc, done;
+  DBuf<int> xb, yb, gb, G_hub, hub_acc, done;   // xb/yb: parent buffers, gb: gf
   int* hacc = nullptr;   // vec: slab holding X, Y, G
   int* X = nullptr;
   int* Y = nullptr;
@@ -260,11 +260,11 @@ extern "C" int fsv_create(int device, fsv_ctx** out) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_shortcut, SC_THREADS, 0);
     c->sc_grid = std::max(1, per_sm) * c->sm_count;
   }
-  cudaError_t e = cudaFuncSetAttribute(k_hook<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       std::max((kHubMax + HOT_ACC) * (int)sizeof(int), PUSH_SCRATCH_BYTES));
+  const int hook_smem = std::max((kHubMax + HOT_ACC) * (int)sizeof(int), PUSH_SCRATCH_BYTES);
+  cudaError_t e = cudaFuncSetAttribute(k_hook<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       hook_smem);
   if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(k_hook<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             std::max((kHubMax + HOT_ACC) * (int)sizeof(int), PUSH_SCRATCH_BYTES));
+    e = cudaFuncSetAttribute(k_hook<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, hook_smem);
   if (e != cudaSuccess) {
     delete c;
     return fail(FSV_ERR_RUNTIME, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
@@ -1007,10 +1007,8 @@ static int upload_impl(fsv_ctx* c, int64_t n, const int64_t* h_off, const ColT* 
 
   // solve buffers: n + dummy vertex, padded for 16-byte vector access
   const size_t nv = ((size_t)n + 1 + 63) / 64 * 64;
-  CUDA_TRY(c->vec.alloc(3 * nv));
-  c->X = c->vec.p;
-  c->Y = c->X + nv;
-  c->G = c->Y + nv;
+  CUDA_TRY(c->xb.alloc(nv)); CUDA_TRY(c->yb.alloc(nv)); CUDA_TRY(c->gb.alloc(nv));
+  c->X = c->xb.p; c->Y = c->yb.p; c->G = c->gb.p;
   CUDA_TRY(c->G_hub.alloc(std::max(HT, 4))); {
     long long hpad = 0;   // dev: FSV_HPAD shifts the hub accumulator (placement checks)
     if (const char* e = getenv("FSV_HPAD")) hpad = atoll(e);
@@ -1172,9 +1170,11 @@ static int launch_iteration(fsv_ctx* c, int k, int max_iter, bool graph = false)
     // for the grid barrier of the sparse (push) path
     pmark(c, k, 0);
     void* kargs[] = {&a};
-    const size_t dyn = std::max<size_t>((size_t)(c->H + std::min(c->H, HOT_ACC)) * sizeof(int),
+    const size_t dyn = std::max<size_t>(c->H ? (size_t)(HOT_ACC + c->H) * sizeof(int) : 0,
                                         PUSH_SCRATCH_BYTES);
-    const void* fn = c->HT > c->H ? (const void*)k_hook<true> : (const void*)k_hook<false>;
+    const void* fn = c->HT > c->H ? (const void*)k_hook<true, true>
+                     : c->H       ? (const void*)k_hook<true, false>
+                                  : (const void*)k_hook<false, false>;
     CUDA_TRY(cudaLaunchCooperativeKernel(fn, dim3(c->sm_count), dim3(HOOK_THREADS), kargs, dyn, st));
     pmark(c, k, 1);
     ++c->launches;

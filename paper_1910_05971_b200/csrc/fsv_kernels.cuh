@@ -408,7 +408,9 @@ __device__ __forceinline__ int gather_gf_tier(uint32_t c, uint32_t s_base, const
 // differs and no carried minimum is pending, the whole step is a no-op apart
 // from carry bookkeeping — the common case once components have converged.
 
-template <bool TIER>
+// HUBS = false (no hub slots, H == 0) compiles the hub table, hub mask and
+// accumulators out; TIER (implies HUBS) adds the L2 rank tier gathers.
+template <bool HUBS, bool TIER>
 __global__ void __launch_bounds__(HOOK_THREADS, 1) k_hook(HookArgs a) {
   extern __shared__ int s_hub[];
   if (*(volatile const int*)a.done) return;
@@ -449,15 +451,18 @@ __global__ void __launch_bounds__(HOOK_THREADS, 1) k_hook(HookArgs a) {
 #endif
     return;
   }
-  // s_hub[0, H): gf of the shared-memory hubs; s_hub[H, H + hot): this CTA's
-  // accumulator of the hottest hub slots
-  const int hot = min(a.H, HOT_ACC);
-  for (int i = threadIdx.x; i < (a.H >> 2); i += blockDim.x)
-    reinterpret_cast<int4*>(s_hub)[i] = reinterpret_cast<const int4*>(a.G_hub)[i];
-  for (int i = threadIdx.x; i < hot; i += blockDim.x) s_hub[a.H + i] = INF;
-  __syncthreads();
-  const uint32_t s_base = (uint32_t)__cvta_generic_to_shared(s_hub);
-  const uint32_t s_acc = s_base + 4u * (uint32_t)a.H;
+  // s_hub[0, HOT_ACC): this CTA's accumulator of the hottest hub slots;
+  // s_hub[HOT_ACC, HOT_ACC + H): gf of the shared-memory hubs. Both bases are
+  // constants, so neither costs a register in the loop. Only slots < HT ever
+  // receive a value, so both passes over the accumulator run to HOT_ACC.
+  if (HUBS) {
+    for (int i = threadIdx.x; i < (a.H >> 2); i += blockDim.x)
+      reinterpret_cast<int4*>(s_hub + HOT_ACC)[i] = reinterpret_cast<const int4*>(a.G_hub)[i];
+    for (int i = threadIdx.x; i < HOT_ACC; i += blockDim.x) s_hub[i] = INF;
+    __syncthreads();
+  }
+  const uint32_t s_acc = (uint32_t)__cvta_generic_to_shared(s_hub);
+  const uint32_t s_base = s_acc + 4u * HOT_ACC;
 
   const int* __restrict__ F = a.F;
   const int* __restrict__ G = a.G;
@@ -465,15 +470,18 @@ __global__ void __launch_bounds__(HOOK_THREADS, 1) k_hook(HookArgs a) {
   int* __restrict__ hub_acc = a.hub_acc;
   const int lane = threadIdx.x & 31;
   const unsigned lt = (1u << lane) - 1u;
-  const long long nwarps = (long long)gridDim.x * (blockDim.x >> 5);
-  const long long gw = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  // span counts fit 32 bits (2^31 spans = 2^41 entries); a 64-bit counter
+  // costs a register the loop body cannot spare
+  const int nwarps = gridDim.x * (blockDim.x >> 5);
+  const int gw = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int nspans = (int)a.nspans;
   const uint64_t pol = policy_evict_first();
 
-  for (long long s = gw; s < a.nspans; s += nwarps) {
+  for (int s = gw; s < nspans; s += nwarps) {
     int carry_u = ldg(a.span_row + s);              // row open at the span start
     int carry_gu = carry_u >= 0 ? ldg(G + carry_u) : INF;
     int carry_run = INF;
-    const uint4* p = reinterpret_cast<const uint4*>(a.ecol + s * SPAN) + 2 * lane;
+    const uint4* p = reinterpret_cast<const uint4*>(a.ecol + (size_t)s * SPAN) + 2 * lane;
     uint4 n0 = ld_stream(p, pol), n1 = ld_stream(p + 1, pol);
 #pragma unroll 1
     for (int st = 0; st < STEPS; ++st) {
@@ -541,7 +549,7 @@ __global__ void __launch_bounds__(HOOK_THREADS, 1) k_hook(HookArgs a) {
         w[j] = h ? cu : (int)(c[j] & IDMASK);
         y[j] = yj;
         act |= ((yj < gj) && !first ? 1u : 0u) << j;
-        hubm |= (!h && (c[j] & HUB) ? 1u : 0u) << j;
+        if (HUBS) hubm |= (!h && (c[j] & HUB) ? 1u : 0u) << j;
         seen |= h;
         cu = h ? (int)(c[j] & IDMASK) : cu;
         cgu = h ? val[j] : cgu;
@@ -553,8 +561,8 @@ __global__ void __launch_bounds__(HOOK_THREADS, 1) k_hook(HookArgs a) {
         for (int j = 0; j < EPL; ++j) {
           t[j] = -1;
           if ((act >> j) & 1u) {
-            if ((hubm >> j) & 1u) {
-              if (w[j] < hot) red_min_shared(s_acc + 4u * (uint32_t)w[j], y[j]);
+            if (HUBS && ((hubm >> j) & 1u)) {
+              if (w[j] < HOT_ACC) red_min_shared(s_acc + 4u * (uint32_t)w[j], y[j]);
               else red_min(hub_acc + w[j], y[j]);
             } else {
               red_min(N + w[j], y[j]);
@@ -599,10 +607,12 @@ __global__ void __launch_bounds__(HOOK_THREADS, 1) k_hook(HookArgs a) {
     // the run still open at the span end: partial minimum of row carry_u
     if (lane == 0 && carry_run < carry_gu) emit_row(carry_u, carry_gu, carry_run, F, G, N);
   }
-  __syncthreads();
-  for (int i = threadIdx.x; i < hot; i += blockDim.x) {
-    const int v = s_hub[a.H + i];
-    if (v != INF) red_min(hub_acc + i, v);
+  if (HUBS) {
+    __syncthreads();
+    for (int i = threadIdx.x; i < HOT_ACC; i += blockDim.x) {
+      const int v = s_hub[i];
+      if (v != INF) red_min(hub_acc + i, v);
+    }
   }
 }
 
