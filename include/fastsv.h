@@ -106,6 +106,29 @@ int fsv_upload_csr(fsv_ctx* ctx, int64_t n, const int64_t* row_offsets,
 int fsv_upload_csr64(fsv_ctx* ctx, int64_t n, const int64_t* row_offsets,
                      const int64_t* col_indices, int64_t row_begin, int64_t row_end);
 
+/*
+ * Upload a raw edge list and build the CsrGraph on the device with
+ * svcc.build_csr's semantics (graph.py:55-97): every pair range-checked
+ * (status 1, "edge (u, v) out of range for n=N" for the first offending pair
+ * in input order, graph.py:71-75), self-loops dropped, both orientations
+ * stored, duplicates merged, rows sorted. Then the device layout is built as
+ * by fsv_upload_csr for rows [row_begin, row_end). pairs: m (u, v) pairs,
+ * 2*m ids, int32 or int64 (the reference's ID_DTYPE).
+ */
+int fsv_upload_edges(fsv_ctx* ctx, int64_t n, int64_t m, const int32_t* pairs,
+                     int64_t row_begin, int64_t row_end);
+int fsv_upload_edges64(fsv_ctx* ctx, int64_t n, int64_t m, const int64_t* pairs,
+                       int64_t row_begin, int64_t row_end);
+
+/*
+ * Copy the resident symmetric CSR to host: row_offsets (n+1, int64, full
+ * graph) and the columns of this context's rows (csr_entries of them; the
+ * count is returned in *csr_entries when cols is NULL). Lets callers obtain
+ * the CsrGraph that fsv_upload_edges built (CsrGraph.row_offsets /
+ * col_indices, graph.py:20-52).
+ */
+int fsv_get_csr(fsv_ctx* ctx, int64_t* row_offsets, int32_t* cols, int64_t* csr_entries);
+
 /* Run FastSV to convergence on the resident graph. Labels stay on device. */
 int fsv_solve(fsv_ctx* ctx, const fsv_config* cfg, fsv_stats* stats);
 

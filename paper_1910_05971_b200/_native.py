@@ -44,6 +44,9 @@ FASTSV_SYMBOLS = {
     "fsv_set_stream": (c_int, [c_void_p, c_void_p]),
     "fsv_upload_csr": (c_int, [c_void_p, c_int64, c_void_p, c_void_p, c_int64, c_int64]),
     "fsv_upload_csr64": (c_int, [c_void_p, c_int64, c_void_p, c_void_p, c_int64, c_int64]),
+    "fsv_upload_edges": (c_int, [c_void_p, c_int64, c_int64, c_void_p, c_int64, c_int64]),
+    "fsv_upload_edges64": (c_int, [c_void_p, c_int64, c_int64, c_void_p, c_int64, c_int64]),
+    "fsv_get_csr": (c_int, [c_void_p, c_void_p, c_void_p, POINTER(c_int64)]),
     "fsv_solve": (c_int, [c_void_p, POINTER(FsvConfig), POINTER(FsvStats)]),
     "fsv_get_labels": (c_int, [c_void_p, c_void_p]),
     "fsv_get_labels64": (c_int, [c_void_p, c_void_p]),

@@ -159,6 +159,7 @@ struct fsv_ctx {
   DBuf<int64_t> csr_off;
   DBuf<int> csr_cols;
   int64_t col_base = 0, row_begin = 0, row_end = 0;
+  int64_t csr_local = 0;   // entries of this rank's rows in csr_cols
   // changed-gf lists of the vertex pass (one region per warp)
   DBuf<int> dlist, dcount, mode;
   DBuf<int2> chunks;
@@ -182,7 +183,7 @@ struct fsv_ctx {
   int dgrid = 1;
   // solve state
   DBuf<int> xb, yb, gb, G_hub, hub_acc, done;   // xb/yb: parent buffers, gb: gf
-  int* hacc = nullptr;   // vec: slab holding X, Y, G
+  int* hacc = nullptr;   // hub accumulator start inside hub_acc
   int* X = nullptr;
   int* Y = nullptr;
   int* G = nullptr;
@@ -190,6 +191,8 @@ struct fsv_ctx {
   DBuf<unsigned int> ticket;
   DBuf<unsigned> partials;
   int* h_done = nullptr;  // pinned
+  int64_t* h_off_pin = nullptr;   // pinned host copy of device-built row offsets
+  size_t h_off_cap = 0;
   std::vector<cudaEvent_t> events;
   // profile mode: events around every kernel of iteration k: [k][0..7]
   std::vector<cudaEvent_t> pev;
@@ -283,6 +286,7 @@ extern "C" int fsv_destroy(fsv_ctx* c) {
   if (c->graph) cudaGraphDestroy(c->graph);
   if (c->comm && g_nccl.CommDestroy) g_nccl.CommDestroy(c->comm);
   if (c->h_done) cudaFreeHost(c->h_done);
+  if (c->h_off_pin) cudaFreeHost(c->h_off_pin);
   for (auto e : c->chunk_ev) cudaEventDestroy(e);
   if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
   if (c->own_stream) cudaStreamDestroy(c->own_stream);
@@ -731,6 +735,68 @@ __global__ void k_narrow(const int64_t* __restrict__ in, long long m, int* __res
     out[e] = (int)in[e];
 }
 
+// ---- CSR build from an edge list on the device (graph.py:55-97) -------------
+// Directed entry (u, v) -> key u << b | v (b id bits, n <= 2^b). A dropped
+// pair (self-loop, or out of range: reported) gets the all-ones 2b-bit key,
+// which no kept entry has (it would need u == v) and which sorts last.
+template <typename IdT>
+struct PairT;
+template <>
+struct PairT<int32_t> { using V = int2; };
+template <>
+struct PairT<int64_t> { using V = longlong2; };
+
+template <typename IdT>
+__global__ void k_edge_keys(const IdT* __restrict__ pairs, long long i0, long long i1, long long n, int b,
+                            unsigned long long* __restrict__ keys, unsigned long long* bad) {
+  const unsigned long long sent = (1ull << (2 * b)) - 1ull;
+  const auto* P = reinterpret_cast<const typename PairT<IdT>::V*>(pairs);
+  for (long long i = i0 + blockIdx.x * (long long)blockDim.x + threadIdx.x; i < i1;
+       i += (long long)gridDim.x * blockDim.x) {
+    const auto p = P[i];
+    const long long u = (long long)p.x, v = (long long)p.y;
+    ulonglong2 k = make_ulonglong2(sent, sent);
+    if (u < 0 || u >= n || v < 0 || v >= n) {
+      atomicMin(bad, (unsigned long long)i);
+    } else if (u != v) {
+      k.x = ((unsigned long long)u << b) | (unsigned long long)v;
+      k.y = ((unsigned long long)v << b) | (unsigned long long)u;
+    }
+    reinterpret_cast<ulonglong2*>(keys)[i] = k;
+  }
+}
+
+// Unique-key count without the sentinel: out[0] = entries of the CSR.
+__global__ void k_key_count(const unsigned long long* keys, const long long* nuniq, int b, long long* out) {
+  const unsigned long long sent = (1ull << (2 * b)) - 1ull;
+  const long long u = *nuniq;
+  out[0] = (u > 0 && keys[u - 1] == sent) ? u - 1 : u;
+}
+
+// CSR from sorted unique keys: cols[i] = v, row_offsets[r] = first entry of
+// row >= r (each entry fills the offsets of the rows up to its own when it
+// starts a row; the last entry fills the tail).
+__global__ void k_csr_from_keys(const unsigned long long* __restrict__ keys, const long long* M_p, long long n,
+                                int b, int64_t* __restrict__ off, int* __restrict__ cols) {
+  const long long M = *M_p;
+  const unsigned long long mask = (1ull << b) - 1ull;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  const long long t0 = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (M == 0) {
+    for (long long r = t0; r <= n; r += stride) off[r] = 0;
+    return;
+  }
+  for (long long i = t0; i < M; i += stride) {
+    const unsigned long long k = keys[i];
+    const long long u = (long long)(k >> b);
+    cols[i] = (int)(k & mask);
+    const long long up = i ? (long long)(keys[i - 1] >> b) : -1;
+    for (long long r = up + 1; r <= u; ++r) off[r] = i;
+    if (i == M - 1)
+      for (long long r = u + 1; r <= n; ++r) off[r] = M;
+  }
+}
+
 static int grid_for(fsv_ctx* c, long long work, int threads, int per_sm = 8) {
   long long g = (work + threads - 1) / threads;
   g = std::min<long long>(g, (long long)c->sm_count * per_sm);
@@ -744,9 +810,12 @@ DBuf<int32_t>& cols_buffer<int32_t>(fsv_ctx* c) { return c->csr_cols; }
 template <>
 DBuf<int64_t>& cols_buffer<int64_t>(fsv_ctx* c) { return c->ws.cols64; }
 
+// h_off: host copy of the full row offsets. Columns come from host h_cols
+// (copied up in chunks), or, when d_src is set, from a device array holding
+// every row's columns whose offsets are already in csr_off (fsv_upload_edges).
 template <typename ColT>
 static int upload_impl(fsv_ctx* c, int64_t n, const int64_t* h_off, const ColT* h_cols,
-                       int64_t row_begin, int64_t row_end) {
+                       int64_t row_begin, int64_t row_end, const ColT* d_src = nullptr) {
   if (!c) return fail(FSV_ERR_CONTRACT, "NULL context");
   if (n < 0) return fail(FSV_ERR_INPUT, "vertex count must be non-negative, got %lld", (long long)n);
   if (n >= (int64_t)IDMASK) return fail(FSV_ERR_INPUT, "n=%lld exceeds the device id range", (long long)n);
@@ -759,7 +828,7 @@ static int upload_impl(fsv_ctx* c, int64_t n, const int64_t* h_off, const ColT* 
   const int64_t e_begin = h_off[row_begin], e_end = h_off[row_end];
   const int64_t mloc = e_end - e_begin;
   if (mloc < 0 || e_begin < 0) return fail(FSV_ERR_INPUT, "row_offsets must be non-decreasing");
-  if (mloc > 0 && !h_cols) return fail(FSV_ERR_CONTRACT, "col_indices is NULL");
+  if (mloc > 0 && !h_cols && !d_src) return fail(FSV_ERR_CONTRACT, "col_indices is NULL");
   CUDA_TRY(cudaSetDevice(c->device));
   cudaStream_t st = c->stream;
   c->ready = false;
@@ -777,7 +846,8 @@ static int upload_impl(fsv_ctx* c, int64_t n, const int64_t* h_off, const ColT* 
   DBuf<ColT>& d_cols = cols_buffer<ColT>(c);
   CUDA_TRY(d_off.alloc((size_t)n + 1));
   CUDA_TRY(d_cols.alloc((size_t)mloc));
-  CUDA_TRY(cudaMemcpyAsync(d_off.p, h_off, sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice, st));
+  if (!d_src)
+    CUDA_TRY(cudaMemcpyAsync(d_off.p, h_off, sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice, st));
   // columns go up in row-aligned chunks on the copy stream, so the degree
   // sort and the orientation of earlier chunks overlap the transfer
   std::vector<int64_t> chunk_rows;  // row boundaries, chunk k = [chunk_rows[k], chunk_rows[k+1])
@@ -785,9 +855,9 @@ static int upload_impl(fsv_ctx* c, int64_t n, const int64_t* h_off, const ColT* 
     // eighths of the entries, the last eighth cut geometrically (1/16, 1/32,
     // 1/64, 1/64) so the work trailing the final copy is small
     std::vector<int64_t> cut;  // chunk ends in 1/64ths of mloc
-    if (mloc >= ((int64_t)1 << 24)) cut = {8, 16, 24, 32, 40, 48, 56, 60, 62, 63, 64};
+    if (mloc >= ((int64_t)1 << 24) && !d_src) cut = {8, 16, 24, 32, 40, 48, 56, 60, 62, 63, 64};
     else cut = {64};
-    if (const char* env = getenv("FSV_UPLOAD_CHUNKS")) {   // dev: K equal chunks
+    if (const char* env = d_src ? nullptr : getenv("FSV_UPLOAD_CHUNKS")) {   // dev: K equal chunks
       const int k_eq = std::max(1, std::min(64, atoi(env)));
       cut.clear();
       for (int k = 1; k <= k_eq; ++k) cut.push_back(64 * k / k_eq);
@@ -811,9 +881,12 @@ static int upload_impl(fsv_ctx* c, int64_t n, const int64_t* h_off, const ColT* 
     CUDA_TRY(cudaStreamWaitEvent(c->copy_stream, off_ready, 0));
     for (int k = 0; k < K; ++k) {
       const int64_t lo = h_off[chunk_rows[k]] - e_begin, hi = h_off[chunk_rows[k + 1]] - e_begin;
-      if (hi > lo)
+      if (hi > lo && !d_src)
         CUDA_TRY(cudaMemcpyAsync(d_cols.p + lo, h_cols + lo, sizeof(ColT) * (hi - lo),
                                  cudaMemcpyHostToDevice, c->copy_stream));
+      else if (hi > lo && d_src + e_begin + lo != d_cols.p + lo)   // this rank's slice of a device CSR
+        CUDA_TRY(cudaMemcpyAsync(d_cols.p + lo, d_src + e_begin + lo, sizeof(ColT) * (hi - lo),
+                                 cudaMemcpyDeviceToDevice, c->copy_stream));
       CUDA_TRY(cudaEventRecord(c->chunk_ev[k], c->copy_stream));
       if (udbg) {
         cudaEvent_t e; cudaEventCreate(&e); cudaEventRecord(e, c->copy_stream);
@@ -980,7 +1053,7 @@ static int upload_impl(fsv_ctx* c, int64_t n, const int64_t* h_off, const ColT* 
     const int64_t* it = std::upper_bound(h_off, h_off + n + 1, e);
     const long long u = (long long)(it - h_off) - 1;
     return fail(FSV_ERR_INPUT, "edge (%lld, %lld) out of range for n=%lld", u,
-                (long long)h_cols[h_bad], (long long)n);
+                h_cols ? (long long)h_cols[h_bad] : -1LL, (long long)n);
   }
   const long long Epad = (E + SPAN - 1) / SPAN * SPAN;
   umark(4);
@@ -1002,6 +1075,7 @@ static int upload_impl(fsv_ctx* c, int64_t n, const int64_t* h_off, const ColT* 
       k_narrow<<<grid_for(c, mloc, 256), 256, 0, st>>>(d_cols.p, mloc, c->csr_cols.p);
   }
   c->col_base = e_begin;
+  c->csr_local = mloc;
   c->row_begin = row_begin;
   c->row_end = row_end;
 
@@ -1085,6 +1159,168 @@ extern "C" int fsv_upload_csr(fsv_ctx* c, int64_t n, const int64_t* off, const i
 extern "C" int fsv_upload_csr64(fsv_ctx* c, int64_t n, const int64_t* off, const int64_t* cols,
                                 int64_t row_begin, int64_t row_end) {
   return upload_impl<int64_t>(c, n, off, cols, row_begin, row_end);
+}
+
+// Edge list -> CsrGraph on the device (graph.py:55-97), then the layout of
+// upload_impl. Pairs go up in chunks on the copy stream while the keys of
+// earlier chunks are formed; one radix sort over 2b key bits; unique; CSR.
+// Temporaries are stream-ordered allocations returned after the build.
+template <typename IdT>
+static int upload_edges_impl(fsv_ctx* c, int64_t n, int64_t m, const IdT* h_pairs, int64_t row_begin,
+                             int64_t row_end) {
+  if (!c) return fail(FSV_ERR_CONTRACT, "NULL context");
+  if (n < 0) return fail(FSV_ERR_INPUT, "vertex count must be non-negative, got %lld", (long long)n);
+  if (n >= (int64_t)IDMASK) return fail(FSV_ERR_INPUT, "n=%lld exceeds the device id range", (long long)n);
+  if (m < 0) return fail(FSV_ERR_CONTRACT, "negative edge count %lld", (long long)m);
+  if (m > 0 && !h_pairs) return fail(FSV_ERR_CONTRACT, "pairs is NULL");
+  if (row_begin < 0 || row_end < row_begin || row_end > n)
+    return fail(FSV_ERR_CONTRACT, "row range [%lld, %lld) invalid for n=%lld", (long long)row_begin,
+                (long long)row_end, (long long)n);
+  CUDA_TRY(cudaSetDevice(c->device));
+  cudaStream_t st = c->stream;
+  c->ready = false;
+  c->labels_ready = 0;
+  int b = 1;
+  while ((1LL << b) < n) ++b;        // ids < n <= 2^b
+  const long long m2 = 2 * m;
+  IdT* d_pairs = nullptr;
+  unsigned long long *ka = nullptr, *kb = nullptr;
+  long long* d_cnt = nullptr;        // [0] unique keys, [1] CSR entries
+  void* d_tmp = nullptr;
+  int* d_full = nullptr;             // all rows' columns when only a row range is kept
+  auto release = [&]() {
+    if (d_pairs) cudaFreeAsync(d_pairs, st);
+    if (ka) cudaFreeAsync(ka, st);
+    if (kb) cudaFreeAsync(kb, st);
+    if (d_tmp) cudaFreeAsync(d_tmp, st);
+    if (d_full) cudaFreeAsync(d_full, st);
+    if (d_cnt) cudaFreeAsync(d_cnt, st);
+    cudaStreamSynchronize(st);
+  };
+#define EDGE_TRY(x)                                                              \
+  do {                                                                           \
+    cudaError_t e_ = (x);                                                        \
+    if (e_ != cudaSuccess) {                                                     \
+      release();                                                                 \
+      return fail(FSV_ERR_RUNTIME, "%s: %s", #x, cudaGetErrorString(e_));        \
+    }                                                                            \
+  } while (0)
+  EDGE_TRY(cudaMallocAsync(&d_cnt, 2 * sizeof(long long), st));
+  EDGE_TRY(c->ws.bad.alloc(2));
+  EDGE_TRY(cudaMemsetAsync(c->ws.bad.p, 0xff, sizeof(unsigned long long), st));
+  if (m) {
+    EDGE_TRY(cudaMallocAsync(&d_pairs, sizeof(IdT) * m2, st));
+    EDGE_TRY(cudaMallocAsync(&ka, sizeof(unsigned long long) * m2, st));
+    EDGE_TRY(cudaMallocAsync(&kb, sizeof(unsigned long long) * m2, st));
+    // chunked H2D on the copy stream, keys of each chunk as it lands
+    const int K = m >= (1LL << 22) ? 8 : 1;
+    while (c->chunk_ev.size() < (size_t)K + 1) {
+      cudaEvent_t e;
+      EDGE_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      c->chunk_ev.push_back(e);
+    }
+    EDGE_TRY(cudaEventRecord(c->chunk_ev[K], st));          // allocations ordered before the copies
+    EDGE_TRY(cudaStreamWaitEvent(c->copy_stream, c->chunk_ev[K], 0));
+    for (int k = 0; k < K; ++k) {
+      const long long i0 = m * k / K, i1 = m * (k + 1) / K;
+      EDGE_TRY(cudaMemcpyAsync(d_pairs + 2 * i0, h_pairs + 2 * i0, sizeof(IdT) * 2 * (i1 - i0),
+                               cudaMemcpyHostToDevice, c->copy_stream));
+      EDGE_TRY(cudaEventRecord(c->chunk_ev[k], c->copy_stream));
+    }
+    for (int k = 0; k < K; ++k) {
+      const long long i0 = m * k / K, i1 = m * (k + 1) / K;
+      EDGE_TRY(cudaStreamWaitEvent(st, c->chunk_ev[k], 0));
+      if (i1 > i0)
+        k_edge_keys<IdT><<<grid_for(c, i1 - i0, 256, 16), 256, 0, st>>>(d_pairs, i0, i1, n, b, ka, c->ws.bad.p);
+    }
+    unsigned long long h_bad = ~0ull;
+    EDGE_TRY(cudaMemcpyAsync(&h_bad, c->ws.bad.p, sizeof h_bad, cudaMemcpyDeviceToHost, st));
+    EDGE_TRY(cudaStreamSynchronize(st));
+    if (h_bad != ~0ull) {
+      // graph.py:71-75: the first pair (input order) with an endpoint out of range
+      const long long u = (long long)h_pairs[2 * h_bad], v = (long long)h_pairs[2 * h_bad + 1];
+      release();
+      return fail(FSV_ERR_INPUT, "edge (%lld, %lld) out of range for n=%lld", u, v, (long long)n);
+    }
+    cudaFreeAsync(d_pairs, st);
+    d_pairs = nullptr;
+    // sort (2b key bits), unique
+    size_t sort_bytes = 0, uniq_bytes = 0;
+    cub::DoubleBuffer<unsigned long long> dbuf(ka, kb);
+    cub::DeviceRadixSort::SortKeys(nullptr, sort_bytes, dbuf, m2, 0, 2 * b, st);
+    cub::DeviceSelect::Unique(nullptr, uniq_bytes, ka, kb, d_cnt, m2, st);
+    EDGE_TRY(cudaMallocAsync(&d_tmp, std::max(sort_bytes, uniq_bytes), st));
+    EDGE_TRY(cub::DeviceRadixSort::SortKeys(d_tmp, sort_bytes, dbuf, m2, 0, 2 * b, st));
+    unsigned long long* sorted = dbuf.Current();
+    unsigned long long* uniq = dbuf.Alternate();
+    EDGE_TRY(cub::DeviceSelect::Unique(d_tmp, uniq_bytes, sorted, uniq, d_cnt, m2, st));
+    k_key_count<<<1, 1, 0, st>>>(uniq, d_cnt, b, d_cnt + 1);
+    long long M = 0;
+    EDGE_TRY(cudaMemcpyAsync(&M, d_cnt + 1, sizeof M, cudaMemcpyDeviceToHost, st));
+    EDGE_TRY(cudaStreamSynchronize(st));
+    // the CSR: offsets into csr_off, columns into csr_cols (full range) or a
+    // temporary from which upload_impl copies this rank's slice
+    EDGE_TRY(c->csr_off.alloc((size_t)n + 1));
+    int* cols_out = nullptr;
+    if (row_begin == 0 && row_end == n) {
+      EDGE_TRY(c->csr_cols.alloc((size_t)std::max<long long>(M, 1)));
+      cols_out = c->csr_cols.p;
+    } else {
+      EDGE_TRY(cudaMallocAsync(&d_full, sizeof(int) * std::max<long long>(M, 1), st));
+      cols_out = d_full;
+    }
+    k_csr_from_keys<<<grid_for(c, std::max<long long>(M, n + 1), 256, 16), 256, 0, st>>>(uniq, d_cnt + 1, n, b,
+                                                                                     c->csr_off.p, cols_out);
+  } else {
+    EDGE_TRY(cudaMemsetAsync(d_cnt + 1, 0, sizeof(long long), st));
+    EDGE_TRY(c->csr_off.alloc((size_t)n + 1));
+    EDGE_TRY(c->csr_cols.alloc(1));
+    k_csr_from_keys<<<grid_for(c, n + 1, 256, 16), 256, 0, st>>>(nullptr, d_cnt + 1, n, b, c->csr_off.p,
+                                                                 c->csr_cols.p);
+  }
+  // host copy of the offsets for the layout build's row bookkeeping
+  if (c->h_off_cap < (size_t)n + 1) {
+    if (c->h_off_pin) cudaFreeHost(c->h_off_pin);
+    c->h_off_pin = nullptr;
+    c->h_off_cap = 0;
+    EDGE_TRY(cudaMallocHost(&c->h_off_pin, sizeof(int64_t) * ((size_t)n + 1)));
+    c->h_off_cap = (size_t)n + 1;
+  }
+  EDGE_TRY(cudaMemcpyAsync(c->h_off_pin, c->csr_off.p, sizeof(int64_t) * (n + 1), cudaMemcpyDeviceToHost, st));
+  EDGE_TRY(cudaStreamSynchronize(st));
+  if (ka) { cudaFreeAsync(ka, st); ka = nullptr; }
+  if (kb) { cudaFreeAsync(kb, st); kb = nullptr; }
+  if (d_tmp) { cudaFreeAsync(d_tmp, st); d_tmp = nullptr; }
+  const int32_t* src = d_full ? d_full : c->csr_cols.p;
+  const int rc = upload_impl<int32_t>(c, n, c->h_off_pin, nullptr, row_begin, row_end, src);
+  release();
+#undef EDGE_TRY
+  return rc;
+}
+
+extern "C" int fsv_upload_edges(fsv_ctx* c, int64_t n, int64_t m, const int32_t* pairs, int64_t row_begin,
+                                int64_t row_end) {
+  return upload_edges_impl<int32_t>(c, n, m, pairs, row_begin, row_end);
+}
+
+extern "C" int fsv_upload_edges64(fsv_ctx* c, int64_t n, int64_t m, const int64_t* pairs, int64_t row_begin,
+                                  int64_t row_end) {
+  return upload_edges_impl<int64_t>(c, n, m, pairs, row_begin, row_end);
+}
+
+extern "C" int fsv_get_csr(fsv_ctx* c, int64_t* row_offsets, int32_t* cols, int64_t* csr_entries) {
+  if (!c) return fail(FSV_ERR_CONTRACT, "NULL context");
+  if (!c->ready) return fail(FSV_ERR_CONTRACT, "no graph uploaded");
+  const int64_t mloc = c->csr_local;
+  if (csr_entries) *csr_entries = mloc;
+  CUDA_TRY(cudaSetDevice(c->device));
+  if (row_offsets)
+    CUDA_TRY(cudaMemcpyAsync(row_offsets, c->csr_off.p, sizeof(int64_t) * (c->n + 1), cudaMemcpyDeviceToHost,
+                             c->stream));
+  if (cols && mloc)
+    CUDA_TRY(cudaMemcpyAsync(cols, c->csr_cols.p, sizeof(int32_t) * mloc, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  return FSV_OK;
 }
 
 // ---------------------------------------------------------------------------

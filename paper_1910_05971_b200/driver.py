@@ -21,8 +21,8 @@ import numpy as np
 
 from . import _native
 from ._native import FsvConfig, FsvStats
-from .errors import DeviceError, raise_for_status
-from .graph import ID_DTYPE, CsrGraph, Labeling, build_csr, labeling_from_parents
+from .errors import DeviceError, InputError, raise_for_status
+from .graph import ID_DTYPE, CsrGraph, Labeling, labeling_from_parents
 
 _FORCE_MODES = ("auto", "dense_only", "sparse_only")
 
@@ -177,6 +177,38 @@ class Solver:
         self.n = n
         self.m = int(offsets[-1]) if n else 0
 
+    def upload_edges(self, n: int, edges, row_begin: int = 0, row_end: int | None = None) -> None:
+        """Edge list in: the CsrGraph is built on the device with
+        svcc.build_csr's semantics (graph.py:55-97: range check with the
+        reference's message, self-loops dropped, both orientations,
+        duplicates merged, rows sorted), then the layout (fsv_upload_edges)."""
+        n = int(n)
+        if n < 0:
+            raise InputError(f"vertex count must be non-negative, got {n}")
+        pairs = edge_pairs(edges)
+        fn = self._lib.fsv_upload_edges if pairs.dtype == np.int32 else self._lib.fsv_upload_edges64
+        row_end = n if row_end is None else int(row_end)
+        _check(fn(self._ctx, n, int(pairs.shape[0]), pairs.ctypes.data if pairs.size else None,
+                  int(row_begin), row_end))
+        self.n = n
+        cnt = ctypes.c_int64(0)
+        _check(self._lib.fsv_get_csr(self._ctx, None, None, ctypes.byref(cnt)))
+        self.m = int(cnt.value)
+
+    def csr(self) -> CsrGraph:
+        """The resident symmetric CSR (full row offsets, this context's
+        columns) as a CsrGraph with the reference's int64 ids."""
+        cnt = ctypes.c_int64(0)
+        _check(self._lib.fsv_get_csr(self._ctx, None, None, ctypes.byref(cnt)))
+        off = np.empty(self.n + 1, dtype=np.int64)
+        cols = np.empty(int(cnt.value), dtype=np.int32)
+        _check(self._lib.fsv_get_csr(self._ctx, off.ctypes.data, cols.ctypes.data if cols.size else None,
+                                     ctypes.byref(cnt)))
+        off.flags.writeable = False
+        c64 = cols.astype(ID_DTYPE)
+        c64.flags.writeable = False
+        return CsrGraph(n=self.n, row_offsets=off, col_indices=c64)
+
     def upload_arrays(self, n: int, offsets_ptr: int, cols_ptr: int, row_begin: int = 0,
                       row_end: int | None = None, int64_cols: bool = False) -> None:
         """Upload from raw host pointers (e.g. pinned buffers) — the e2e path."""
@@ -326,12 +358,30 @@ def fastsv(g, cfg: HookingConfig | None = None, record_snapshots: bool = False,
     return res
 
 
+def edge_pairs(edges) -> np.ndarray:
+    """(k, 2) contiguous int32/int64 array of an edge list, with build_csr's
+    input rules (graph.py:63-69): any iterable of pairs or an integer array."""
+    if isinstance(edges, np.ndarray) and edges.dtype in (np.int32, np.int64):
+        pairs = edges
+    else:
+        pairs = np.asarray(list(edges) if not isinstance(edges, np.ndarray) else edges, dtype=ID_DTYPE)
+    if pairs.size == 0:
+        pairs = pairs.reshape(0, 2)
+    if pairs.ndim != 2 or pairs.shape[1] != 2:
+        raise InputError("edges must be (u, v) pairs")
+    return np.ascontiguousarray(pairs)
+
+
 def connected_components(n: int, edges, device: int = 0) -> np.ndarray:
-    """Edge list in, label vector out (int64, minimum id per component)."""
-    g = build_csr(n, edges)
-    if g.n == 0:
+    """Edge list in, label vector out (int64, minimum id per component).
+    The CSR is built on the device (fsv_upload_edges), then FastSV runs."""
+    n = int(n)
+    solver = default_solver(device)
+    solver.upload_edges(n, edges)
+    if n == 0:
         return np.zeros(0, dtype=ID_DTYPE)
-    return fastsv_la(g, device=device).labeling.labels
+    solver.solve()
+    return solver.labels(np.empty(n, dtype=ID_DTYPE))
 
 
 def device_count() -> int:

@@ -55,3 +55,16 @@ def load_driver_traces():
         a, b = d["off"][i], d["off"][i + 1]
         out[(cfg, name)] = (d["kernel"][a:b].tolist(), d["flops"][a:b].tolist())
     return out
+
+
+def csr_digest(row_offsets, col_indices) -> str:
+    """sha256 (first 16 hex) of a CSR as int64 little-endian bytes: offsets, then columns."""
+    import hashlib
+    h = hashlib.sha256()
+    h.update(np.ascontiguousarray(row_offsets, dtype="<i8").tobytes())
+    h.update(np.ascontiguousarray(col_indices, dtype="<i8").tobytes())
+    return h.hexdigest()[:16]
+
+
+def load_csr_digests():
+    return json.loads((GOLDEN / "csr_digests.json").read_text())

@@ -252,3 +252,103 @@ def test_rank_tier_path(solver, monkeypatch):
             assert iters == o.iterations and gfc.tolist() == o.gf_changed.tolist()
             assert np.array_equal(snaps, o.snapshots)
     solver.set_hub_slots(0)
+
+
+# ---- device CSR build from edge lists (fsv_upload_edges, graph.py:55-97) ----
+
+def test_device_csr_build_matches_reference_suite(solver):
+    """fsv_upload_edges builds exactly svcc.build_csr's arrays (reference-made
+    digests) and the solve on that CSR matches the reference's golden run."""
+    from golden_io import csr_digest, load_csr_digests
+    gold = load_csr_digests()["suite"]
+    solver.set_hub_slots(0)
+    for i, c in enumerate(load_suite()):
+        pairs = c.edges if i % 2 else c.edges.astype(np.int64)    # both id widths
+        solver.upload_edges(c.n, pairs)
+        g = solver.csr()
+        assert g.m == c.m_dir, c.name
+        assert csr_digest(g.row_offsets, g.col_indices) == gold[c.name]["digest"], c.name
+        labels, iters, gfc, fc, ms, snaps = solver.run(snapshots=True, snap_cap=512)
+        assert iters == c.iterations and gfc.tolist() == c.gf_changed, c.name
+        assert np.array_equal(labels, c.labels) and np.array_equal(snaps, c.snapshots), c.name
+
+
+@pytest.mark.parametrize("index", [1, 2, 3, 4])
+def test_device_csr_build_baseline_configs(solver, index):
+    """Full-size configs: the device-built CSR equals the reference's (digest,
+    configs 1 and 3) or the host builder's arrays (configs 2 and 4, whose
+    reference build takes minutes), and the solve reproduces the golden run."""
+    from golden_io import csr_digest, load_csr_digests
+    rec = load_configs()[index]
+    n, pairs = gen.baseline_graph(index)
+    solver.set_hub_slots(0)
+    solver.upload_edges(n, pairs)
+    g = solver.csr()
+    assert g.m == rec["m_dir"]
+    gold = load_csr_digests()["configs"].get(str(index))
+    if gold is not None:
+        assert csr_digest(g.row_offsets, g.col_indices) == gold["digest"]
+    else:
+        h = fb.build_csr(n, pairs)
+        assert np.array_equal(g.row_offsets, h.row_offsets)
+        assert np.array_equal(g.col_indices, h.col_indices)
+    labels, iters, gfc, fc, ms, _ = solver.run()
+    assert iters == rec["iterations"] and gfc.tolist() == rec["gf_changed"]
+    assert gen.pairs_digest(labels) == rec["labels_digest"]
+
+
+def test_device_csr_build_edge_cases(solver):
+    solver.set_hub_slots(0)
+    cases = [
+        (0, np.zeros((0, 2), np.int32)),
+        (1, np.zeros((0, 2), np.int32)),
+        (1, np.array([[0, 0]], np.int32)),                      # self-loop only
+        (5, np.array([[3, 3], [1, 1]], np.int64)),
+        (6, np.array([[5, 0], [0, 5], [5, 0], [2, 2], [4, 1]], np.int32)),
+        (3, [(0, 1), (1, 2)]),                                    # list input
+        (2 ** 20, np.array([[2 ** 20 - 1, 0], [7, 2 ** 19]], np.int64)),
+    ]
+    for n, e in cases:
+        solver.upload_edges(n, e)
+        g = solver.csr()
+        h = fb.build_csr(n, e)
+        assert np.array_equal(g.row_offsets, h.row_offsets), (n, e)
+        assert np.array_equal(g.col_indices, h.col_indices), (n, e)
+        if n:
+            labels, *_ = solver.run()
+            assert np.array_equal(labels, oracle.uf_labels(n, np.asarray(e, np.int64).reshape(-1, 2))), (n, e)
+
+
+def test_device_csr_build_errors(solver):
+    # the first offending pair in input order, with the reference's message
+    with pytest.raises(fb.InputError, match=r"edge \(5, -1\) out of range for n=10"):
+        solver.upload_edges(10, np.array([[0, 1], [5, -1], [7, 100]], np.int64))
+    with pytest.raises(fb.InputError, match=r"edge \(7, 10\) out of range for n=10"):
+        solver.upload_edges(10, np.array([[0, 1], [7, 10], [3, -4]], np.int32))
+    with pytest.raises(fb.InputError, match="vertex count must be non-negative"):
+        solver.upload_edges(-1, [])
+    with pytest.raises(fb.InputError, match=r"edges must be \(u, v\) pairs"):
+        solver.upload_edges(4, np.zeros((2, 3), np.int64))
+    # a failed upload leaves the context usable
+    solver.upload_edges(4, [(0, 1), (2, 3)])
+    labels, *_ = solver.run()
+    assert labels.tolist() == [0, 0, 2, 2]
+
+
+def test_device_csr_build_row_ranges():
+    """Two contexts each build the CSR and keep half the rows: every
+    undirected edge is oriented by exactly one of them, and each keeps the
+    reference's columns of its rows."""
+    n, e = gen.rmat(12, 16, seed=23)
+    h = fb.build_csr(n, e)
+    import bench
+    sizes = []
+    for r in range(2):
+        lo, hi = bench.row_partition(h.row_offsets, 2, r)
+        with fb.Solver(0) as s:
+            s.upload_edges(n, e, lo, hi)
+            g = s.csr()
+            assert np.array_equal(g.row_offsets, h.row_offsets)
+            assert np.array_equal(g.col_indices, h.col_indices[h.row_offsets[lo]:h.row_offsets[hi]])
+            sizes.append(int(s.solve().oriented_entries))
+    assert sum(sizes) == h.m // 2

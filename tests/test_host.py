@@ -107,3 +107,13 @@ def test_permutation_is_bijection():
     p = np.empty(1000, dtype=np.int32)
     assert graphgen_lib().fsvg_permutation(1000, 11, p.ctypes.data) == 0
     assert sorted(p.tolist()) == list(range(1000))
+
+
+def test_build_csr_matches_reference_arrays():
+    """The host CSR builder reproduces svcc.build_csr's arrays exactly
+    (digests made by the reference itself, tests/golden/make_csr_golden.py)."""
+    from golden_io import csr_digest, load_csr_digests
+    gold = load_csr_digests()["suite"]
+    for c in load_suite():
+        g = fb.build_csr(c.n, c.edges)
+        assert csr_digest(g.row_offsets, g.col_indices) == gold[c.name]["digest"], c.name
