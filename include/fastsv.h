@@ -35,7 +35,7 @@ extern "C" {
 #define FSV_ERR_INVARIANT 3
 #define FSV_ERR_RUNTIME 4
 
-#define FSV_ABI_VERSION 1
+#define FSV_ABI_VERSION 2
 
 typedef struct fsv_ctx fsv_ctx;
 
@@ -51,8 +51,20 @@ typedef struct fsv_config {
    * results are identical either way, only the trace's kernel/flops differ. */
   int32_t sparse_policy;
   double sparse_threshold;  /* double: the rule must round like Python's 0.1 * n */
-  int32_t reserved[2];
+  /* 0 = all-flags FastSV on the fast path. FSV_HOOKING_SET | flag bits runs
+   * the reference's HookingConfig variant (algorithms.py:28-35,85-114) on the
+   * generic variant kernels: FSV_HOOKING_SET alone is simplified_sv
+   * (algorithms.py:66-76,145-149, trace-identical to all flags off). The
+   * variant trace reports kernel "none" (0) and flops 0, as the reference. */
+  int32_t hooking;
+  int32_t reserved;
 } fsv_config;
+
+#define FSV_HOOKING_SET 0x100
+#define FSV_HOOK_GRANDPARENT 1        /* hook gf[v] rather than f[v] */
+#define FSV_HOOK_STOCHASTIC 2         /* f[f[u]] <-min, one commit per iteration */
+#define FSV_HOOK_AGGRESSIVE 4         /* f[u] <-min */
+#define FSV_HOOK_EARLY_TERMINATION 8  /* stop on gf stability (only with all four) */
 
 /* Result summary of the last solve. */
 typedef struct fsv_stats {
@@ -81,7 +93,7 @@ int fsv_create(int device, fsv_ctx** out);
 int fsv_destroy(fsv_ctx* ctx);
 
 /* Hub table size used by the NEXT upload: <0 = no hubs, 0 = auto
- * (top-degree vertices up to 49152 shared-memory slots), >0 = at most that. */
+ * (top-degree vertices up to 55296 shared-memory slots), >0 = at most that. */
 int fsv_set_hub_slots(fsv_ctx* ctx, int slots);
 
 /* Use an external stream (e.g. torch.cuda.current_stream().cuda_stream);

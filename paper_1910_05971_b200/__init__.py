@@ -7,8 +7,9 @@ hand-written sm_100a kernels behind the C ABI of ``include/fastsv.h``.
 """
 
 from .driver import (DriverConfig, HookingConfig, IterationTrace, RunResult, Solver,
-                     choose_kernel, connected_components, default_solver, device_count,
-                     fastsv, fastsv_la, require_device)
+                     ablation_results, ablation_suite, choose_kernel, connected_components,
+                     default_solver, device_count, fastsv, fastsv_la, require_device,
+                     simplified_sv, sv_level_config)
 from .errors import DeviceError, InputError, InvariantError, SvccError, VerificationError
 from .graph import CsrGraph, Labeling, build_csr, labeling_from_parents
 
@@ -18,6 +19,7 @@ __all__ = [
     "CsrGraph", "Labeling", "build_csr", "labeling_from_parents",
     "DriverConfig", "HookingConfig", "IterationTrace", "RunResult", "Solver",
     "choose_kernel", "fastsv_la", "fastsv", "connected_components", "default_solver",
+    "simplified_sv", "sv_level_config", "ablation_results", "ablation_suite",
     "device_count", "require_device",
     "SvccError", "InputError", "VerificationError", "InvariantError", "DeviceError",
     "__version__",

@@ -21,7 +21,8 @@ FSV_OK, FSV_ERR_INPUT, FSV_ERR_CONTRACT, FSV_ERR_INVARIANT, FSV_ERR_RUNTIME = 0,
 
 class FsvConfig(ctypes.Structure):
     _fields_ = [("max_iters", c_int32), ("batch", c_int32), ("profile", c_int32),
-                ("sparse_policy", c_int32), ("sparse_threshold", c_double), ("reserved", c_int32 * 2)]
+                ("sparse_policy", c_int32), ("sparse_threshold", c_double), ("hooking", c_int32),
+                ("reserved", c_int32)]
 
 
 class FsvStats(ctypes.Structure):

@@ -12,6 +12,7 @@
 //   - result marshalling into the reference's RunResult/trace shape.
 #include "../../include/fastsv.h"
 #include "fsv_kernels.cuh"
+#include "fsv_variants.cuh"
 
 #include <cub/cub.cuh>
 #include <cuda/std/functional>
@@ -192,6 +193,12 @@ struct fsv_ctx {
   DBuf<unsigned> partials;
   int* h_done = nullptr;  // pinned
   int64_t* h_off_pin = nullptr;   // pinned host copy of device-built row offsets
+  // hooking variants (fsv_variants.cuh): row ids of the stored entries, two
+  // extra vectors, and where the labels of the last solve live
+  DBuf<int> var_rows, var_t, var_g;
+  bool var_rows_ready = false;
+  bool variant = false;
+  const int* labels_src = nullptr;
   size_t h_off_cap = 0;
   std::vector<cudaEvent_t> events;
   // profile mode: events around every kernel of iteration k: [k][0..7]
@@ -1076,6 +1083,7 @@ static int upload_impl(fsv_ctx* c, int64_t n, const int64_t* h_off, const ColT* 
   }
   c->col_base = e_begin;
   c->csr_local = mloc;
+  c->var_rows_ready = false;
   c->row_begin = row_begin;
   c->row_end = row_end;
 
@@ -1486,6 +1494,112 @@ static int copy_snapshot(fsv_ctx* c, int k, int32_t* dst) {
   return FSV_OK;
 }
 
+// HookingConfig variants and simplified_sv (fsv_variants.cuh): a host-driven
+// loop of init -> hook -> [shortcut] -> commit count per iteration, with the
+// reference's stop rule (gf stability only with all four flags,
+// algorithms.py:103-114; f stability otherwise, :139).
+template <bool STO, bool AGG, bool GP>
+static void launch_var_hook(fsv_ctx* c, const int* F, const int* G, int* N) {
+  const long long m = c->csr_local;
+  if (m)
+    k_var_hook<STO, AGG, GP><<<grid_for(c, m, 256, 16), 256, 0, c->stream>>>(c->var_rows.p, c->csr_cols.p, m, F,
+                                                                              G, N);
+}
+
+static int solve_variant(fsv_ctx* c, const fsv_config& d, int cap, int32_t* snapshots, int32_t snap_cap) {
+  if (c->comm || c->row_begin != 0 || c->row_end != c->n)
+    return fail(FSV_ERR_CONTRACT, "hooking variants run on a single context owning all rows");
+  const int fl = d.hooking & 15;
+  const bool GP = fl & FSV_HOOK_GRANDPARENT, STO = fl & FSV_HOOK_STOCHASTIC, AGG = fl & FSV_HOOK_AGGRESSIVE;
+  const bool gf_stop = (fl & 15) == 15;   // _uses_gf_termination (algorithms.py:103-114)
+  cudaStream_t st = c->stream;
+  const long long n = c->n;
+  c->variant = true;
+  c->launches = 0;
+  c->host_syncs = 0;
+  if (!c->var_rows_ready) {
+    CUDA_TRY(c->var_rows.alloc((size_t)std::max<long long>(c->csr_local, 1)));
+    if (c->csr_local)
+      k_row_ids<<<grid_for(c, n * 32, 256, 16), 256, 0, st>>>(c->csr_off.p, c->col_base, 0, n, c->var_rows.p);
+    c->var_rows_ready = true;
+  }
+  const size_t nv = (size_t)n + 64;
+  CUDA_TRY(c->var_t.alloc(nv));
+  CUDA_TRY(c->var_g.alloc(nv));
+  int* P[5] = {c->X, c->G, c->Y, c->var_t.p, c->var_g.p};   // F, G, N, T, Gn
+  CUDA_TRY(cudaMemsetAsync(c->cnt.p, 0, sizeof(unsigned long long) * NCOUNT * (size_t)cap, st));
+  {
+    int rc = ensure_events(c, 3);   // start + two alternating iteration ends
+    if (rc) return rc;
+  }
+  const int vgrid = grid_for(c, n, 256, 8);
+  CUDA_TRY(cudaEventRecord(c->events[0], st));
+  if (n) k_var_iota<<<vgrid, 256, 0, st>>>(P[0], P[1], n);
+  int k = 0;
+  bool stopped = false;
+  std::vector<float> ms;
+  unsigned long long h[NCOUNT];
+  cudaEvent_t prev = c->events[0];
+  while (k < cap) {
+    ++k;
+    int* F = P[0];
+    int* G = P[1];
+    int* N = P[2];
+    unsigned long long* cnt = c->cnt.p + (size_t)(k - 1) * NCOUNT;
+    if (n) {
+      k_var_init<<<vgrid, 256, 0, st>>>(F, G, N, n, STO);
+      switch ((STO ? 4 : 0) | (AGG ? 2 : 0) | (GP ? 1 : 0)) {
+        case 0: launch_var_hook<false, false, false>(c, F, G, N); break;
+        case 1: launch_var_hook<false, false, true>(c, F, G, N); break;
+        case 2: launch_var_hook<false, true, false>(c, F, G, N); break;
+        case 3: launch_var_hook<false, true, true>(c, F, G, N); break;
+        case 4: launch_var_hook<true, false, false>(c, F, G, N); break;
+        case 5: launch_var_hook<true, false, true>(c, F, G, N); break;
+        case 6: launch_var_hook<true, true, false>(c, F, G, N); break;
+        default: launch_var_hook<true, true, true>(c, F, G, N); break;
+      }
+      if (!STO) k_var_shortcut<<<vgrid, 256, 0, st>>>(N, P[3], n);
+      k_var_count<<<vgrid, 256, 0, st>>>(STO ? N : P[3], F, G, P[4], n, cnt);
+      c->launches += STO ? 3 : 4;
+    }
+    cudaEvent_t ev = c->events[1 + (k & 1)];
+    CUDA_TRY(cudaEventRecord(ev, st));
+    CUDA_TRY(cudaMemcpyAsync(h, cnt, sizeof h, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    ++c->host_syncs;
+    float t = 0.f;
+    cudaEventElapsedTime(&t, prev, ev);
+    ms.push_back(t);
+    prev = ev;
+    // commit: the new parents become F, their grandparents G
+    int* Pn = STO ? P[2] : P[3];
+    int* newP[5] = {Pn, P[4], STO ? P[3] : P[2], P[0], P[1]};
+    for (int i = 0; i < 5; ++i) P[i] = newP[i];
+    if (snapshots) {
+      if (k > snap_cap) return fail(FSV_ERR_CONTRACT, "more than %d iterations ran", snap_cap);
+      if (n) CUDA_TRY(cudaMemcpyAsync(snapshots + (size_t)(k - 1) * n, P[0], sizeof(int) * n,
+                                      cudaMemcpyDeviceToHost, st));
+    }
+    if (h[C_VIOL]) return fail(FSV_ERR_INVARIANT, "parent vector increased during hooking");
+    if ((gf_stop ? h[C_GF] : h[C_F]) == 0) { stopped = true; break; }
+  }
+  CUDA_TRY(cudaStreamSynchronize(st));
+  if (!stopped) return fail(FSV_ERR_RUNTIME, "did not converge within %d iterations", cap);
+  c->iterations = k;
+  c->h_cnt.assign((size_t)k * NCOUNT, 0ull);
+  CUDA_TRY(cudaMemcpy(c->h_cnt.data(), c->cnt.p, sizeof(unsigned long long) * k * NCOUNT, cudaMemcpyDeviceToHost));
+  c->h_mode.assign((size_t)k + 1, 0);
+  c->iter_ms = ms;
+  c->solve_ms = 0.f;
+  for (float x : ms) c->solve_ms += x;
+  c->components = (int)c->h_cnt[(size_t)(k - 1) * NCOUNT + C_ROOTS];
+  c->labels_src = P[0];
+  c->labels_ready = 1;
+  if (c->h_cnt[(size_t)(k - 1) * NCOUNT + C_NONSTAR])
+    return fail(FSV_ERR_INVARIANT, "algorithm terminated on non-star forest");
+  return FSV_OK;
+}
+
 static int solve_impl(fsv_ctx* c, const fsv_config* cfg, int32_t* snapshots, int32_t snap_cap) {
   if (!c) return fail(FSV_ERR_CONTRACT, "NULL context");
   if (!c->ready) return fail(FSV_ERR_CONTRACT, "no graph uploaded");
@@ -1511,6 +1625,13 @@ static int solve_impl(fsv_ctx* c, const fsv_config* cfg, int32_t* snapshots, int
   c->threshold = d.sparse_policy == 3 ? d.sparse_threshold : 0.1;
   c->hook_ms = c->hubfix_ms = c->shortcut_ms = c->first_ms = c->allreduce_ms = c->push_ms = 0.f;
   c->hook_launches = 0;
+  if (d.hooking) {
+    if ((d.hooking & ~(FSV_HOOKING_SET | 15)) || !(d.hooking & FSV_HOOKING_SET))
+      return fail(FSV_ERR_CONTRACT, "hooking must be 0 or FSV_HOOKING_SET | flag bits, got 0x%x", d.hooking);
+    return solve_variant(c, d, cap, snapshots, snap_cap);
+  }
+  c->variant = false;
+  c->labels_src = c->G;
   if (c->profile && (rc = ensure_pevents(c, 2 * kPev))) return rc;
 
   // graph mode: the whole iteration loop is one conditional-WHILE graph launch
@@ -1683,7 +1804,8 @@ extern "C" int fsv_get_labels(fsv_ctx* c, int32_t* labels) {
   if (!c->n) return FSV_OK;
   if (!labels) return fail(FSV_ERR_CONTRACT, "labels is NULL");
   CUDA_TRY(cudaSetDevice(c->device));
-  CUDA_TRY(cudaMemcpyAsync(labels, c->G, sizeof(int) * c->n, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(cudaMemcpyAsync(labels, c->labels_src ? c->labels_src : c->G, sizeof(int) * c->n,
+                           cudaMemcpyDeviceToHost, c->stream));
   CUDA_TRY(cudaStreamSynchronize(c->stream));
   return FSV_OK;
 }
@@ -1716,7 +1838,11 @@ extern "C" int fsv_get_trace_ex(fsv_ctx* c, int64_t* gfc, int64_t* fc, float* ms
   const int k = std::min(cap, c->iterations);
   for (int i = 0; i < k; ++i) {
     const int md = (i + 1 < (int)c->h_mode.size()) ? c->h_mode[(size_t)i + 1] : 0;
-    if (kernel) kernel[i] = md;
+    if (kernel) kernel[i] = c->variant ? 2 : md;   // 2: "none" (vertex-level fastsv trace)
+    if (c->variant) {
+      if (flops) flops[i] = 0;
+      continue;
+    }
     if (flops) {
       // dense product: m_dir (kernels.py:67-68); sparse: pushed degree sum
       // (kernels.py:94,102); iteration 1 sparse pushes the whole vector = m_dir

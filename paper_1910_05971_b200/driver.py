@@ -67,9 +67,10 @@ def choose_kernel(gf_changed: int, n: int, cfg: DriverConfig) -> str:
 
 @dataclass(frozen=True)
 class HookingConfig:
-    """svcc.HookingConfig (algorithms.py:28-35). The device path implements
-    the all-flags configuration (FastSV proper); weaker flag sets are the
-    ablation study, not the hot path."""
+    """svcc.HookingConfig (algorithms.py:28-35). All flags (FastSV proper)
+    runs on the optimised path; weaker flag sets (the sv1..sv4 ablation,
+    SURVEY §8f-3) run on the generic variant kernels with the same results
+    as the reference."""
 
     grandparent_hooking: bool = True
     stochastic_hooking: bool = True
@@ -220,8 +221,9 @@ class Solver:
     # -- solve ------------------------------------------------------------
     @staticmethod
     def _config(batch: int = 0, max_iters: int = 0, profile: bool = False,
-                policy: int = 0, threshold: float = 0.1) -> FsvConfig:
+                policy: int = 0, threshold: float = 0.1, hooking: int = 0) -> FsvConfig:
         cfg = FsvConfig()
+        cfg.hooking = int(hooking)
         cfg.batch = int(batch)
         cfg.max_iters = int(max_iters)
         cfg.profile = int(bool(profile))
@@ -230,12 +232,14 @@ class Solver:
         return cfg
 
     def solve(self, batch: int = 0, max_iters: int = 0, profile: bool = False,
-              policy: int = 0, threshold: float = 0.1) -> FsvStats:
+              policy: int = 0, threshold: float = 0.1, hooking: int = 0) -> FsvStats:
         """Run to convergence; labels stay on the device. ``profile`` brackets
         every kernel with CUDA events (per-kernel *_ms in the stats).
         ``policy``: 0 reference default (auto, 0.1), 1 dense only, 2 sparse
-        only, 3 auto with ``threshold`` (svcc.choose_kernel)."""
-        cfg = self._config(batch, max_iters, profile, policy, threshold)
+        only, 3 auto with ``threshold`` (svcc.choose_kernel). ``hooking``: 0
+        all-flags FastSV, else HOOKING_SET | flag bits (a HookingConfig
+        variant; HOOKING_SET alone is simplified_sv)."""
+        cfg = self._config(batch, max_iters, profile, policy, threshold, hooking)
         _check(self._lib.fsv_solve(self._ctx, ctypes.byref(cfg), ctypes.byref(self.stats)))
         return self.stats
 
@@ -264,10 +268,10 @@ class Solver:
         return gfc[:k], fc[:k], ms[:k]
 
     def run(self, batch: int = 0, max_iters: int = 0, snapshots: bool = False, snap_cap: int = 256,
-            policy: int = 0, threshold: float = 0.1, full_trace: bool = False):
+            policy: int = 0, threshold: float = 0.1, full_trace: bool = False, hooking: int = 0):
         """Solve + copy out: (labels int32, iterations, gf_changed, f_changed,
         per-iteration ms, snapshots or None[, kernel, flops])."""
-        cfg = self._config(batch, max_iters, False, policy, threshold)
+        cfg = self._config(batch, max_iters, False, policy, threshold, hooking)
         n = self.n
         labels = np.empty(n, dtype=np.int32)
         iters = ctypes.c_int32(0)
@@ -304,11 +308,24 @@ def default_solver(device: int = 0) -> Solver:
 
 
 _POLICY = {"auto": 3, "dense_only": 1, "sparse_only": 2}
+_KIND = {0: "dense", 1: "sparse", 2: "none"}
+
+# fsv_config.hooking (include/fastsv.h)
+HOOKING_SET = 0x100
+HOOK_GRANDPARENT, HOOK_STOCHASTIC, HOOK_AGGRESSIVE, HOOK_EARLY_TERMINATION = 1, 2, 4, 8
+
+
+def hooking_code(cfg: "HookingConfig") -> int:
+    """fsv_config.hooking for a HookingConfig variant (algorithms.py:28-35)."""
+    return (HOOKING_SET | (HOOK_GRANDPARENT if cfg.grandparent_hooking else 0)
+            | (HOOK_STOCHASTIC if cfg.stochastic_hooking else 0)
+            | (HOOK_AGGRESSIVE if cfg.aggressive_hooking else 0)
+            | (HOOK_EARLY_TERMINATION if cfg.early_termination else 0))
 
 
 def _result(g, labels, iters, gfc, fc, ms, snaps, kern, flops) -> RunResult:
     trace = [IterationTrace(iteration=i + 1, gf_changed=int(gfc[i]), f_changed=int(fc[i]),
-                            kernel="sparse" if kern[i] == 1 else "dense",
+                            kernel=_KIND.get(int(kern[i]), "dense"),
                             elapsed=float(ms[i]) / 1e3, flops=int(flops[i]))
              for i in range(iters)]
     snapshots = None
@@ -323,12 +340,12 @@ def _result(g, labels, iters, gfc, fc, ms, snaps, kern, flops) -> RunResult:
 
 
 def _solve_graph(g, record_snapshots: bool, batch: int, device: int, policy: int = 0,
-                 threshold: float = 0.1) -> RunResult:
+                 threshold: float = 0.1, hooking: int = 0) -> RunResult:
     solver = default_solver(device)
     solver.upload(g)
     labels, iters, gfc, fc, ms, snaps, kern, flops = solver.run(
         batch=batch, snapshots=record_snapshots, snap_cap=max(64, 4 * int(np.log2(max(g.n, 2))) + 16),
-        policy=policy, threshold=threshold, full_trace=True)
+        policy=policy, threshold=threshold, full_trace=True, hooking=hooking)
     return _result(g, labels, iters, gfc, fc, ms, snaps, kern, flops)
 
 
@@ -348,14 +365,47 @@ def fastsv(g, cfg: HookingConfig | None = None, record_snapshots: bool = False,
     """All-flags FastSV (algorithms.py:152-167) on a B200; identical results
     to fastsv_la (the reference proves this, test_acceptance.py:207-218)."""
     cfg = cfg or HookingConfig()
-    if cfg != HookingConfig():
-        raise NotImplementedError(
-            "the B200 path implements all-flags FastSV; weaker HookingConfig variants "
-            "(the sv1..sv4 ablation) are not on the hot path")
+    if hooking_code(cfg) != HOOKING_SET | 15:
+        # weaker variants (the sv1..sv4 ablation) run on the generic variant
+        # kernels (csrc/fsv_variants.cuh), same results as algorithms.py:79-114
+        return _solve_graph(g, record_snapshots, 0, device, hooking=hooking_code(cfg))
     res = _solve_graph(g, record_snapshots, 0, device)
     for i, t in enumerate(res.trace):
         res.trace[i] = IterationTrace(t.iteration, t.gf_changed, t.f_changed, "none", t.elapsed, 0)
     return res
+
+
+def simplified_sv(g, record_snapshots: bool = False, device: int = 0) -> RunResult:
+    """Baseline SV (algorithms.py:66-76,145-149): guarded tree hooking onto
+    parents plus shortcutting, two commits per iteration, until f is stable."""
+    return _solve_graph(g, record_snapshots, 0, device, hooking=HOOKING_SET)
+
+
+def sv_level_config(level: int) -> "HookingConfig":
+    """Cumulative ablation configurations sv1..sv5 (algorithms.py:170-181)."""
+    if level not in (1, 2, 3, 4, 5):
+        raise ValueError(f"sv level must be 1..5, got {level}")
+    return HookingConfig(grandparent_hooking=level >= 2, stochastic_hooking=level >= 3,
+                         aggressive_hooking=level >= 4, early_termination=level >= 5)
+
+
+def ablation_results(g, device: int = 0):
+    """sv1 (simplified_sv) and sv2..sv5 (fastsv under sv_level_config), all
+    on the device; insists the five labelings agree (algorithms.py:184-199)."""
+    from .errors import InvariantError
+    runs = [("sv1", simplified_sv(g, device=device))]
+    for level in (2, 3, 4, 5):
+        runs.append((f"sv{level}", fastsv(g, sv_level_config(level), device=device)))
+    base = runs[0][1].labeling.labels
+    for name, result in runs[1:]:
+        if not np.array_equal(result.labeling.labels, base):
+            raise InvariantError(f"ablation configuration {name} disagrees with sv1 labels")
+    return runs
+
+
+def ablation_suite(g, device: int = 0):
+    """(config_name, iterations) for sv1..sv5 (algorithms.py:202-204)."""
+    return [(name, result.iterations) for name, result in ablation_results(g, device)]
 
 
 def edge_pairs(edges) -> np.ndarray:

@@ -68,3 +68,29 @@ def csr_digest(row_offsets, col_indices) -> str:
 
 def load_csr_digests():
     return json.loads((GOLDEN / "csr_digests.json").read_text())
+
+
+def load_variants():
+    """Reference traces of the hooking variants: list of (graph name, code,
+    iterations, gf_changed, f_changed, snapshot digest) and the pair-stream
+    digests of the generated extra graphs."""
+    d = np.load(GOLDEN / "variants.npz", allow_pickle=False)
+    runs = []
+    for i in range(len(d["names"])):
+        a, b = d["trace_off"][i], d["trace_off"][i + 1]
+        runs.append((str(d["names"][i]), int(d["codes"][i]), int(d["iterations"][i]),
+                     d["gf_changed"][a:b].tolist(), d["f_changed"][a:b].tolist(), str(d["digests"][i])))
+    extra = dict(zip([str(x) for x in d["extra_names"]], [str(x) for x in d["extra_digests"]]))
+    return runs, extra
+
+
+def variant_graphs():
+    """{name: (n, pairs)} for every graph of the variant goldens (the suite
+    plus the generated extras, regenerated from the same seeded streams)."""
+    from paper_1910_05971_b200 import generators as gen
+    out = {c.name: (c.n, c.edges) for c in load_suite()}
+    out["x:config1"] = gen.baseline_graph(1)
+    out["x:rmat14"] = gen.rmat(14, 16, seed=5)
+    out["x:grid300"] = gen.grid(300, 300, 0.4, seed=3)
+    out["x:forest2000"] = gen.forest(2000, 1, 64, 2, seed=4)
+    return out

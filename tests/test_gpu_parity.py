@@ -352,3 +352,54 @@ def test_device_csr_build_row_ranges():
             assert np.array_equal(g.col_indices, h.col_indices[h.row_offsets[lo]:h.row_offsets[hi]])
             sizes.append(int(s.solve().oriented_entries))
     assert sum(sizes) == h.m // 2
+
+
+# ---- hooking variants and simplified_sv (fsv_config.hooking) ----------------
+
+def _snap_digest(snaps):
+    import hashlib
+    h = hashlib.sha256()
+    for s in snaps:
+        h.update(np.ascontiguousarray(s, dtype="<i8").tobytes())
+    return h.hexdigest()[:16]
+
+
+def test_hooking_variants_match_reference_traces(solver):
+    """Every HookingConfig (16 flag sets) and simplified_sv on every golden
+    graph: iteration count, gf_changed/f_changed traces and every committed
+    parent vector (snapshot digest) equal the reference's own runs."""
+    from golden_io import load_variants, variant_graphs
+    from paper_1910_05971_b200.driver import HOOKING_SET
+    runs, extra = load_variants()
+    graphs = variant_graphs()
+    for name, digest in extra.items():
+        assert gen.pairs_digest(graphs[name][1]) == digest, name
+    solver.set_hub_slots(0)
+    current = None
+    for name, code, iters, gfc, fc, digest in runs:
+        if name != current:
+            n, e = graphs[name]
+            solver.upload(fb.build_csr(n, e))
+            current = name
+        hooking = HOOKING_SET if code == 16 else HOOKING_SET | code
+        labels, k, g2, f2, ms, snaps, kern, flops = solver.run(snapshots=True, snap_cap=64, hooking=hooking,
+                                                               full_trace=True)
+        assert (k, g2.tolist(), f2.tolist()) == (iters, gfc, fc), (name, code)
+        assert _snap_digest(snaps) == digest, (name, code)
+        assert all(x == 2 for x in kern) and all(x == 0 for x in flops)
+
+
+def test_public_variant_api():
+    """fastsv(g, HookingConfig(...)), simplified_sv and the sv1..sv5 ablation
+    through the public API: RunResult shape of the reference."""
+    n, e = gen.rmat(11, 8, seed=41)
+    g = fb.build_csr(n, e)
+    uf = oracle.uf_labels(n, e).astype(np.int64)
+    r = fb.simplified_sv(g, record_snapshots=True)
+    assert np.array_equal(r.labeling.labels, uf) and len(r.snapshots) == r.iterations
+    assert all(t.kernel == "none" and t.flops == 0 for t in r.trace)
+    r3 = fb.fastsv(g, fb.sv_level_config(3))
+    assert np.array_equal(r3.labeling.labels, uf)
+    suite = fb.ablation_suite(g)
+    assert [s[0] for s in suite] == ["sv1", "sv2", "sv3", "sv4", "sv5"]
+    assert suite[4][1] == fb.fastsv(g).iterations
