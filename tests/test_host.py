@@ -70,10 +70,24 @@ def test_driver_config_and_choose_kernel():
             fb.DriverConfig(**bad)
 
 
-def test_weaker_hooking_configs_are_refused_not_faked():
+def test_hooking_variant_codes():
+    """HookingConfig -> fsv_config.hooking (include/fastsv.h) and the sv1..sv5
+    ladder of algorithms.py:170-181."""
+    from paper_1910_05971_b200.driver import HOOKING_SET, hooking_code
+    assert [hooking_code(fb.sv_level_config(k)) for k in range(1, 6)] == \
+        [HOOKING_SET, HOOKING_SET | 1, HOOKING_SET | 3, HOOKING_SET | 7, HOOKING_SET | 15]
+    assert hooking_code(fb.HookingConfig()) == HOOKING_SET | 15
+    with pytest.raises(ValueError, match="sv level must be 1..5"):
+        fb.sv_level_config(0)
+
+
+@pytest.mark.skipif(fb.device_count() > 0, reason="checks the no-GPU behaviour")
+def test_variants_fail_loudly_without_a_gpu():
     g = fb.build_csr(3, [(0, 1)])
-    with pytest.raises(NotImplementedError):
+    with pytest.raises(fb.DeviceError):
         fb.fastsv(g, fb.HookingConfig(stochastic_hooking=False))
+    with pytest.raises(fb.DeviceError):
+        fb.simplified_sv(g)
 
 
 def test_status_mapping():
