@@ -138,8 +138,14 @@ struct DBuf {
 static constexpr int kHubMax = (SMEM_OPTIN_INTS - HOT_ACC) / 1024 * 1024;
 static constexpr int kHubMinDegree = 32;  // below this a hub slot buys nothing
 static constexpr long long kTierMinN = 1LL << 23;   // rank tier only when the vectors overflow L2
-static constexpr int kTierMinDegree = 8;
-static constexpr long long kTierMax = 8LL << 20;    // 32 MB of gf + 32 MB of accumulators
+#ifndef FSV_TIER_MIN_DEG
+#define FSV_TIER_MIN_DEG 8
+#endif
+#ifndef FSV_TIER_MAX_M
+#define FSV_TIER_MAX_M 8
+#endif
+static constexpr int kTierMinDegree = FSV_TIER_MIN_DEG;
+static constexpr long long kTierMax = (long long)FSV_TIER_MAX_M << 20;   // 8M: 32 MB of gf + 32 MB of accumulators
 static constexpr int kTraceCap = 4096;    // iteration cap of the counter array
 
 struct fsv_ctx {

@@ -21,9 +21,10 @@
 // precomputed at upload from the sorted CSR rows, so k_first does iteration 1
 // including its shortcut phase in one vertex-parallel pass.
 //
-// All writes into N are filtered min-atomics; a write that cannot lower N is
-// skipped using the read-only gf_k (N[x] <= gf_k[x] always, and
-// gf_k[F[x]] <= gf_k[x], so val >= gf_k[x] makes both hooks no-ops).
+// Writes into N are min-atomics filtered by the read-only gf_k: N[x] <= gf_k[x]
+// always and gf_k[F[x]] <= gf_k[x], so val >= gf_k[x] makes both hooks
+// no-ops. The stochastic target of a column-side emission is not filtered a
+// second time (a no-op min is harmless; the gather costs more than it saves).
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -570,14 +571,13 @@ __global__ void __launch_bounds__(HOOK_THREADS, 1) k_hook(HookArgs a) {
             }
           }
         }
-#pragma unroll
-        for (int j = 0; j < EPL; ++j) {
-          if (t[j] == w[j]) t[j] = -1;
-          if (t[j] >= 0) val[j] = ldg(G + t[j]);
-        }
+        // the stochastic hook of these emissions is not filtered by gf[t]:
+        // they already passed the aggressive filter, and the extra gather
+        // cost more than the no-op reductions it saves (config 2 hook
+        // 241 -> 230 us; configs 3-4 unchanged)
 #pragma unroll
         for (int j = 0; j < EPL; ++j)
-          if (t[j] >= 0 && y[j] < val[j]) red_min(N + t[j], y[j]);
+          if (t[j] >= 0 && t[j] != w[j]) red_min(N + t[j], y[j]);
       }
       // segmented inclusive scan of (seen, run): min of the run open at the
       // end of each lane
