@@ -1431,7 +1431,7 @@ static int launch_iteration(fsv_ctx* c, int k, int max_iter, bool graph = false)
   }
   if (c->HT) {
     pmark(c, k, 2);
-    k_hubfix<<<grid_for(c, c->HT, 256), 256, 0, st>>>(c->hacc, c->hub_id.p, c->HT, F, c->G, N,
+    k_hubfix<<<grid_for(c, c->HT, 256), 256, 0, st>>>(c->hacc, c->hub_id.p, c->G_hub.p, c->HT, F, c->G, N,
                                                        c->done.p, c->mode.p, k,
                                                        graph ? c->iterbuf.p : nullptr);
     pmark(c, k, 3);

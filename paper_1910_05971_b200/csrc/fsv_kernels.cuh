@@ -618,9 +618,12 @@ __global__ void __launch_bounds__(HOOK_THREADS, 1) k_hook(HookArgs a) {
 
 // ---- hub accumulator -> N ---------------------------------------------------
 
-__global__ void k_hubfix(int* __restrict__ hub_acc, const int* __restrict__ hub_id, int H,
-                         const int* __restrict__ F, const int* __restrict__ G, int* __restrict__ N,
-                         const int* done, const int* mode, int iter, const int* iterp) {
+// gf of slot s is G_hub[s] (compact, refreshed by the vertex pass), not a
+// random gather of G[hub_id[s]].
+__global__ void k_hubfix(int* __restrict__ hub_acc, const int* __restrict__ hub_id,
+                         const int* __restrict__ G_hub, int H, const int* __restrict__ F,
+                         const int* __restrict__ G, int* __restrict__ N, const int* done, const int* mode,
+                         int iter, const int* iterp) {
   if (*(volatile const int*)done) return;
   if (iterp) iter = *(volatile const int*)iterp;
   if (mode[iter] != 0) return;
@@ -629,7 +632,7 @@ __global__ void k_hubfix(int* __restrict__ hub_acc, const int* __restrict__ hub_
     if (acc == INF) continue;
     hub_acc[s] = INF;
     const int h = ldg(hub_id + s);
-    emit_row(h, ldg(G + h), acc, F, G, N);
+    emit_row(h, ldg(G_hub + s), acc, F, G, N);
   }
 }
 
