@@ -189,7 +189,7 @@ struct fsv_ctx {
   long long rcap = 0;
   int dgrid = 1;
   // solve state
-  DBuf<int> xb, yb, gb, G_hub, hub_acc, done;   // xb/yb: parent buffers, gb: gf
+  DBuf<int> xb, gb, G_hub, hub_acc, done;   // xb and f1: parent buffers, gb: gf
   int* hacc = nullptr;   // hub accumulator start inside hub_acc
   int* X = nullptr;
   int* Y = nullptr;
@@ -1095,8 +1095,9 @@ static int upload_impl(fsv_ctx* c, int64_t n, const int64_t* h_off, const ColT* 
 
   // solve buffers: n + dummy vertex, padded for 16-byte vector access
   const size_t nv = ((size_t)n + 1 + 63) / 64 * 64;
-  CUDA_TRY(c->xb.alloc(nv)); CUDA_TRY(c->yb.alloc(nv)); CUDA_TRY(c->gb.alloc(nv));
-  c->X = c->xb.p; c->Y = c->yb.p; c->G = c->gb.p;
+  // Y (f_k of even k) is f1's buffer: k_first leaves f_1 there without a copy
+  CUDA_TRY(c->xb.alloc(nv)); CUDA_TRY(c->gb.alloc(nv));
+  c->X = c->xb.p; c->Y = c->f1.p; c->G = c->gb.p;
   CUDA_TRY(c->G_hub.alloc(std::max(HT, 4))); {
     long long hpad = 0;   // dev: FSV_HPAD shifts the hub accumulator (placement checks)
     if (const char* e = getenv("FSV_HPAD")) hpad = atoll(e);
@@ -1667,7 +1668,7 @@ static int solve_impl(fsv_ctx* c, const fsv_config* cfg, int32_t* snapshots, int
   }
   {
     FirstArgs fa;
-    fa.f1 = c->f1.p; fa.Y = c->Y; fa.G = c->G; fa.X = c->X; fa.n = c->n;
+    fa.f1 = c->f1.p; fa.G = c->G; fa.X = c->X; fa.n = c->n;
     fa.hub_id = c->hub_id.p; fa.G_hub = c->G_hub.p; fa.H = c->HT; fa.cnt = c->cnt.p;
     fa.partials = c->partials.p; fa.ticket = c->ticket.p; fa.done = c->done.p; fa.max_iter = cap;
     fa.dl = delta_out(c);

@@ -811,11 +811,11 @@ __global__ void __launch_bounds__(SC_THREADS) k_shortcut(ShortcutArgs a) {
 }
 
 // ---- iteration 1 in closed form ---------------------------------------------
-// f_1[u] = min(u, min neighbour) = f1[u]; gf_1 = f1[f1]. Writes Y = f_1,
-// G = gf_1 and X = gf_1 (the N init of iteration 2).
+// f_1[u] = min(u, min neighbour) = f1[u]; gf_1 = f1[f1]. f_1 stays in f1's
+// buffer (it is the Y parent buffer); writes G = gf_1 and X = gf_1 (the N
+// init of iteration 2).
 struct FirstArgs {
   const int* f1;
-  int* Y;
   int* G;
   int* X;
   long long n;
@@ -855,7 +855,6 @@ __global__ void __launch_bounds__(SC_THREADS) k_first(FirstArgs a) {
       c[C_NONSTAR] += (gg.x != f.x) + (gg.y != f.y) + (gg.z != f.z) + (gg.w != f.w);
       c[C_ROOTS] += (f.x == u) + (f.y == u + 1) + (f.z == u + 2) + (f.w == u + 3);
       c[C_VIOL] += (f.x > u) + (f.y > u + 1) + (f.z > u + 2) + (f.w > u + 3);
-      reinterpret_cast<int4*>(a.Y)[i] = f;
       reinterpret_cast<int4*>(a.G)[i] = gg;
       reinterpret_cast<int4*>(a.X)[i] = gg;
       m4 = (gg.x != u) | ((gg.y != u + 1) << 1) | ((gg.z != u + 2) << 2) | ((gg.w != u + 3) << 3);
@@ -868,7 +867,7 @@ __global__ void __launch_bounds__(SC_THREADS) k_first(FirstArgs a) {
       const int gg = ldg(f1 + f);
       c[C_GF] += gg != (int)u; c[C_F] += f != (int)u; c[C_NONSTAR] += gg != f;
       c[C_ROOTS] += f == (int)u; c[C_VIOL] += f > (int)u;
-      a.Y[u] = f; a.G[u] = gg; a.X[u] = gg;
+      a.G[u] = gg; a.X[u] = gg;
       return gg != (int)u;
     }, region, wo);
   if (lane == 0) a.dl.count[gwarp] = wo;
