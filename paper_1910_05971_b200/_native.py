@@ -9,11 +9,13 @@ present, the solver entry points raise. Build with
 from __future__ import annotations
 
 import ctypes
+import os
 from ctypes import POINTER, c_char_p, c_double, c_float, c_int, c_int32, c_int64, c_uint64, c_void_p
 from pathlib import Path
 
 _PKG = Path(__file__).resolve().parent
-LIB_FASTSV_PATH = _PKG / "libfastsv.so"
+# FSV_LIB: dev override (a kernel-shape variant built by tools/variants.sh)
+LIB_FASTSV_PATH = Path(os.environ["FSV_LIB"]).resolve() if os.environ.get("FSV_LIB") else _PKG / "libfastsv.so"
 LIB_GRAPHGEN_PATH = _PKG / "libfsv_graphgen.so"
 
 FSV_OK, FSV_ERR_INPUT, FSV_ERR_CONTRACT, FSV_ERR_INVARIANT, FSV_ERR_RUNTIME = 0, 1, 2, 3, 4

@@ -31,7 +31,7 @@ NVCC = shutil.which("nvcc") or os.path.join(CUDA_HOME, "bin", "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 CUDA_SOURCES = ["fastsv.cu"]
-CUDA_HEADERS = ["fsv_kernels.cuh", "philox.h"]
+CUDA_HEADERS = ["fsv_kernels.cuh", "fsv_variants.cuh", "philox.h"]
 
 
 def _stale(target: Path, deps) -> bool:

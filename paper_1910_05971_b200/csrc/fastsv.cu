@@ -169,9 +169,7 @@ struct fsv_ctx {
   int64_t csr_local = 0;   // entries of this rank's rows in csr_cols
   // changed-gf lists of the vertex pass (one region per warp)
   DBuf<int> dlist, dcount, mode;
-  DBuf<int2> chunks;
-  DBuf<PushDesc> pdesc;
-  DBuf<long long> pbtotal;
+  DBuf<PushChunk> chunks;   // long-row chunks of a sparse iteration
   // upload workspace (grow-only, reused across uploads)
   struct {
     DBuf<unsigned long long> bad;
@@ -1118,10 +1116,8 @@ static int upload_impl(fsv_ctx* c, int64_t n, const int64_t* h_off, const ColT* 
     CUDA_TRY(c->mode.alloc((size_t)kTraceCap + 2));
     CUDA_TRY(c->iterbuf.alloc(4));
     CUDA_TRY(c->tstamp.alloc((size_t)kTraceCap + 2));
-    const long long max_batches = n / 32 + warps + 2;
-    CUDA_TRY(c->pdesc.alloc((size_t)(max_batches * 32)));
-    CUDA_TRY(c->pbtotal.alloc((size_t)max_batches));
-    CUDA_TRY(c->chunks.alloc((size_t)(mloc / PUSH_CHUNK + max_batches + 64)));
+    // rows longer than PUSH_BIG: sum of ceil(deg / PUSH_CHUNK) <= 2 * mloc / PUSH_CHUNK + 1
+    CUDA_TRY(c->chunks.alloc((size_t)(2 * (mloc / PUSH_CHUNK) + 64)));
   }
   CUDA_TRY(c->cnt.alloc((size_t)kTraceCap * NCOUNT));
   umark(6);
@@ -1413,9 +1409,8 @@ static int launch_iteration(fsv_ctx* c, int k, int max_iter, bool graph = false)
     p.row_begin = (int)c->row_begin; p.row_end = (int)c->row_end;
     p.F = F; p.G = c->G; p.N = N; p.mode = c->mode.p; p.iter = k;
     unsigned long long* slot = c->cnt.p + (size_t)(k - 1) * NCOUNT;
-    p.flops = slot + C_FLOPS; p.nchunks = slot + C_CHUNKS; p.nbatches = slot + C_BATCHES;
+    p.flops = slot + C_FLOPS; p.nchunks = slot + C_CHUNKS;
     p.barrier = reinterpret_cast<unsigned*>(slot + C_BARRIER); p.chunks = c->chunks.p;
-    p.desc = c->pdesc.p; p.btotal = c->pbtotal.p;
     a.lc = lc;
     // persistent, one CTA per SM; cooperative launch guarantees co-residency
     // for the grid barrier of the sparse (push) path

@@ -71,11 +71,18 @@ constexpr int PUSH_SCRATCH_BYTES = HOOK_THREADS * 20;  // s_start, s_excl (8 B) 
 #define FSV_HOT_ACC 2048
 #endif
 constexpr int HOT_ACC = FSV_HOT_ACC;
+// Steps in which no lane has more than FSV_REC entries that differ from their
+// row's gf take the record path of k_hook (per-entry emissions, no scan);
+// 0 disables it. At most 2 records are held in registers.
+#ifndef FSV_REC
+#define FSV_REC 2
+#endif
+static_assert(FSV_REC >= 0 && FSV_REC <= 2, "FSV_REC must be 0, 1 or 2");
 constexpr int SMEM_OPTIN_INTS = 232448 / 4;   // 227 KB opt-in dynamic shared memory per CTA
 constexpr int SC_THREADS = 512;
 constexpr int NCOUNT = 16;               // counter slots per iteration
 enum { C_GF = 0, C_F = 1, C_NONSTAR = 2, C_ROOTS = 3, C_VIOL = 4,   // vertex-pass counters
-       C_FLOPS = 5, C_CHUNKS = 6, C_BATCHES = 7, C_BARRIER = 8 };     // push bookkeeping
+       C_FLOPS = 5, C_CHUNKS = 6, C_BARRIER = 8 };     // push bookkeeping
 
 // ---- memory helpers -------------------------------------------------------
 
@@ -136,15 +143,16 @@ __device__ __forceinline__ bool converged_exit(const int* done, const LoopCtl& l
   return false;
 }
 
-// Sparse iteration (push). Phase 1 turns the delta list into batches of 32
-// vertices (descriptor per vertex: row start, exclusive prefix of degrees
-// within the batch, gf) and cuts each batch's flattened entry range into
-// PUSH_CHUNK-entry chunks; phase 2 (after a grid barrier) processes chunks.
-struct PushDesc {
-  long long start;   // first column index of the row (rank-local)
-  long long excl;    // entries of the batch before this vertex
+// Sparse iteration (push). Phase A: one warp per delta region takes the
+// changed vertices 32 at a time; rows of at most PUSH_BIG entries are pushed
+// by that warp right away (the batch's rows flattened, 8 entries per lane per
+// pass), longer rows are cut into PUSH_CHUNK-entry chunks appended to a
+// global list. Phase B (after a grid barrier) pushes the chunks, one warp per
+// chunk, so a high-degree vertex is spread over the whole GPU.
+struct PushChunk {
+  long long pos;     // first column index of the chunk (rank-local)
+  int cnt;           // entries in the chunk (<= PUSH_CHUNK)
   int val;           // gf[v] pushed to every neighbour
-  int pad;
 };
 
 struct PushArgs {
@@ -162,11 +170,8 @@ struct PushArgs {
   const int* mode;        // mode[iter]
   int iter;
   unsigned long long* flops;    // this iteration's pushed-entry count
-  unsigned long long* nchunks;  // chunk list length
-  unsigned long long* nbatches; // batch count
-  PushDesc* desc;               // [batch][32]
-  long long* btotal;            // entries per batch
-  int2* chunks;                 // (batch, first flattened entry)
+  unsigned long long* nchunks;  // long-row chunk list length
+  PushChunk* chunks;            // long-row chunks
   unsigned* barrier;            // grid barrier counter of this iteration
 };
 
@@ -233,6 +238,23 @@ __device__ __forceinline__ void emit_row(int u, int gu, int val, const int* __re
   }
 }
 
+// Row emission inside k_hook, with the parent t = F[u] already loaded (or
+// loaded here when t < 0). The stochastic target is filtered by gf[t] only
+// with FSV_ROW_FILTER: the filter is a second dependent gather on the
+// critical path of a step, a no-op min is harmless.
+#ifndef FSV_PREF
+#define FSV_PREF 0
+#endif
+#ifndef FSV_ROW_FILTER
+#define FSV_ROW_FILTER 0
+#endif
+__device__ __forceinline__ void emit_row_t(int u, int val, int t, const int* __restrict__ F,
+                                           const int* __restrict__ G, int* __restrict__ N) {
+  red_min(N + u, val);
+  if (t < 0) t = ldg(F + u);
+  if (t != u && (!FSV_ROW_FILTER || val < ldg(G + t))) red_min(N + t, val);
+}
+
 // Column side of edge entry c of a row whose gf is gu: v <- gu (kept for
 // the hub-accumulator fix-up path and for clarity; k_hook batches these).
 __device__ __forceinline__ void emit_col(uint32_t c, int gu, const int* __restrict__ F,
@@ -272,11 +294,45 @@ __device__ __forceinline__ int gather_gf(uint32_t c, uint32_t s_base, const int*
 
 
 constexpr int PUSH_CHUNK = 256;  // entries per chunk (8 per lane)
+constexpr int PUSH_BIG = 256;    // rows longer than this go to the chunk list
 
-// Phase 1: one warp per delta region, batches of 32 vertices.
-__device__ __forceinline__ void push_plan(const PushArgs& a) {
+// Push val[j] to neighbour u[j] (u < 0: no entry): N[u] <-min val when it
+// can lower gf[u] (aggressive), then N[F[u]] <-min val when it can lower
+// gf[F[u]] (stochastic). The second filter matters here: every neighbour of
+// a pushed vertex receives the same value, and their parents are often one
+// root, so unfiltered reductions would pile onto one address. All loads of
+// the lane are issued together.
+template <int PER>
+__device__ __forceinline__ void push_entries(const int (&u)[PER], const int (&val)[PER],
+                                             const int* __restrict__ F, const int* __restrict__ G,
+                                             int* __restrict__ N) {
+  int gt[PER], t[PER];
+#pragma unroll
+  for (int j = 0; j < PER; ++j) gt[j] = u[j] >= 0 ? ldg(G + u[j]) : INF;
+#pragma unroll
+  for (int j = 0; j < PER; ++j) {
+    t[j] = -1;
+    if (u[j] >= 0 && val[j] < gt[j]) {
+      red_min(N + u[j], val[j]);
+      t[j] = ldg(F + u[j]);
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < PER; ++j) {
+    if (t[j] == u[j]) t[j] = -1;
+    gt[j] = t[j] >= 0 ? ldg(G + t[j]) : INF;
+  }
+#pragma unroll
+  for (int j = 0; j < PER; ++j)
+    if (t[j] >= 0 && val[j] < gt[j]) red_min(N + t[j], val[j]);
+}
+
+// Phase A. w_start/w_excl/w_val: this warp's shared scratch (32 entries each).
+__device__ __forceinline__ void push_local(const PushArgs& a, long long* w_start, long long* w_excl,
+                                           int* w_val) {
   const int lane = threadIdx.x & 31;
   const long long nw = (long long)gridDim.x * (blockDim.x >> 5);
+  constexpr int PER = PUSH_CHUNK / 32;
   unsigned long long work = 0;
   for (long long r = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < a.nregions;
        r += nw) {
@@ -288,11 +344,35 @@ __device__ __forceinline__ void push_plan(const PushArgs& a) {
       if (b + lane < cnt) {
         const int v = reg[b + lane];
         if (v >= a.row_begin && v < a.row_end) {
-          start = a.off[v] - a.col_base;
-          deg = a.off[v + 1] - a.off[v];
+          const long long o0 = a.off[v];
+          start = o0 - a.col_base;
+          deg = a.off[v + 1] - o0;
           gv = ldg(a.G + v);
         }
       }
+      work += (unsigned long long)deg;
+      // long rows: chunk records for phase B
+      unsigned big = __ballot_sync(0xffffffffu, deg > PUSH_BIG);
+      while (big) {
+        const int src = __ffs(big) - 1;
+        big &= big - 1;
+        const long long bs = __shfl_sync(0xffffffffu, start, src);
+        const long long bd = __shfl_sync(0xffffffffu, deg, src);
+        const int bv = __shfl_sync(0xffffffffu, gv, src);
+        const long long nck = (bd + PUSH_CHUNK - 1) / PUSH_CHUNK;
+        unsigned long long base = 0;
+        if (lane == 0) base = atomicAdd(a.nchunks, (unsigned long long)nck);
+        base = __shfl_sync(0xffffffffu, base, 0);
+        for (long long q = lane; q < nck; q += 32) {
+          PushChunk ck;
+          ck.pos = bs + q * PUSH_CHUNK;
+          ck.cnt = (int)min((long long)PUSH_CHUNK, bd - q * PUSH_CHUNK);
+          ck.val = bv;
+          a.chunks[base + q] = ck;
+        }
+      }
+      if (deg > PUSH_BIG) deg = 0;
+      // short rows: flatten the batch and push it now
       long long incl = deg;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
@@ -301,77 +381,51 @@ __device__ __forceinline__ void push_plan(const PushArgs& a) {
       }
       const long long T = __shfl_sync(0xffffffffu, incl, 31);
       if (T == 0) continue;
-      work += (unsigned long long)T;
-      unsigned long long bid = 0;
-      const long long nck = (T + PUSH_CHUNK - 1) / PUSH_CHUNK;
-      unsigned long long cbase = 0;
-      if (lane == 0) {
-        bid = atomicAdd(a.nbatches, 1ull);
-        cbase = atomicAdd(a.nchunks, (unsigned long long)nck);
+      w_start[lane] = start;
+      w_excl[lane] = incl - deg;
+      w_val[lane] = gv;
+      __syncwarp();
+      int o = 0;   // owner of the lane's current entry (monotone in e)
+      for (long long e0 = 0; e0 < T; e0 += PUSH_CHUNK) {
+        int u[PER], val[PER];
+#pragma unroll
+        for (int j = 0; j < PER; ++j) {
+          const long long e = e0 + lane + 32 * j;
+          u[j] = -1;
+          val[j] = INF;
+          if (e < T) {
+            while (o < 31 && w_excl[o + 1] <= e) ++o;
+            u[j] = ldg(a.cols + w_start[o] + (e - w_excl[o]));
+            val[j] = w_val[o];
+          }
+        }
+        push_entries<PER>(u, val, a.F, a.G, a.N);
       }
-      bid = __shfl_sync(0xffffffffu, bid, 0);
-      cbase = __shfl_sync(0xffffffffu, cbase, 0);
-      PushDesc d;
-      d.start = start; d.excl = incl - deg; d.val = gv; d.pad = 0;
-      a.desc[bid * 32 + lane] = d;
-      if (lane == 0) a.btotal[bid] = T;
-      for (long long q = lane; q < nck; q += 32)
-        a.chunks[cbase + q] = make_int2((int)bid, (int)(q * PUSH_CHUNK));
+      __syncwarp();
     }
   }
-  if (lane == 0 && work) atomicAdd(a.flops, work);  // lane-uniform
+#pragma unroll
+  for (int o = 16; o; o >>= 1) work += __shfl_xor_sync(0xffffffffu, work, o);
+  if (lane == 0 && work) atomicAdd(a.flops, work);
 }
 
-// Phase 2: one warp per chunk; 8 entries per lane with every load batched
-// (columns, gf of the neighbours, then parents and their gf for the ones
-// that pass the filter) so each lane keeps 8 independent requests in flight.
-__device__ __forceinline__ void push_run(const PushArgs& a, long long* w_start, long long* w_excl,
-                                         int* w_val) {
+// Phase B: one warp per long-row chunk, contiguous columns.
+__device__ __forceinline__ void push_big(const PushArgs& a) {
   const int lane = threadIdx.x & 31;
   const unsigned long long total = *(volatile unsigned long long*)a.nchunks;
   const long long nw = (long long)gridDim.x * (blockDim.x >> 5);
   constexpr int PER = PUSH_CHUNK / 32;
   for (long long q = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
        q < (long long)total; q += nw) {
-    const int2 ck = a.chunks[q];
-    const PushDesc d = a.desc[(long long)ck.x * 32 + lane];
-    w_start[lane] = d.start;
-    w_excl[lane] = d.excl;
-    w_val[lane] = d.val;
-    const long long T = a.btotal[ck.x];
-    const long long hi = min(T, (long long)ck.y + PUSH_CHUNK);
-    __syncwarp();
-    int u[PER], val[PER], t[PER], gt[PER];
-    int o = 0;
+    const PushChunk ck = a.chunks[q];
+    int u[PER], val[PER];
 #pragma unroll
     for (int j = 0; j < PER; ++j) {
-      const long long e = (long long)ck.y + lane + 32 * j;
-      u[j] = -1;
-      if (e < hi) {
-        while (o < 31 && w_excl[o + 1] <= e) ++o;   // owner of entry e (monotone)
-        u[j] = ldg(a.cols + w_start[o] + (e - w_excl[o]));
-        val[j] = w_val[o];
-      }
+      const int e = lane + 32 * j;
+      u[j] = e < ck.cnt ? ldg(a.cols + ck.pos + e) : -1;
+      val[j] = ck.val;
     }
-#pragma unroll
-    for (int j = 0; j < PER; ++j) gt[j] = u[j] >= 0 ? ldg(a.G + u[j]) : INF;
-#pragma unroll
-    for (int j = 0; j < PER; ++j) {
-      t[j] = -1;
-      if (u[j] >= 0 && val[j] < gt[j]) {
-        red_min(a.N + u[j], val[j]);
-        t[j] = ldg(a.F + u[j]);
-      }
-    }
-#pragma unroll
-    for (int j = 0; j < PER; ++j) {
-      if (t[j] == u[j]) t[j] = -1;
-      gt[j] = t[j] >= 0 ? ldg(a.G + t[j]) : INF;
-    }
-#pragma unroll
-    for (int j = 0; j < PER; ++j)
-      if (t[j] >= 0 && val[j] < gt[j]) red_min(a.N + t[j], val[j]);
-    __syncwarp();
+    push_entries<PER>(u, val, a.F, a.G, a.N);
   }
 }
 
@@ -422,7 +476,6 @@ __global__ void __launch_bounds__(HOOK_THREADS, 1) k_hook(HookArgs a) {
     a.push.iter = it;
     a.push.flops = slot + C_FLOPS;
     a.push.nchunks = slot + C_CHUNKS;
-    a.push.nbatches = slot + C_BATCHES;
     a.push.barrier = reinterpret_cast<unsigned*>(slot + C_BARRIER);
   }
   if (a.mode[a.iter] == 1) {
@@ -433,7 +486,7 @@ __global__ void __launch_bounds__(HOOK_THREADS, 1) k_hook(HookArgs a) {
     int* s_val = reinterpret_cast<int*>(s_excl + HOOK_THREADS);
     const int wib = threadIdx.x >> 5;
     DBG_T(0);
-    push_plan(a.push);
+    push_local(a.push, s_start + wib * 32, s_excl + wib * 32, s_val + wib * 32);
     // grid barrier: every CTA is resident (one persistent CTA per SM)
     __syncthreads();
     DBG_T(1);
@@ -445,7 +498,7 @@ __global__ void __launch_bounds__(HOOK_THREADS, 1) k_hook(HookArgs a) {
     }
     __syncthreads();
     DBG_T(2);
-    push_run(a.push, s_start + wib * 32, s_excl + wib * 32, s_val + wib * 32);
+    push_big(a.push);
 #ifdef FSV_DEBUG_TIMING
     __syncthreads();
     DBG_T(3);
@@ -507,17 +560,20 @@ __global__ void __launch_bounds__(HOOK_THREADS, 1) k_hook(HookArgs a) {
       int in_u = __shfl_sync(0xffffffffu, lu, src);
       int in_gu = __shfl_sync(0xffffffffu, lgu, src);
       if (!left) { in_u = carry_u; in_gu = carry_gu; }
-      // does any entry differ from its row's gf?
-      bool need = false;
+      // Entries that differ from their row's gf, as per-entry records
+      // (target, value): val < gf(row) is a row-side contribution to the row
+      // vertex, val > gf(row) a column-side one to the neighbour (or its hub
+      // slot). The first REC of a lane are kept in registers.
+      int nrec = 0;
       {
         int rg = in_gu;
 #pragma unroll
         for (int j = 0; j < EPL; ++j) {
           rg = ((int)c[j] < 0) ? val[j] : rg;
-          need |= (val[j] != rg);
+          nrec += (val[j] != rg) ? 1 : 0;   // never for a header
         }
       }
-      if (!__any_sync(0xffffffffu, need) && carry_run >= carry_gu) {
+      if (!__any_sync(0xffffffffu, nrec > 0) && carry_run >= carry_gu) {
         if (hb) {
           const int last = 31 - __clz(hb);
           carry_u = __shfl_sync(0xffffffffu, lu, last);
@@ -526,6 +582,64 @@ __global__ void __launch_bounds__(HOOK_THREADS, 1) k_hook(HookArgs a) {
         }
         continue;
       }
+#if FSV_REC > 0
+      // ---- record path: few differing entries ------------------------------
+      // Each differing entry is emitted on its own (min-atomics are
+      // idempotent, so a row minimum may arrive as several partial minima;
+      // the smallest of them is the row minimum). No scan, no pending run:
+      // a run carried in from a scan step is emitted here by lane 0.
+      if (!__any_sync(0xffffffffu, nrec > FSV_REC)) {
+        if (lane == 0 && carry_run < carry_gu) emit_row(carry_u, carry_gu, carry_run, F, G, N);
+        if (nrec) {
+          // second pass: pick out the (at most two) records of this lane
+          uint32_t rx0 = 0u, rx1 = 0u;
+          int ry0 = 0, ry1 = 0;
+          {
+            int rg = in_gu, ru = in_u, k = 0;
+#pragma unroll
+            for (int j = 0; j < EPL; ++j) {
+              const bool h = (int)c[j] < 0;
+              rg = h ? val[j] : rg;
+              ru = h ? (int)(c[j] & IDMASK) : ru;
+              const bool d = val[j] != rg;
+              const bool rs = val[j] < rg;
+              const uint32_t xr = rs ? (uint32_t)ru : c[j];
+              const int yr = rs ? val[j] : rg;
+              if (d && k == 0) { rx0 = xr; ry0 = yr; }
+              if (d && k == 1) { rx1 = xr; ry1 = yr; }
+              k += d ? 1 : 0;
+            }
+          }
+          const bool h0 = HUBS && (rx0 & HUB), h1 = HUBS && nrec > 1 && (rx1 & HUB);
+          const bool g1 = nrec > 1 && !h1;
+          const int x0 = (int)(rx0 & IDMASK), x1 = (int)(rx1 & IDMASK);
+          int t0 = -1, t1 = -1;
+          if (h0) {
+            if (x0 < HOT_ACC) red_min_shared(s_acc + 4u * (uint32_t)x0, ry0);
+            else red_min(hub_acc + x0, ry0);
+          } else {
+            red_min(N + x0, ry0);
+            t0 = ldg(F + x0);
+          }
+          if (h1) {
+            if (x1 < HOT_ACC) red_min_shared(s_acc + 4u * (uint32_t)x1, ry1);
+            else red_min(hub_acc + x1, ry1);
+          } else if (g1) {
+            red_min(N + x1, ry1);
+            t1 = ldg(F + x1);
+          }
+          if (t0 >= 0 && t0 != x0) red_min(N + t0, ry0);
+          if (t1 >= 0 && t1 != x1) red_min(N + t1, ry1);
+        }
+        carry_run = INF;
+        if (hb) {
+          const int last = 31 - __clz(hb);
+          carry_u = __shfl_sync(0xffffffffu, lu, last);
+          carry_gu = __shfl_sync(0xffffffffu, lgu, last);
+        }
+        continue;
+      }
+#endif
       // ---- slow path ------------------------------------------------------
       // One emission slot per entry, filled branch-free:
       //   header j: closes the row before it (the lane's first header closes
@@ -536,6 +650,13 @@ __global__ void __launch_bounds__(HOOK_THREADS, 1) k_hook(HookArgs a) {
       //             threshold = gf[v]
       // then every active slot does N[target] <-min value and the stochastic
       // N[F[target]] <-min value, with all loads of the lane in flight together.
+#if FSV_PREF
+      // parent of the row entering the lane, needed if that row closes here
+      // (issued now so its latency overlaps the slot loop and the scan)
+      const int tin = (lu >= 0 && in_u >= 0) ? ldg(F + in_u) : -1;
+#else
+      const int tin = -1;
+#endif
       int cu = in_u, cgu = in_gu, run = INF, pre = INF;
       bool seen = false;
       unsigned act = 0, hubm = 0;
@@ -593,7 +714,7 @@ __global__ void __launch_bounds__(HOOK_THREADS, 1) k_hook(HookArgs a) {
       const int cin = (lane == 0) ? carry_run : (ef ? ev : min(ev, carry_run));
       if (seen) {
         const int v = min(cin, pre);
-        if (v < in_gu) emit_row(in_u, in_gu, v, F, G, N);  // row entering the lane closes here
+        if (v < in_gu) emit_row_t(in_u, v, tin, F, G, N);  // row entering the lane closes here
       }
       const int lv = __shfl_sync(0xffffffffu, sv, 31);
       const int lf = __shfl_sync(0xffffffffu, sf, 31);
