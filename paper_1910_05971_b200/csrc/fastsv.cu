@@ -146,6 +146,9 @@ static constexpr long long kTierMinN = 1LL << 23;   // rank tier only when the v
 #endif
 static constexpr int kTierMinDegree = FSV_TIER_MIN_DEG;
 static constexpr long long kTierMax = (long long)FSV_TIER_MAX_M << 20;   // 8M: 32 MB of gf + 32 MB of accumulators
+#ifndef FSV_GRAPH_BODY
+#define FSV_GRAPH_BODY 2
+#endif
 static constexpr int kTraceCap = 4096;    // iteration cap of the counter array
 
 struct fsv_ctx {
@@ -1380,6 +1383,8 @@ static LoopCtl loop_ctl(fsv_ctx* c, int graph) {
   l.tstamp = c->tstamp.p;
   l.cond = (unsigned long long)c->graph_cond;
   l.graph = graph;
+  l.X = c->X;
+  l.Y = c->Y;
   return l;
 }
 
@@ -1400,7 +1405,7 @@ static int launch_iteration(fsv_ctx* c, int k, int max_iter, bool graph = false)
     HookArgs a;
     a.ecol = c->ecolp; a.nspans = nspans; a.span_row = c->span_row.p;
     a.F = F; a.G = c->G; a.N = N; a.G_hub = c->G_hub.p; a.H = c->H; a.HT = c->HT;
-    a.hub_acc = c->hacc;
+    a.hub_acc = c->hacc; a.hub_id = c->hub_id.p;
     a.done = c->done.p; a.mode = c->mode.p; a.iter = k;
     PushArgs& p = a.push;
     p.list = c->dlist.p; p.count = c->dcount.p; p.rcap = c->rcap;
@@ -1411,6 +1416,7 @@ static int launch_iteration(fsv_ctx* c, int k, int max_iter, bool graph = false)
     unsigned long long* slot = c->cnt.p + (size_t)(k - 1) * NCOUNT;
     p.flops = slot + C_FLOPS; p.nchunks = slot + C_CHUNKS;
     p.barrier = reinterpret_cast<unsigned*>(slot + C_BARRIER); p.chunks = c->chunks.p;
+    a.fix_barrier = reinterpret_cast<unsigned*>(slot + C_FIXBAR);
     a.lc = lc;
     // persistent, one CTA per SM; cooperative launch guarantees co-residency
     // for the grid barrier of the sparse (push) path
@@ -1425,11 +1431,11 @@ static int launch_iteration(fsv_ctx* c, int k, int max_iter, bool graph = false)
     pmark(c, k, 1);
     ++c->launches;
   }
-  if (c->HT) {
+  if (c->HT && !FSV_FUSE_HUBFIX) {
     pmark(c, k, 2);
     k_hubfix<<<grid_for(c, c->HT, 256), 256, 0, st>>>(c->hacc, c->hub_id.p, c->G_hub.p, c->HT, F, c->G, N,
                                                        c->done.p, c->mode.p, k,
-                                                       graph ? c->iterbuf.p : nullptr);
+                                                       graph ? c->iterbuf.p : nullptr, c->X, c->Y);
     pmark(c, k, 3);
     ++c->launches;
   }
@@ -1474,8 +1480,11 @@ static int ensure_graph(fsv_ctx* c, int cap) {
   c->profile = false;
   CUDA_TRY(cudaStreamBeginCaptureToGraph(c->stream, body, nullptr, nullptr, 0,
                                          cudaStreamCaptureModeRelaxed));
-  int rc = launch_iteration(c, 2, cap, true);
-  if (!rc) rc = launch_iteration(c, 3, cap, true);
+  // FSV_GRAPH_BODY iterations per body pass (kernels pick their buffers by
+  // the device-side iteration number; iterations past convergence exit at
+  // once, which is cheaper than relaunching the body)
+  int rc = FSV_OK;
+  for (int k = 2; k < 2 + FSV_GRAPH_BODY && !rc; ++k) rc = launch_iteration(c, k, cap, true);
   cudaGraph_t captured = body;
   const cudaError_t ec = cudaStreamEndCapture(c->stream, &captured);
   c->profile = prof;
@@ -1688,10 +1697,10 @@ static int solve_impl(fsv_ctx* c, const fsv_config* cfg, int32_t* snapshots, int
     done = *c->h_done;
     if (done == 0) return fail(FSV_ERR_RUNTIME, "graph loop ended without convergence");
     {
-      // kernels the graph ran: each body pass is two iterations' worth
+      // kernels the graph ran: iterations 2..it, rounded up to whole body passes
       const int it = done > 0 ? done : -done;
-      const int passes = std::max(1, it / 2);
-      c->launches += passes * 2 * (2 + (c->HT ? 1 : 0));
+      const int passes = std::max(1, (it - 1 + FSV_GRAPH_BODY - 1) / FSV_GRAPH_BODY);
+      c->launches += passes * FSV_GRAPH_BODY * (2 + (c->HT && !FSV_FUSE_HUBFIX ? 1 : 0));
     }
     if (done > 0 && (rc = ensure_events(c, (size_t)done + 1))) return rc;
     if (done > 0) CUDA_TRY(cudaEventRecord(c->events[done], st));
@@ -1756,7 +1765,7 @@ static int solve_impl(fsv_ctx* c, const fsv_config* cfg, int32_t* snapshots, int
       } else {
         c->push_ms += hk;
       }
-      if (c->HT) c->hubfix_ms += span(k, 2, 3);
+      if (c->HT && !FSV_FUSE_HUBFIX) c->hubfix_ms += span(k, 2, 3);
       if (c->comm && c->n) c->allreduce_ms += span(k, 8, 9);
       c->shortcut_ms += span(k, 6, 7);
     }

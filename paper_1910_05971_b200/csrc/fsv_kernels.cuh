@@ -82,7 +82,8 @@ constexpr int SMEM_OPTIN_INTS = 232448 / 4;   // 227 KB opt-in dynamic shared me
 constexpr int SC_THREADS = 512;
 constexpr int NCOUNT = 16;               // counter slots per iteration
 enum { C_GF = 0, C_F = 1, C_NONSTAR = 2, C_ROOTS = 3, C_VIOL = 4,   // vertex-pass counters
-       C_FLOPS = 5, C_CHUNKS = 6, C_BARRIER = 8 };     // push bookkeeping
+       C_FLOPS = 5, C_CHUNKS = 6, C_BARRIER = 8,       // push bookkeeping
+       C_FIXBAR = 9 };                                 // hub fix-up barrier of the dense hook
 
 // ---- memory helpers -------------------------------------------------------
 
@@ -122,7 +123,16 @@ struct LoopCtl {
   unsigned long long* tstamp;        // per-iteration end time (%globaltimer, ns)
   unsigned long long cond;           // cudaGraphConditionalHandle
   int graph;                         // 0 host loop, 1 inside the graph, 2 k_first before it
+  int* X;                            // graph mode: the two rotating parent buffers; iteration k
+  int* Y;                            // reads F = f_{k-1} and writes N = f_k by its parity
 };
+
+// Graph mode: the loop body is one iteration, so the buffers rotate by the
+// iteration number read on the device (k_first leaves f_1 in Y).
+__device__ __forceinline__ void loop_bufs(const LoopCtl& lc, int it, int*& F, int*& N) {
+  F = (it & 1) ? lc.X : lc.Y;
+  N = (it & 1) ? lc.Y : lc.X;
+}
 
 __device__ __forceinline__ unsigned long long global_ns() {
   unsigned long long t;
@@ -186,6 +196,8 @@ struct HookArgs {
   int H;                  // shared-memory slots (multiple of 4)
   int HT;                 // all tier slots: [0,H) shared memory, [H,HT) the L2 rank tier
   int* hub_acc;           // column-side minima aimed at tier slots
+  const int* hub_id;      // slot -> vertex (fused hub fix-up)
+  unsigned* fix_barrier;  // grid barrier before the fused hub fix-up
   const int* done;        // convergence flag (iteration number, 0 = running)
   const int* mode;        // mode[iter]: 0 dense pull (this layout), 1 sparse push
   int iter;
@@ -242,6 +254,11 @@ __device__ __forceinline__ void emit_row(int u, int gu, int val, const int* __re
 // loaded here when t < 0). The stochastic target is filtered by gf[t] only
 // with FSV_ROW_FILTER: the filter is a second dependent gather on the
 // critical path of a step, a no-op min is harmless.
+// k_hook applies the hub accumulator itself after a grid barrier instead of
+// a separate k_hubfix launch.
+#ifndef FSV_FUSE_HUBFIX
+#define FSV_FUSE_HUBFIX 1
+#endif
 #ifndef FSV_PREF
 #define FSV_PREF 0
 #endif
@@ -474,9 +491,13 @@ __global__ void __launch_bounds__(HOOK_THREADS, 1) k_hook(HookArgs a) {
     unsigned long long* slot = a.lc.cnt_base + (size_t)(it - 1) * NCOUNT;
     a.iter = it;
     a.push.iter = it;
+    int *Fb, *Nb;
+    loop_bufs(a.lc, it, Fb, Nb);
+    a.F = Fb; a.N = Nb; a.push.F = Fb; a.push.N = Nb;
     a.push.flops = slot + C_FLOPS;
     a.push.nchunks = slot + C_CHUNKS;
     a.push.barrier = reinterpret_cast<unsigned*>(slot + C_BARRIER);
+    a.fix_barrier = reinterpret_cast<unsigned*>(slot + C_FIXBAR);
   }
   if (a.mode[a.iter] == 1) {
     // sparse iteration: push from the vertices whose gf changed; the push
@@ -734,6 +755,24 @@ __global__ void __launch_bounds__(HOOK_THREADS, 1) k_hook(HookArgs a) {
       const int v = s_hub[i];
       if (v != INF) red_min(hub_acc + i, v);
     }
+#if FSV_FUSE_HUBFIX
+    // hub fix-up in the same launch: grid barrier (every CTA is resident),
+    // then the accumulated column-side minima go to N (k_hubfix's work)
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      atomicAdd(a.fix_barrier, 1u);
+      while (*(volatile unsigned*)a.fix_barrier < gridDim.x) __nanosleep(32);
+      __threadfence();
+    }
+    __syncthreads();
+    for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < a.HT; s += gridDim.x * blockDim.x) {
+      const int acc = __ldcg(hub_acc + s);
+      if (acc == INF) continue;
+      hub_acc[s] = INF;
+      emit_row(ldg(a.hub_id + s), ldg(a.G_hub + s), acc, F, G, N);
+    }
+#endif
   }
 }
 
@@ -744,9 +783,13 @@ __global__ void __launch_bounds__(HOOK_THREADS, 1) k_hook(HookArgs a) {
 __global__ void k_hubfix(int* __restrict__ hub_acc, const int* __restrict__ hub_id,
                          const int* __restrict__ G_hub, int H, const int* __restrict__ F,
                          const int* __restrict__ G, int* __restrict__ N, const int* done, const int* mode,
-                         int iter, const int* iterp) {
+                         int iter, const int* iterp, int* X, int* Y) {
   if (*(volatile const int*)done) return;
-  if (iterp) iter = *(volatile const int*)iterp;
+  if (iterp) {   // graph mode: iteration and buffers from the device (loop_bufs)
+    iter = *(volatile const int*)iterp;
+    F = (iter & 1) ? X : Y;
+    N = (iter & 1) ? Y : X;
+  }
   if (mode[iter] != 0) return;
   for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < H; s += gridDim.x * blockDim.x) {
     const int acc = hub_acc[s];
@@ -892,6 +935,9 @@ __global__ void __launch_bounds__(SC_THREADS) k_shortcut(ShortcutArgs a) {
   if (a.lc.graph == 1) {
     a.iter = loop_iter(a.lc, a.iter);
     a.cnt = a.lc.cnt_base + (size_t)(a.iter - 1) * NCOUNT;
+    int* Nb;
+    loop_bufs(a.lc, a.iter, a.F, Nb);
+    a.N = Nb;
   }
   unsigned c[5] = {0u, 0u, 0u, 0u, 0u};
   const long long stride = (long long)gridDim.x * blockDim.x;
