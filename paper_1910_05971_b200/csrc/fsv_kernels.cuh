@@ -913,9 +913,11 @@ __device__ __forceinline__ void sgroup_commit(bool valid, long long i, const SGr
     c[C_NONSTAR] += (gg.x != nu.x) + (gg.y != nu.y) + (gg.z != nu.z) + (gg.w != nu.w);
     c[C_ROOTS] += (nu.x == u) + (nu.y == u + 1) + (nu.z == u + 2) + (nu.w == u + 3);
     c[C_VIOL] += (nu.x > fo.x) + (nu.y > fo.y) + (nu.z > fo.z) + (nu.w > fo.w);
-    G4[i] = gg;
-    F4[i] = gg;
     m4 = (gg.x != go.x) | ((gg.y != go.y) << 1) | ((gg.z != go.z) << 2) | ((gg.w != go.w) << 3);
+    // stores only where the value changes: once most vertices are stable,
+    // whole sectors stay clean and are never written back to DRAM
+    if (m4) G4[i] = gg;
+    if ((gg.x != fo.x) | (gg.y != fo.y) | (gg.z != fo.z) | (gg.w != fo.w)) F4[i] = gg;
   }
   delta_append(m4, (int)(i << 2), region, wo);
 }
