@@ -167,6 +167,8 @@ struct fsv_ctx {
   DBuf<int> span_row, hub_id, f1;
   // full symmetric CSR of this rank's rows, for sparse (push) iterations
   DBuf<int64_t> csr_off;
+  DBuf<int> csr_off32;       // int32 copy when the offsets fit (f_1 pass)
+  bool off32 = false;
   DBuf<int> csr_cols;
   int64_t col_base = 0, row_begin = 0, row_end = 0;
   int64_t csr_local = 0;   // entries of this rank's rows in csr_cols
@@ -710,17 +712,24 @@ __global__ void k_f1(const int64_t* __restrict__ off, const ColT* __restrict__ c
 
 // In-solve f_1 for the full single-rank row range: 4 vertices per thread,
 // offsets as two 16-byte loads, the four first-column loads in flight together.
-__global__ void k_f1_solve(const int64_t* __restrict__ off, const int* __restrict__ cols, long long n,
+template <typename OffT>
+__global__ void k_f1_solve(const OffT* __restrict__ off, const int* __restrict__ cols, long long n,
                            int* __restrict__ f1) {
   const long long n4 = n >> 2;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i <= n4;
        i += (long long)gridDim.x * blockDim.x) {
     const long long u0 = i << 2;
     if (u0 + 4 <= n) {
-      const longlong2 a = *reinterpret_cast<const longlong2*>(off + u0);   // off[u0], off[u0+1]
-      const longlong2 b = *reinterpret_cast<const longlong2*>(off + u0 + 2);
-      const long long e4 = off[u0 + 4];
-      const long long o[5] = {a.x, a.y, b.x, b.y, e4};
+      long long o[5];
+      if constexpr (sizeof(OffT) == 4) {
+        const int4 a = *reinterpret_cast<const int4*>(off + u0);            // off[u0 .. u0+3]
+        o[0] = a.x; o[1] = a.y; o[2] = a.z; o[3] = a.w;
+      } else {
+        const longlong2 a = *reinterpret_cast<const longlong2*>(off + u0);  // off[u0], off[u0+1]
+        const longlong2 b = *reinterpret_cast<const longlong2*>(off + u0 + 2);
+        o[0] = a.x; o[1] = a.y; o[2] = b.x; o[3] = b.y;
+      }
+      o[4] = off[u0 + 4];
       int4 r;
       int* rp = reinterpret_cast<int*>(&r);
 #pragma unroll
@@ -1149,6 +1158,15 @@ static int upload_impl(fsv_ctx* c, int64_t n, const int64_t* h_off, const ColT* 
     uint64_t d = 1469598103934665603ull;
     for (uint32_t x : h) { d ^= x; d *= 1099511628211ull; }
     fprintf(stderr, "[upload] layout digest %016llx E=%lld R=%d\n", (unsigned long long)d, E, R);
+  }
+  // int32 copy of the offsets for the per-solve f_1 pass when they fit
+  // (half the bytes of its offset stream)
+  c->off32 = h_off[n] < (int64_t(1) << 31);
+  if (c->off32) {
+    CUDA_TRY(c->csr_off32.alloc((size_t)n + 1));
+    k_narrow<<<grid_for(c, n + 1, 256), 256, 0, st>>>(d_off.p, n + 1, c->csr_off32.p);
+    CUDA_TRY(cudaStreamSynchronize(st));
+    CUDA_TRY(cudaGetLastError());
   }
   c->n = n;
   c->m_dir = h_off[n];
@@ -1656,8 +1674,12 @@ static int solve_impl(fsv_ctx* c, const fsv_config* cfg, int32_t* snapshots, int
   // iteration 1 in closed form: f_1[u] = min(u, smallest neighbour) from the
   // resident CSR rows (first column of each sorted row), every solve
   if (c->n && !c->comm && c->row_begin == 0 && c->row_end == c->n) {
-    k_f1_solve<<<grid_for(c, c->n / 4 + 1, 256, 32), 256, 0, st>>>(c->csr_off.p, c->csr_cols.p, c->n,
-                                                                   c->f1.p);
+    if (c->off32)
+      k_f1_solve<int><<<grid_for(c, c->n / 4 + 1, 256, 32), 256, 0, st>>>(c->csr_off32.p, c->csr_cols.p,
+                                                                        c->n, c->f1.p);
+    else
+      k_f1_solve<int64_t><<<grid_for(c, c->n / 4 + 1, 256, 32), 256, 0, st>>>(c->csr_off.p, c->csr_cols.p,
+                                                                            c->n, c->f1.p);
     ++c->launches;
   } else if (c->n) {
     k_f1<int><<<grid_for(c, c->n, 256, 64), 256, 0, st>>>(c->csr_off.p, c->csr_cols.p, c->col_base,
