@@ -259,6 +259,13 @@ __device__ __forceinline__ void emit_row(int u, int gu, int val, const int* __re
 #ifndef FSV_FUSE_HUBFIX
 #define FSV_FUSE_HUBFIX 1
 #endif
+// A scan step with emissions on at least FSV_DENSE_LANES lanes puts the warp
+// in dense mode: its next step goes straight to the scan path (no
+// differing-entry count). 0 disables; used by the hub-table kernels (skewed
+// graphs, where the dense iterations have most entries differing).
+#ifndef FSV_DENSE_LANES
+#define FSV_DENSE_LANES 16
+#endif
 #ifndef FSV_PREF
 #define FSV_PREF 0
 #endif
@@ -552,6 +559,7 @@ __global__ void __launch_bounds__(HOOK_THREADS, 1) k_hook(HookArgs a) {
   const int nspans = (int)a.nspans;
   const uint64_t pol = policy_evict_first();
 
+  bool dense = false;   // warp-uniform, see FSV_DENSE_LANES
   for (int s = gw; s < nspans; s += nwarps) {
     int carry_u = ldg(a.span_row + s);              // row open at the span start
     int carry_gu = carry_u >= 0 ? ldg(G + carry_u) : INF;
@@ -585,8 +593,10 @@ __global__ void __launch_bounds__(HOOK_THREADS, 1) k_hook(HookArgs a) {
       // (target, value): val < gf(row) is a row-side contribution to the row
       // vertex, val > gf(row) a column-side one to the neighbour (or its hub
       // slot). The first REC of a lane are kept in registers.
+      // (skipped while the warp is in dense mode: the last scan step had
+      // emissions on most lanes, so the next one almost surely needs the scan)
       int nrec = 0;
-      {
+      if (!dense) {
         int rg = in_gu;
 #pragma unroll
         for (int j = 0; j < EPL; ++j) {
@@ -594,7 +604,7 @@ __global__ void __launch_bounds__(HOOK_THREADS, 1) k_hook(HookArgs a) {
           nrec += (val[j] != rg) ? 1 : 0;   // never for a header
         }
       }
-      if (!__any_sync(0xffffffffu, nrec > 0) && carry_run >= carry_gu) {
+      if (!dense && !__any_sync(0xffffffffu, nrec > 0) && carry_run >= carry_gu) {
         if (hb) {
           const int last = 31 - __clz(hb);
           carry_u = __shfl_sync(0xffffffffu, lu, last);
@@ -609,7 +619,7 @@ __global__ void __launch_bounds__(HOOK_THREADS, 1) k_hook(HookArgs a) {
       // idempotent, so a row minimum may arrive as several partial minima;
       // the smallest of them is the row minimum). No scan, no pending run:
       // a run carried in from a scan step is emitted here by lane 0.
-      if (!__any_sync(0xffffffffu, nrec > FSV_REC)) {
+      if (!dense && !__any_sync(0xffffffffu, nrec > FSV_REC)) {
         if (lane == 0 && carry_run < carry_gu) emit_row(carry_u, carry_gu, carry_run, F, G, N);
         if (nrec) {
           // second pass: pick out the (at most two) records of this lane
@@ -721,6 +731,9 @@ __global__ void __launch_bounds__(HOOK_THREADS, 1) k_hook(HookArgs a) {
         for (int j = 0; j < EPL; ++j)
           if (t[j] >= 0 && t[j] != w[j]) red_min(N + t[j], y[j]);
       }
+#if FSV_DENSE_LANES > 0
+      if (HUBS) dense = __popc(__ballot_sync(0xffffffffu, act != 0)) >= FSV_DENSE_LANES;
+#endif
       // segmented inclusive scan of (seen, run): min of the run open at the
       // end of each lane
       int sv = run, sf = seen ? 1 : 0;
