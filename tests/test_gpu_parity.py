@@ -87,6 +87,31 @@ def test_edge_cases(solver):
         check_against_oracle(solver, n, p)
 
 
+def test_push_long_rows_and_record_path(solver):
+    """Sparse (push) iterations over very long rows (phase-B chunks) and
+    dense iterations with few differing entries (record path): stars of
+    thousands of leaves hung off a random forest, with and without hub slots,
+    under the default and the sparse-only schedule; every snapshot equals
+    the oracle's."""
+    rng = np.random.default_rng(73)
+    for n, centers, extra in ((20000, 3, 2000), (120000, 8, 30000), (70000, 1, 0)):
+        leaves = rng.integers(0, n, n - centers)
+        hub = rng.integers(0, centers, n - centers)
+        star = np.stack([hub * (n // max(centers, 1)), leaves], 1)
+        chain = np.stack([rng.integers(0, n, extra), rng.integers(0, n, extra)], 1)
+        pairs = np.concatenate([star, chain]).astype(np.int32)
+        g = fb.build_csr(n, pairs)
+        o = oracle.fastsv_csr(n, g.row_offsets, g.col_indices, snapshots=True)
+        for hub_slots in (0, -1):
+            solver.set_hub_slots(hub_slots)
+            solver.upload(g)
+            for policy in (0, 2):
+                labels, iters, gfc, fc, ms, snaps = solver.run(snapshots=True, snap_cap=64, policy=policy)
+                assert iters == o.iterations and gfc.tolist() == o.gf_changed.tolist(), (n, hub_slots, policy)
+                assert np.array_equal(snaps, o.snapshots), (n, hub_slots, policy)
+    solver.set_hub_slots(0)
+
+
 def test_empty_graph_runs_one_iteration():
     r = fb.fastsv_la(fb.build_csr(0, []))
     assert r.iterations == 1 and r.labeling.component_count == 0
