@@ -1128,8 +1128,8 @@ static int upload_impl(fsv_ctx* c, int64_t n, const int64_t* h_off, const ColT* 
     CUDA_TRY(c->mode.alloc((size_t)kTraceCap + 2));
     CUDA_TRY(c->iterbuf.alloc(4));
     CUDA_TRY(c->tstamp.alloc((size_t)kTraceCap + 2));
-    // rows longer than PUSH_BIG: sum of ceil(deg / PUSH_CHUNK) <= 2 * mloc / PUSH_CHUNK + 1
-    CUDA_TRY(c->chunks.alloc((size_t)(2 * (mloc / PUSH_CHUNK) + 64)));
+    // rows longer than PUSH_BIG: sum of ceil(deg / PUSH_BCHUNK) <= mloc / PUSH_BCHUNK + mloc / PUSH_BIG + 1
+    CUDA_TRY(c->chunks.alloc((size_t)(mloc / PUSH_BCHUNK + mloc / PUSH_BIG + 64)));
   }
   CUDA_TRY(c->cnt.alloc((size_t)kTraceCap * NCOUNT));
   umark(6);

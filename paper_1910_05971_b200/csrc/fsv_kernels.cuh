@@ -161,7 +161,7 @@ __device__ __forceinline__ bool converged_exit(const int* done, const LoopCtl& l
 // chunk, so a high-degree vertex is spread over the whole GPU.
 struct PushChunk {
   long long pos;     // first column index of the chunk (rank-local)
-  int cnt;           // entries in the chunk (<= PUSH_CHUNK)
+  int cnt;           // entries in the chunk (<= PUSH_BCHUNK)
   int val;           // gf[v] pushed to every neighbour
 };
 
@@ -317,8 +317,16 @@ __device__ __forceinline__ int gather_gf(uint32_t c, uint32_t s_base, const int*
 // the reference's SpMSpV (kernels.py:71-102) without the mngf accumulator.
 
 
-constexpr int PUSH_CHUNK = 256;  // entries per chunk (8 per lane)
-constexpr int PUSH_BIG = 256;    // rows longer than this go to the chunk list
+constexpr int PUSH_CHUNK = 256;  // entries per phase-A pass (8 per lane)
+#ifndef FSV_PUSH_BIG
+#define FSV_PUSH_BIG 128
+#endif
+#ifndef FSV_PUSH_BCHUNK
+#define FSV_PUSH_BCHUNK 64
+#endif
+constexpr int PUSH_BIG = FSV_PUSH_BIG;        // rows longer than this go to the chunk list
+constexpr int PUSH_BCHUNK = FSV_PUSH_BCHUNK;  // entries per long-row chunk (phase B)
+static_assert(PUSH_BCHUNK % 32 == 0 && PUSH_BIG <= 8192, "push chunk shapes");
 
 // Push val[j] to neighbour u[j] (u < 0: no entry): N[u] <-min val when it
 // can lower gf[u] (aggressive), then N[F[u]] <-min val when it can lower
@@ -383,14 +391,14 @@ __device__ __forceinline__ void push_local(const PushArgs& a, long long* w_start
         const long long bs = __shfl_sync(0xffffffffu, start, src);
         const long long bd = __shfl_sync(0xffffffffu, deg, src);
         const int bv = __shfl_sync(0xffffffffu, gv, src);
-        const long long nck = (bd + PUSH_CHUNK - 1) / PUSH_CHUNK;
+        const long long nck = (bd + PUSH_BCHUNK - 1) / PUSH_BCHUNK;
         unsigned long long base = 0;
         if (lane == 0) base = atomicAdd(a.nchunks, (unsigned long long)nck);
         base = __shfl_sync(0xffffffffu, base, 0);
         for (long long q = lane; q < nck; q += 32) {
           PushChunk ck;
-          ck.pos = bs + q * PUSH_CHUNK;
-          ck.cnt = (int)min((long long)PUSH_CHUNK, bd - q * PUSH_CHUNK);
+          ck.pos = bs + q * PUSH_BCHUNK;
+          ck.cnt = (int)min((long long)PUSH_BCHUNK, bd - q * PUSH_BCHUNK);
           ck.val = bv;
           a.chunks[base + q] = ck;
         }
@@ -438,7 +446,7 @@ __device__ __forceinline__ void push_big(const PushArgs& a) {
   const int lane = threadIdx.x & 31;
   const unsigned long long total = *(volatile unsigned long long*)a.nchunks;
   const long long nw = (long long)gridDim.x * (blockDim.x >> 5);
-  constexpr int PER = PUSH_CHUNK / 32;
+  constexpr int PER = PUSH_BCHUNK / 32;
   for (long long q = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
        q < (long long)total; q += nw) {
     const PushChunk ck = a.chunks[q];
