@@ -146,6 +146,9 @@ static constexpr long long kTierMinN = 1LL << 23;   // rank tier only when the v
 #endif
 static constexpr int kTierMinDegree = FSV_TIER_MIN_DEG;
 static constexpr long long kTierMax = (long long)FSV_TIER_MAX_M << 20;   // 8M: 32 MB of gf + 32 MB of accumulators
+#ifndef FSV_SMALL_TASKS
+#define FSV_SMALL_TASKS 4
+#endif
 #ifndef FSV_GRAPH_BODY
 #define FSV_GRAPH_BODY 2
 #endif
@@ -280,10 +283,10 @@ extern "C" int fsv_create(int device, fsv_ctx** out) {
     c->sc_grid = std::max(1, per_sm) * c->sm_count;
   }
   const int hook_smem = std::max((kHubMax + HOT_ACC) * (int)sizeof(int), PUSH_SCRATCH_BYTES);
-  cudaError_t e = cudaFuncSetAttribute(k_hook<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       hook_smem);
-  if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(k_hook<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, hook_smem);
+  cudaError_t e = cudaSuccess;
+  for (const void* fn : {(const void*)k_hook<true, false, STEPS>, (const void*)k_hook<true, true, STEPS>,
+                         (const void*)k_hook<true, false, 1>, (const void*)k_hook<true, true, 1>})
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, hook_smem);
   if (e != cudaSuccess) {
     delete c;
     return fail(FSV_ERR_RUNTIME, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
@@ -675,13 +678,13 @@ __global__ void k_pad(uint32_t* ecol, long long E, long long Epad, int n, int* n
   }
 }
 
-// span_row[s] = vertex of the row whose entries include s*SPAN when that
+// span_row[s] = vertex of the row whose entries include s*task when that
 // entry is an edge (the row started in an earlier span), else -1.
 __global__ void k_span_row(const long long* __restrict__ nzoff, const int* __restrict__ nzrows,
-                           int R1, long long nspans, int* __restrict__ span_row) {
+                           int R1, long long nspans, int task, int* __restrict__ span_row) {
   for (long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x; s < nspans;
        s += (long long)gridDim.x * blockDim.x) {
-    const long long target = s * SPAN;
+    const long long target = s * task;
     int lo = 0, hi = R1;  // upper_bound over nzoff[0..R1)
     while (lo < hi) {
       const int mid = (lo + hi) >> 1;
@@ -818,6 +821,13 @@ __global__ void k_csr_from_keys(const unsigned long long* __restrict__ keys, con
     if (i == M - 1)
       for (long long r = u + 1; r <= n; ++r) off[r] = M;
   }
+}
+
+// A layout with fewer STEP-entry steps than FSV_SMALL_TASKS x the resident
+// hook warps is processed one step per warp task (every warp busy) instead
+// of STEPS-step tasks (a few long tasks).
+static bool small_layout(const fsv_ctx* c, long long Epad) {
+  return Epad / STEP < (long long)FSV_SMALL_TASKS * c->sm_count * (HOOK_THREADS / 32);
 }
 
 static int grid_for(fsv_ctx* c, long long work, int threads, int per_sm = 8) {
@@ -1082,10 +1092,15 @@ static int upload_impl(fsv_ctx* c, int64_t n, const int64_t* h_off, const ColT* 
   umark(4);
   k_pad<<<grid_for(c, std::max<long long>(Epad - E, 1), 256), 256, 0, st>>>(c->ecolp, E, Epad, (int)n,
                                                                              nzrows.p, R, nzoff.p);
-  const long long nspans = Epad / SPAN;
-  CUDA_TRY(c->span_row.alloc((size_t)std::max<long long>(nspans, 1)));
-  if (nspans)
-    k_span_row<<<grid_for(c, nspans, 256), 256, 0, st>>>(nzoff.p, nzrows.p, R + 1, nspans, c->span_row.p);
+  // the row open at every task boundary: SPAN entries, or STEP entries for a
+  // small layout whose warp tasks are single steps (small_layout())
+  const long long nsteps = Epad / STEP;
+  const bool small = small_layout(c, Epad);
+  const long long ntask = small ? nsteps : Epad / SPAN;
+  CUDA_TRY(c->span_row.alloc((size_t)std::max<long long>(ntask, 1)));
+  if (ntask)
+    k_span_row<<<grid_for(c, ntask, 256), 256, 0, st>>>(nzoff.p, nzrows.p, R + 1, ntask,
+                                                         small ? STEP : SPAN, c->span_row.p);
   umark(5);
 
   // f_1 is computed by every solve (k_f1 in solve_impl), not cached here
@@ -1418,7 +1433,11 @@ static int launch_iteration(fsv_ctx* c, int k, int max_iter, bool graph = false)
   }
   int* F = bufF(c, k);
   int* N = bufN(c, k);
-  const long long nspans = c->Epad / SPAN;
+  // warp tasks: STEPS steps each, or one step when the layout has fewer
+  // STEP-entry steps than FSV_SMALL_TASKS x the resident warps (a small graph
+  // then spreads over every warp instead of a few long tasks)
+  const bool small = small_layout(c, c->Epad);
+  const long long nspans = small ? c->Epad / STEP : c->Epad / SPAN;
   {
     HookArgs a;
     a.ecol = c->ecolp; a.nspans = nspans; a.span_row = c->span_row.p;
@@ -1442,9 +1461,12 @@ static int launch_iteration(fsv_ctx* c, int k, int max_iter, bool graph = false)
     void* kargs[] = {&a};
     const size_t dyn = std::max<size_t>(c->H ? (size_t)(HOT_ACC + c->H) * sizeof(int) : 0,
                                         PUSH_SCRATCH_BYTES);
-    const void* fn = c->HT > c->H ? (const void*)k_hook<true, true>
-                     : c->H       ? (const void*)k_hook<true, false>
-                                  : (const void*)k_hook<false, false>;
+    const void* fn = small ? (c->HT > c->H ? (const void*)k_hook<true, true, 1>
+                              : c->H       ? (const void*)k_hook<true, false, 1>
+                                           : (const void*)k_hook<false, false, 1>)
+                           : (c->HT > c->H ? (const void*)k_hook<true, true, STEPS>
+                              : c->H       ? (const void*)k_hook<true, false, STEPS>
+                                           : (const void*)k_hook<false, false, STEPS>);
     CUDA_TRY(cudaLaunchCooperativeKernel(fn, dim3(c->sm_count), dim3(HOOK_THREADS), kargs, dyn, st));
     pmark(c, k, 1);
     ++c->launches;

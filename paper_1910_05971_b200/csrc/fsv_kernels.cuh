@@ -187,8 +187,8 @@ struct PushArgs {
 
 struct HookArgs {
   const uint32_t* ecol;   // oriented entries (headers + edges), padded to SPAN
-  long long nspans;
-  const int* span_row;    // vertex of the row open at each span start, -1 if none
+  long long nspans;       // warp tasks of NSTEP consecutive STEP-entry steps
+  const int* span_row;    // vertex of the row open at each task start, -1 if none
   const int* F;           // f_k
   const int* G;           // gf_k
   int* N;                 // f_{k+1}, pre-initialised to gf_k
@@ -497,7 +497,7 @@ __device__ __forceinline__ int gather_gf_tier(uint32_t c, uint32_t s_base, const
 
 // HUBS = false (no hub slots, H == 0) compiles the hub table, hub mask and
 // accumulators out; TIER (implies HUBS) adds the L2 rank tier gathers.
-template <bool HUBS, bool TIER>
+template <bool HUBS, bool TIER, int NSTEP>
 __global__ void __launch_bounds__(HOOK_THREADS, 1) k_hook(HookArgs a) {
   extern __shared__ int s_hub[];
   if (*(volatile const int*)a.done) return;
@@ -569,15 +569,15 @@ __global__ void __launch_bounds__(HOOK_THREADS, 1) k_hook(HookArgs a) {
 
   bool dense = false;   // warp-uniform, see FSV_DENSE_LANES
   for (int s = gw; s < nspans; s += nwarps) {
-    int carry_u = ldg(a.span_row + s);              // row open at the span start
+    int carry_u = ldg(a.span_row + s);              // row open at the task start
     int carry_gu = carry_u >= 0 ? ldg(G + carry_u) : INF;
     int carry_run = INF;
-    const uint4* p = reinterpret_cast<const uint4*>(a.ecol + (size_t)s * SPAN) + 2 * lane;
+    const uint4* p = reinterpret_cast<const uint4*>(a.ecol + (size_t)s * (NSTEP * STEP)) + 2 * lane;
     uint4 n0 = ld_stream(p, pol), n1 = ld_stream(p + 1, pol);
 #pragma unroll 1
-    for (int st = 0; st < STEPS; ++st) {
+    for (int st = 0; st < NSTEP; ++st) {
       const uint32_t c[EPL] = {n0.x, n0.y, n0.z, n0.w, n1.x, n1.y, n1.z, n1.w};
-      if (st + 1 < STEPS) {
+      if (st + 1 < NSTEP) {
         n0 = ld_stream(p + (st + 1) * 64, pol);
         n1 = ld_stream(p + (st + 1) * 64 + 1, pol);
       }
