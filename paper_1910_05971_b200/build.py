@@ -74,9 +74,26 @@ def build_fastsv(force=False, verbose=False, extra_flags=()) -> Path:
     return LIB_FASTSV
 
 
+LIB_FASTSV_CHECKED = PKG / "libfastsv_checked.so"
+
+
+def build_fastsv_checked(force=False, verbose=False) -> Path:
+    """Bounds-checked build (-DFSV_CHECKS) for the tests: every vertex-array
+    load and min-reduction of a solve must hit a registered buffer, else the
+    kernel traps. Not used by the product path."""
+    srcs = [CSRC / s for s in CUDA_SOURCES]
+    deps = srcs + [CSRC / h for h in CUDA_HEADERS] + [INCLUDE / "fastsv.h"]
+    if force or _stale(LIB_FASTSV_CHECKED, deps):
+        cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared",
+               "-cudart", "static", "-I", INCLUDE, "-DFSV_CHECKS", "-o", LIB_FASTSV_CHECKED, *srcs,
+               "-ldl", "-lpthread"]
+        _run(cmd, verbose)
+    return LIB_FASTSV_CHECKED
+
+
 def build_all(force=False, verbose=False):
     return [build_graphgen(force, verbose), build_oracle(force, verbose),
-            build_fastsv(force, verbose)]
+            build_fastsv(force, verbose), build_fastsv_checked(force, verbose)]
 
 
 if __name__ == "__main__":

@@ -1651,7 +1651,22 @@ static int solve_variant(fsv_ctx* c, const fsv_config& d, int cap, int32_t* snap
   return FSV_OK;
 }
 
+static int solve_body(fsv_ctx* c, const fsv_config* cfg, int32_t* snapshots, int32_t snap_cap);
+
+// Checked builds clear the registered ranges after every solve, so upload
+// kernels (which read other buffers through the same helpers) are unchecked.
 static int solve_impl(fsv_ctx* c, const fsv_config* cfg, int32_t* snapshots, int32_t snap_cap) {
+  const int rc = solve_body(c, cfg, snapshots, snap_cap);
+#ifdef FSV_CHECKS
+  if (c) {
+    const ChkRanges none{};
+    cudaMemcpyToSymbol(g_chk, &none, sizeof none);
+  }
+#endif
+  return rc;
+}
+
+static int solve_body(fsv_ctx* c, const fsv_config* cfg, int32_t* snapshots, int32_t snap_cap) {
   if (!c) return fail(FSV_ERR_CONTRACT, "NULL context");
   if (!c->ready) return fail(FSV_ERR_CONTRACT, "no graph uploaded");
   CUDA_TRY(cudaSetDevice(c->device));
@@ -1683,6 +1698,18 @@ static int solve_impl(fsv_ctx* c, const fsv_config* cfg, int32_t* snapshots, int
   }
   c->variant = false;
   c->labels_src = c->G;
+#ifdef FSV_CHECKS
+  {  // checked build: the buffers the solve kernels may load from / reduce into
+    ChkRanges r{};
+    auto add_ld = [&](const int* p, size_t len) { if (p && r.nl < 12) { r.lo[r.nl] = p; r.hi[r.nl++] = p + len; } };
+    auto add_red = [&](const int* p, size_t len) { if (p && r.nr < 4) { r.rlo[r.nr] = p; r.rhi[r.nr++] = p + len; } };
+    add_red(c->xb.p, c->xb.n); add_red(c->f1.p, c->f1.n); add_red(c->hacc, (size_t)c->HT);
+    add_ld(c->xb.p, c->xb.n); add_ld(c->f1.p, c->f1.n); add_ld(c->gb.p, c->gb.n);
+    add_ld(c->G_hub.p, c->G_hub.n); add_ld(c->hub_id.p, c->hub_id.n); add_ld(c->csr_cols.p, c->csr_cols.n);
+    add_ld(c->span_row.p, c->span_row.n);
+    CUDA_TRY(cudaMemcpyToSymbolAsync(g_chk, &r, sizeof r, 0, cudaMemcpyHostToDevice, st));
+  }
+#endif
   if (c->profile && (rc = ensure_pevents(c, 2 * kPev))) return rc;
 
   // graph mode: the whole iteration loop is one conditional-WHILE graph launch

@@ -27,6 +27,7 @@
 // second time (a no-op min is harmless; the gather costs more than it saves).
 #pragma once
 #include <cstdint>
+#include <cstdio>
 #include <cuda_runtime.h>
 
 namespace fsv {
@@ -102,9 +103,53 @@ __device__ __forceinline__ uint4 ld_stream(const uint4* p, uint64_t pol) {
   return r;
 }
 
-__device__ __forceinline__ int ldg(const int* p) { return __ldg(p); }
+#ifdef FSV_CHECKS
+// Checked build (tests only, -DFSV_CHECKS): every read-only vertex-array load
+// and every min-reduction of the FastSV solve kernels must hit one of the
+// buffers the host registered for this solve, else the kernel traps. Ranges
+// are empty (checks off) outside fastsv solves.
+struct ChkRanges {
+  const int* rlo[4];
+  const int* rhi[4];
+  int nr;
+  const int* lo[12];
+  const int* hi[12];
+  int nl;
+};
+__device__ ChkRanges g_chk;
+__device__ __noinline__ void chk_fail(const void* p, int red) {
+  printf("FSV_CHECKS: %s outside the registered buffers: %p (block %d thread %d)\n",
+         red ? "reduction" : "load", p, blockIdx.x, threadIdx.x);
+  __trap();
+}
+__device__ __forceinline__ void chk_red(const int* p) {
+  const int nr = g_chk.nr;
+  if (!nr) return;
+  for (int i = 0; i < nr; ++i)
+    if (p >= g_chk.rlo[i] && p < g_chk.rhi[i]) return;
+  chk_fail(p, 1);
+}
+__device__ __forceinline__ void chk_ld(const int* p) {
+  const int nl = g_chk.nl;
+  if (!nl) return;
+  for (int i = 0; i < nl; ++i)
+    if (p >= g_chk.lo[i] && p < g_chk.hi[i]) return;
+  chk_fail(p, 0);
+}
+#define FSV_CHK_RED(p) chk_red(p)
+#define FSV_CHK_LD(p) chk_ld(p)
+#else
+#define FSV_CHK_RED(p) do { } while (0)
+#define FSV_CHK_LD(p) do { } while (0)
+#endif
+
+__device__ __forceinline__ int ldg(const int* p) {
+  FSV_CHK_LD(p);
+  return __ldg(p);
+}
 
 __device__ __forceinline__ void red_min(int* p, int v) {
+  FSV_CHK_RED(p);
   asm volatile("red.relaxed.gpu.global.min.s32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
 }
 
@@ -298,6 +343,9 @@ __device__ __forceinline__ void emit_col(uint32_t c, int gu, const int* __restri
 // (32-bit shared address, no generic conversion), everything else from
 // global through the read-only path. Both loads are predicated, no branch.
 __device__ __forceinline__ int gather_gf(uint32_t c, uint32_t s_base, const int* __restrict__ G) {
+#ifdef FSV_CHECKS
+  if (!(c & HUB)) chk_ld(G + (c & IDMASK));
+#endif
   int v;
   asm("{\n\t.reg .pred p;\n\t"
       "setp.ne.u32 p, %1, 0;\n\t"
@@ -470,6 +518,9 @@ __device__ __forceinline__ int gather_gf_tier(uint32_t c, uint32_t s_base, const
   const bool hub = (c & HUB) != 0;
   const bool sm = hub && x < H;
   const int* gp = hub ? G_hub + x : G + x;
+#ifdef FSV_CHECKS
+  if (!sm) chk_ld(gp);
+#endif
   asm("{\n\t.reg .pred p;\n\t"
       "setp.ne.u32 p, %1, 0;\n\t"
       "@p  ld.shared.b32 %0, [%2];\n\t"

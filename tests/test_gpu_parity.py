@@ -428,3 +428,24 @@ def test_public_variant_api():
     suite = fb.ablation_suite(g)
     assert [s[0] for s in suite] == ["sv1", "sv2", "sv3", "sv4", "sv5"]
     assert suite[4][1] == fb.fastsv(g).iterations
+
+
+def test_bounds_checked_build_runs_clean():
+    """The -DFSV_CHECKS build (libfastsv_checked.so: every vertex-array load
+    and min-reduction of a solve checked against the registered buffers, trap
+    on a miss) solves the golden suite sample, skewed graphs with hub slots,
+    sparse-only schedules and a row partition without a trap, bit-exactly.
+    Run in a subprocess: a trap poisons the CUDA context."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parent.parent
+    lib = root / "paper_1910_05971_b200" / "libfastsv_checked.so"
+    if not lib.exists():
+        pytest.skip("libfastsv_checked.so not built")
+    env = dict(os.environ, FSV_LIB=str(lib))
+    r = subprocess.run([sys.executable, str(root / "tools" / "sanitize_run.py")], env=env,
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    assert "mismatches: 0" in r.stdout, r.stdout[-2000:]
