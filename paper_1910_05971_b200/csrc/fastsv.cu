@@ -1121,8 +1121,10 @@ static int upload_impl(fsv_ctx* c, int64_t n, const int64_t* h_off, const ColT* 
   // solve buffers: n + dummy vertex, padded for 16-byte vector access
   const size_t nv = ((size_t)n + 1 + 63) / 64 * 64;
   // Y (f_k of even k) is f1's buffer: k_first leaves f_1 there without a copy
-  CUDA_TRY(c->xb.alloc(nv)); CUDA_TRY(c->gb.alloc(nv));
-  c->X = c->xb.p; c->Y = c->f1.p; c->G = c->gb.p;
+  long long vpad = 0;   // dev: FSV_VPAD shifts X and G (placement checks)
+  if (const char* e = getenv("FSV_VPAD")) vpad = atoll(e) / 4 * 4;
+  CUDA_TRY(c->xb.alloc(nv + vpad)); CUDA_TRY(c->gb.alloc(nv + vpad));
+  c->X = c->xb.p + vpad; c->Y = c->f1.p; c->G = c->gb.p + vpad;
   CUDA_TRY(c->G_hub.alloc(std::max(HT, 4))); {
     long long hpad = 0;   // dev: FSV_HPAD shifts the hub accumulator (placement checks)
     if (const char* e = getenv("FSV_HPAD")) hpad = atoll(e);
