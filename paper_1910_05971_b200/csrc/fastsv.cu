@@ -1128,7 +1128,7 @@ static int upload_impl(fsv_ctx* c, int64_t n, const int64_t* h_off, const ColT* 
   CUDA_TRY(c->G_hub.alloc(std::max(HT, 4))); {
     long long hpad = 0;   // dev: FSV_HPAD shifts the hub accumulator (placement checks)
     if (const char* e = getenv("FSV_HPAD")) hpad = atoll(e);
-    CUDA_TRY(c->hub_acc.alloc(std::max(HT, 4) + hpad));
+    CUDA_TRY(c->hub_acc.alloc(std::max<long long>(acc_len(HT), 4) + hpad));
     c->hacc = c->hub_acc.p + hpad;
   }
   CUDA_TRY(c->done.alloc(1)); CUDA_TRY(c->ticket.alloc(1));
@@ -1705,7 +1705,7 @@ static int solve_body(fsv_ctx* c, const fsv_config* cfg, int32_t* snapshots, int
     ChkRanges r{};
     auto add_ld = [&](const int* p, size_t len) { if (p && r.nl < 12) { r.lo[r.nl] = p; r.hi[r.nl++] = p + len; } };
     auto add_red = [&](const int* p, size_t len) { if (p && r.nr < 4) { r.rlo[r.nr] = p; r.rhi[r.nr++] = p + len; } };
-    add_red(c->xb.p, c->xb.n); add_red(c->f1.p, c->f1.n); add_red(c->hacc, (size_t)c->HT);
+    add_red(c->xb.p, c->xb.n); add_red(c->f1.p, c->f1.n); add_red(c->hacc, (size_t)acc_len(c->HT));
     add_ld(c->xb.p, c->xb.n); add_ld(c->f1.p, c->f1.n); add_ld(c->gb.p, c->gb.n);
     add_ld(c->G_hub.p, c->G_hub.n); add_ld(c->hub_id.p, c->hub_id.n); add_ld(c->csr_cols.p, c->csr_cols.n);
     add_ld(c->span_row.p, c->span_row.n);

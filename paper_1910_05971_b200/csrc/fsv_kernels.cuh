@@ -157,6 +157,22 @@ __device__ __forceinline__ void red_min_shared(uint32_t saddr, int v) {
   asm volatile("red.shared.min.s32 [%0], %1;" :: "r"(saddr), "r"(v) : "memory");
 }
 
+// Hub accumulator slot -> int index. FSV_ACC_STRIDE > 1 spreads the first
+// ACC_SPREAD slots (the shared-memory hubs, whose accumulators take most of
+// the column-side reductions) one per STRIDE ints; tier slots beyond stay
+// packed.
+#ifndef FSV_ACC_STRIDE
+#define FSV_ACC_STRIDE 1
+#endif
+constexpr int ACC_SPREAD = 65536;
+__host__ __device__ __forceinline__ long long acc_at(long long s) {
+  return FSV_ACC_STRIDE == 1 ? s
+         : (s < ACC_SPREAD ? s * FSV_ACC_STRIDE : (long long)ACC_SPREAD * FSV_ACC_STRIDE + (s - ACC_SPREAD));
+}
+__host__ __device__ __forceinline__ long long acc_len(long long slots) {
+  return slots <= 0 ? 0 : acc_at(slots - 1) + 1;
+}
+
 // ---- argument blocks --------------------------------------------------------
 
 // Device-side loop control. Graph mode runs the iteration loop inside a
@@ -331,7 +347,7 @@ __device__ __forceinline__ void emit_col(uint32_t c, int gu, const int* __restri
                                          int* __restrict__ hub_acc) {
   const int x = (int)(c & IDMASK);
   if (c & HUB) {
-    red_min(hub_acc + x, gu);
+    red_min(hub_acc + acc_at(x), gu);
   } else {
     red_min(N + x, gu);
     int t = ldg(F + x);
@@ -706,14 +722,14 @@ __global__ void __launch_bounds__(HOOK_THREADS, 1) k_hook(HookArgs a) {
           int t0 = -1, t1 = -1;
           if (h0) {
             if (x0 < HOT_ACC) red_min_shared(s_acc + 4u * (uint32_t)x0, ry0);
-            else red_min(hub_acc + x0, ry0);
+            else red_min(hub_acc + acc_at(x0), ry0);
           } else {
             red_min(N + x0, ry0);
             t0 = ldg(F + x0);
           }
           if (h1) {
             if (x1 < HOT_ACC) red_min_shared(s_acc + 4u * (uint32_t)x1, ry1);
-            else red_min(hub_acc + x1, ry1);
+            else red_min(hub_acc + acc_at(x1), ry1);
           } else if (g1) {
             red_min(N + x1, ry1);
             t1 = ldg(F + x1);
@@ -775,7 +791,7 @@ __global__ void __launch_bounds__(HOOK_THREADS, 1) k_hook(HookArgs a) {
           if ((act >> j) & 1u) {
             if (HUBS && ((hubm >> j) & 1u)) {
               if (w[j] < HOT_ACC) red_min_shared(s_acc + 4u * (uint32_t)w[j], y[j]);
-              else red_min(hub_acc + w[j], y[j]);
+              else red_min(hub_acc + acc_at(w[j]), y[j]);
             } else {
               red_min(N + w[j], y[j]);
               t[j] = ldg(F + w[j]);
@@ -825,7 +841,7 @@ __global__ void __launch_bounds__(HOOK_THREADS, 1) k_hook(HookArgs a) {
     __syncthreads();
     for (int i = threadIdx.x; i < HOT_ACC; i += blockDim.x) {
       const int v = s_hub[i];
-      if (v != INF) red_min(hub_acc + i, v);
+      if (v != INF) red_min(hub_acc + acc_at(i), v);
     }
 #if FSV_FUSE_HUBFIX
     // hub fix-up in the same launch: grid barrier (every CTA is resident),
@@ -839,9 +855,9 @@ __global__ void __launch_bounds__(HOOK_THREADS, 1) k_hook(HookArgs a) {
     }
     __syncthreads();
     for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < a.HT; s += gridDim.x * blockDim.x) {
-      const int acc = __ldcg(hub_acc + s);
+      const int acc = __ldcg(hub_acc + acc_at(s));
       if (acc == INF) continue;
-      hub_acc[s] = INF;
+      hub_acc[acc_at(s)] = INF;
       emit_row(ldg(a.hub_id + s), ldg(a.G_hub + s), acc, F, G, N);
     }
 #endif
@@ -864,9 +880,9 @@ __global__ void k_hubfix(int* __restrict__ hub_acc, const int* __restrict__ hub_
   }
   if (mode[iter] != 0) return;
   for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < H; s += gridDim.x * blockDim.x) {
-    const int acc = hub_acc[s];
+    const int acc = hub_acc[acc_at(s)];
     if (acc == INF) continue;
-    hub_acc[s] = INF;
+    hub_acc[acc_at(s)] = INF;
     const int h = ldg(hub_id + s);
     emit_row(h, ldg(G_hub + s), acc, F, G, N);
   }
@@ -1125,7 +1141,7 @@ __global__ void k_solve_init(int* X, int* Y, int* G, long long n, int* hub_acc, 
                              int* mode, int first_mode, unsigned long long* tstamp) {
   const long long t0 = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const long long stride = (long long)gridDim.x * blockDim.x;
-  for (long long s = t0; s < H; s += stride) hub_acc[s] = INF;
+  for (long long s = t0; s < H; s += stride) hub_acc[acc_at(s)] = INF;
   for (long long k = t0; k < ncnt; k += stride) cnt[k] = 0ull;
   if (t0 == 0) {
     X[n] = (int)n; Y[n] = (int)n; G[n] = INF;  // dummy vertex n of the padding row
