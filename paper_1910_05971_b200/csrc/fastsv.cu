@@ -1456,6 +1456,7 @@ static int launch_iteration(fsv_ctx* c, int k, int max_iter, bool graph = false)
     p.flops = slot + C_FLOPS; p.nchunks = slot + C_CHUNKS;
     p.barrier = reinterpret_cast<unsigned*>(slot + C_BARRIER); p.chunks = c->chunks.p;
     a.fix_barrier = reinterpret_cast<unsigned*>(slot + C_FIXBAR);
+    a.task_ctr = reinterpret_cast<unsigned*>(slot + C_SPANS);
     a.lc = lc;
     // persistent, one CTA per SM; cooperative launch guarantees co-residency
     // for the grid barrier of the sparse (push) path

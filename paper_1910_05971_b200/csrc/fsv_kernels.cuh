@@ -84,7 +84,8 @@ constexpr int SC_THREADS = 512;
 constexpr int NCOUNT = 16;               // counter slots per iteration
 enum { C_GF = 0, C_F = 1, C_NONSTAR = 2, C_ROOTS = 3, C_VIOL = 4,   // vertex-pass counters
        C_FLOPS = 5, C_CHUNKS = 6, C_BARRIER = 8,       // push bookkeeping
-       C_FIXBAR = 9 };                                 // hub fix-up barrier of the dense hook
+       C_FIXBAR = 9,                                   // hub fix-up barrier of the dense hook
+       C_SPANS = 10 };                                 // dynamic task counter of the dense hook
 
 // ---- memory helpers -------------------------------------------------------
 
@@ -259,6 +260,7 @@ struct HookArgs {
   int* hub_acc;           // column-side minima aimed at tier slots
   const int* hub_id;      // slot -> vertex (fused hub fix-up)
   unsigned* fix_barrier;  // grid barrier before the fused hub fix-up
+  unsigned* task_ctr;     // dynamic tail of the dense task loop (FSV_DYN_TAIL)
   const int* done;        // convergence flag (iteration number, 0 = running)
   const int* mode;        // mode[iter]: 0 dense pull (this layout), 1 sparse push
   int iter;
@@ -324,6 +326,11 @@ __device__ __forceinline__ void emit_row(int u, int gu, int val, const int* __re
 // in dense mode: its next step goes straight to the scan path (no
 // differing-entry count). 0 disables; used by the hub-table kernels (skewed
 // graphs, where the dense iterations have most entries differing).
+// Dense task loop: the last FSV_DYN_TAIL rounds of tasks are handed out by
+// an atomic counter (0: fully static round-robin).
+#ifndef FSV_DYN_TAIL
+#define FSV_DYN_TAIL 2
+#endif
 #ifndef FSV_DENSE_LANES
 #define FSV_DENSE_LANES 16
 #endif
@@ -580,6 +587,7 @@ __global__ void __launch_bounds__(HOOK_THREADS, 1) k_hook(HookArgs a) {
     a.push.nchunks = slot + C_CHUNKS;
     a.push.barrier = reinterpret_cast<unsigned*>(slot + C_BARRIER);
     a.fix_barrier = reinterpret_cast<unsigned*>(slot + C_FIXBAR);
+    a.task_ctr = reinterpret_cast<unsigned*>(slot + C_SPANS);
   }
   if (a.mode[a.iter] == 1) {
     // sparse iteration: push from the vertices whose gf changed; the push
@@ -635,7 +643,14 @@ __global__ void __launch_bounds__(HOOK_THREADS, 1) k_hook(HookArgs a) {
   const uint64_t pol = policy_evict_first();
 
   bool dense = false;   // warp-uniform, see FSV_DENSE_LANES
-  for (int s = gw; s < nspans; s += nwarps) {
+  // Tasks gw, gw + nwarps, ... for the first `fixed` rounds, then (hub-table
+  // kernels with at least 4 rounds, FSV_DYN_TAIL > 0) one task at a time
+  // from a shared counter: the slow warps of a launch no longer set its tail,
+  // which every CTA waits out at the hub fix-up barrier.
+  const int rounds = nspans / nwarps;
+  const int fixed = (HUBS && FSV_DYN_TAIL > 0 && rounds >= 4) ? rounds - FSV_DYN_TAIL : INF;
+  int k = 0;
+  for (int s = gw; s < nspans;) {
     int carry_u = ldg(a.span_row + s);              // row open at the task start
     int carry_gu = carry_u >= 0 ? ldg(G + carry_u) : INF;
     int carry_run = INF;
@@ -836,6 +851,17 @@ __global__ void __launch_bounds__(HOOK_THREADS, 1) k_hook(HookArgs a) {
     }
     // the run still open at the span end: partial minimum of row carry_u
     if (lane == 0 && carry_run < carry_gu) emit_row(carry_u, carry_gu, carry_run, F, G, N);
+    if constexpr (HUBS && FSV_DYN_TAIL > 0) {
+      if (++k < fixed) {
+        s += nwarps;
+      } else {
+        unsigned q = 0;
+        if (lane == 0) q = atomicAdd(a.task_ctr, 1u);
+        s = fixed * nwarps + (int)__shfl_sync(0xffffffffu, q, 0);
+      }
+    } else {
+      s += nwarps;
+    }
   }
   if (HUBS) {
     __syncthreads();
