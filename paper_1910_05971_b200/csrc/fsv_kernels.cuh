@@ -331,6 +331,9 @@ __device__ __forceinline__ void emit_row(int u, int gu, int val, const int* __re
 #ifndef FSV_DYN_TAIL
 #define FSV_DYN_TAIL 2
 #endif
+#ifndef FSV_DYN_NOHUB
+#define FSV_DYN_NOHUB 0
+#endif
 #ifndef FSV_DENSE_LANES
 #define FSV_DENSE_LANES 16
 #endif
@@ -648,7 +651,8 @@ __global__ void __launch_bounds__(HOOK_THREADS, 1) k_hook(HookArgs a) {
   // from a shared counter: the slow warps of a launch no longer set its tail,
   // which every CTA waits out at the hub fix-up barrier.
   const int rounds = nspans / nwarps;
-  const int fixed = (HUBS && FSV_DYN_TAIL > 0 && rounds >= 4) ? rounds - FSV_DYN_TAIL : INF;
+  constexpr bool DYN = FSV_DYN_TAIL > 0 && (HUBS || FSV_DYN_NOHUB);
+  const int fixed = (DYN && rounds >= 4) ? rounds - FSV_DYN_TAIL : INF;
   int k = 0;
   for (int s = gw; s < nspans;) {
     int carry_u = ldg(a.span_row + s);              // row open at the task start
@@ -851,7 +855,7 @@ __global__ void __launch_bounds__(HOOK_THREADS, 1) k_hook(HookArgs a) {
     }
     // the run still open at the span end: partial minimum of row carry_u
     if (lane == 0 && carry_run < carry_gu) emit_row(carry_u, carry_gu, carry_run, F, G, N);
-    if constexpr (HUBS && FSV_DYN_TAIL > 0) {
+    if constexpr (DYN) {
       if (++k < fixed) {
         s += nwarps;
       } else {
