@@ -149,6 +149,9 @@ static constexpr long long kTierMax = (long long)FSV_TIER_MAX_M << 20;   // 8M: 
 #ifndef FSV_SMALL_TASKS
 #define FSV_SMALL_TASKS 4
 #endif
+#ifndef FSV_GRAPH_IF
+#define FSV_GRAPH_IF 0
+#endif
 #ifndef FSV_GRAPH_BODY
 #define FSV_GRAPH_BODY 2
 #endif
@@ -236,6 +239,8 @@ struct fsv_ctx {
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t graph_exec = nullptr;
   cudaGraphConditionalHandle graph_cond = 0;
+  cudaGraphConditionalHandle graph_cond_next = 0;   // IF node of the body's second iteration
+  bool graph_half2 = false;                          // capturing the body's first iteration
   bool graph_dirty = true;
   int graph_key_policy = -1, graph_key_cap = -1;
   double graph_key_thr = -1.0;
@@ -1417,6 +1422,7 @@ static LoopCtl loop_ctl(fsv_ctx* c, int graph) {
   l.cnt_base = c->cnt.p;
   l.tstamp = c->tstamp.p;
   l.cond = (unsigned long long)c->graph_cond;
+  l.cond_next = (graph && c->graph_half2) ? (unsigned long long)c->graph_cond_next : 0ull;
   l.graph = graph;
   l.X = c->X;
   l.Y = c->Y;
@@ -1521,18 +1527,62 @@ static int ensure_graph(fsv_ctx* c, int cap) {
   cudaGraph_t body = cp.conditional.phGraph_out[0];
   const bool prof = c->profile;
   c->profile = false;
+  int rc = FSV_OK;
+#if FSV_GRAPH_IF
+  // body = iteration A, then IF(A did not stop) { iteration B }: two
+  // iterations per body pass without launching B's kernels after the last
+  // iteration (A's vertex pass sets the IF condition with the loop's)
+  CUDA_TRY(cudaGraphConditionalHandleCreate(&c->graph_cond_next, body, 0, cudaGraphCondAssignDefault));
+  c->graph_half2 = true;
+  CUDA_TRY(cudaStreamBeginCaptureToGraph(c->stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+  rc = launch_iteration(c, 2, cap, true);
+  {
+    cudaGraph_t captured = body;
+    const cudaError_t ec = cudaStreamEndCapture(c->stream, &captured);
+    c->graph_half2 = false;
+    if (rc) { c->profile = prof; return rc; }
+    CUDA_TRY(ec);
+  }
+  // the IF node depends on every leaf of the captured first iteration
+  size_t nn = 0;
+  CUDA_TRY(cudaGraphGetNodes(body, nullptr, &nn));
+  std::vector<cudaGraphNode_t> nodes(nn), leaves;
+  CUDA_TRY(cudaGraphGetNodes(body, nodes.data(), &nn));
+  for (cudaGraphNode_t nd : nodes) {
+    size_t nd_out = 0;
+    CUDA_TRY(cudaGraphNodeGetDependentNodes(nd, nullptr, &nd_out));
+    if (nd_out == 0) leaves.push_back(nd);
+  }
+  cudaGraphNodeParams ip = {};
+  ip.type = cudaGraphNodeTypeConditional;
+  ip.conditional.handle = c->graph_cond_next;
+  ip.conditional.type = cudaGraphCondTypeIf;
+  ip.conditional.size = 1;
+  cudaGraphNode_t ifnode;
+  CUDA_TRY(cudaGraphAddNode(&ifnode, body, leaves.data(), leaves.size(), &ip));
+  cudaGraph_t body2 = ip.conditional.phGraph_out[0];
+  CUDA_TRY(cudaStreamBeginCaptureToGraph(c->stream, body2, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+  rc = launch_iteration(c, 3, cap, true);
+  {
+    cudaGraph_t captured = body2;
+    const cudaError_t ec = cudaStreamEndCapture(c->stream, &captured);
+    c->profile = prof;
+    if (rc) return rc;
+    CUDA_TRY(ec);
+  }
+#else
   CUDA_TRY(cudaStreamBeginCaptureToGraph(c->stream, body, nullptr, nullptr, 0,
                                          cudaStreamCaptureModeRelaxed));
   // FSV_GRAPH_BODY iterations per body pass (kernels pick their buffers by
   // the device-side iteration number; iterations past convergence exit at
   // once, which is cheaper than relaunching the body)
-  int rc = FSV_OK;
   for (int k = 2; k < 2 + FSV_GRAPH_BODY && !rc; ++k) rc = launch_iteration(c, k, cap, true);
   cudaGraph_t captured = body;
   const cudaError_t ec = cudaStreamEndCapture(c->stream, &captured);
   c->profile = prof;
   if (rc) return rc;
   CUDA_TRY(ec);
+#endif
   CUDA_TRY(cudaGraphInstantiate(&c->graph_exec, c->graph, 0));
   c->graph_dirty = false;
   c->graph_key_policy = c->policy;
@@ -1771,10 +1821,12 @@ static int solve_body(fsv_ctx* c, const fsv_config* cfg, int32_t* snapshots, int
     done = *c->h_done;
     if (done == 0) return fail(FSV_ERR_RUNTIME, "graph loop ended without convergence");
     {
-      // kernels the graph ran: iterations 2..it, rounded up to whole body passes
+      // kernels the graph ran: iterations 2..it, rounded up to whole body
+      // passes unless the IF node skips a pass's second iteration
       const int it = done > 0 ? done : -done;
+      const int per_it = 2 + (c->HT && !FSV_FUSE_HUBFIX ? 1 : 0);
       const int passes = std::max(1, (it - 1 + FSV_GRAPH_BODY - 1) / FSV_GRAPH_BODY);
-      c->launches += passes * FSV_GRAPH_BODY * (2 + (c->HT && !FSV_FUSE_HUBFIX ? 1 : 0));
+      c->launches += (FSV_GRAPH_IF ? std::max(1, it - 1) : passes * FSV_GRAPH_BODY) * per_it;
     }
     if (done > 0 && (rc = ensure_events(c, (size_t)done + 1))) return rc;
     if (done > 0) CUDA_TRY(cudaEventRecord(c->events[done], st));

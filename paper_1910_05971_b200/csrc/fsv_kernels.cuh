@@ -183,7 +183,8 @@ struct LoopCtl {
   int* iterp;                        // graph mode: current iteration (>= 2)
   unsigned long long* cnt_base;      // counters of iteration 1 (NCOUNT per iteration)
   unsigned long long* tstamp;        // per-iteration end time (%globaltimer, ns)
-  unsigned long long cond;           // cudaGraphConditionalHandle
+  unsigned long long cond;           // cudaGraphConditionalHandle of the WHILE loop
+  unsigned long long cond_next;      // IF handle guarding the body's next iteration (0: none)
   int graph;                         // 0 host loop, 1 inside the graph, 2 k_first before it
   int* X;                            // graph mode: the two rotating parent buffers; iteration k
   int* Y;                            // reads F = f_{k-1} and writes N = f_k by its parity
@@ -975,7 +976,10 @@ __device__ __forceinline__ void finish_counters(const unsigned (&c)[5], unsigned
       else stop = false;
       lc.tstamp[iter] = global_ns();
       if (lc.graph) *lc.iterp = iter + 1;                       // 2: iteration 1 before the graph
-      if (lc.graph == 1) cudaGraphSetConditional(lc.cond, stop ? 0u : 1u);
+      if (lc.graph == 1) {
+        cudaGraphSetConditional(lc.cond, stop ? 0u : 1u);
+        if (lc.cond_next) cudaGraphSetConditional(lc.cond_next, stop ? 0u : 1u);
+      }
       // product choice for the next iteration (choose_kernel, driver.py:51-61)
       int m = 0;
       if (dl.policy == 2) m = 1;
