@@ -244,6 +244,7 @@ struct fsv_ctx {
   bool graph_dirty = true;
   int graph_key_policy = -1, graph_key_cap = -1;
   double graph_key_thr = -1.0;
+  std::vector<long long> graph_key;   // every pointer/size the captured launches use
   bool use_graph = true;
   int sc_grid = 296;  // resident blocks of the vertex-pass kernels
   // multi-GPU
@@ -1507,9 +1508,22 @@ static int launch_iteration(fsv_ctx* c, int k, int max_iter, bool graph = false)
   return FSV_OK;
 }
 
+// The buffers, sizes and launch shapes baked into the captured iteration
+// loop. A re-upload that leaves all of them unchanged (the same graph again:
+// the workspaces only grow) keeps the instantiated graph.
+static std::vector<long long> graph_key(const fsv_ctx* c) {
+  auto P = [](const void* p) { return (long long)(uintptr_t)p; };
+  return {P(c->ecolp), c->Epad, P(c->span_row.p), P(c->X), P(c->Y), P(c->G), P(c->G_hub.p), c->H, c->HT,
+          P(c->hacc), P(c->hub_id.p), P(c->done.p), P(c->mode.p), P(c->dlist.p), P(c->dcount.p), c->rcap,
+          c->dgrid, P(c->csr_off.p), P(c->csr_cols.p), c->col_base, c->row_begin, c->row_end, P(c->cnt.p),
+          P(c->chunks.p), P(c->iterbuf.p), P(c->tstamp.p), P(c->ticket.p), P(c->partials.p), c->n,
+          c->sm_count};
+}
+
 // Builds (or reuses) the CUDA graph of the iteration loop: one conditional
 // WHILE node whose body is an even and an odd iteration (buffer parity).
 static int ensure_graph(fsv_ctx* c, int cap) {
+  if (c->graph_dirty && c->graph_exec && graph_key(c) == c->graph_key) c->graph_dirty = false;
   if (!c->graph_dirty && c->graph_exec && c->graph_key_policy == c->policy &&
       c->graph_key_thr == c->threshold && c->graph_key_cap == cap)
     return FSV_OK;
@@ -1585,6 +1599,7 @@ static int ensure_graph(fsv_ctx* c, int cap) {
 #endif
   CUDA_TRY(cudaGraphInstantiate(&c->graph_exec, c->graph, 0));
   c->graph_dirty = false;
+  c->graph_key = graph_key(c);
   c->graph_key_policy = c->policy;
   c->graph_key_thr = c->threshold;
   c->graph_key_cap = cap;
