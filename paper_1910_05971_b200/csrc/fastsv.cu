@@ -155,7 +155,8 @@ static constexpr long long kTierMax = (long long)FSV_TIER_MAX_M << 20;   // 8M: 
 #ifndef FSV_GRAPH_BODY
 #define FSV_GRAPH_BODY 2
 #endif
-static constexpr int kTraceCap = 4096;    // iteration cap of the counter array
+static constexpr int kTraceCap = 4096;
+static constexpr int kStageIters = 64;    // iterations whose trace comes back with the done flag    // iteration cap of the counter array
 
 struct fsv_ctx {
   int device = 0;
@@ -207,6 +208,12 @@ struct fsv_ctx {
   DBuf<unsigned int> ticket;
   DBuf<unsigned> partials;
   int* h_done = nullptr;  // pinned
+  // pinned staging of the per-iteration counters, product kinds and time
+  // stamps of the first kStageIters iterations, copied with the done flag so
+  // a graph-mode solve returns after a single host synchronisation
+  unsigned long long* h_stage_cnt = nullptr;
+  int* h_stage_mode = nullptr;
+  unsigned long long* h_stage_ts = nullptr;
   int64_t* h_off_pin = nullptr;   // pinned host copy of device-built row offsets
   // hooking variants (fsv_variants.cuh): row ids of the stored entries, two
   // extra vectors, and where the labels of the last solve live
@@ -274,7 +281,10 @@ extern "C" int fsv_create(int device, fsv_ctx** out) {
   c->device = device;
   cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device);
   if (cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking) != cudaSuccess ||
-      cudaMallocHost(&c->h_done, sizeof(int)) != cudaSuccess) {
+      cudaMallocHost(&c->h_done, sizeof(int)) != cudaSuccess ||
+      cudaMallocHost(&c->h_stage_cnt, sizeof(unsigned long long) * kStageIters * NCOUNT) != cudaSuccess ||
+      cudaMallocHost(&c->h_stage_mode, sizeof(int) * (kStageIters + 1)) != cudaSuccess ||
+      cudaMallocHost(&c->h_stage_ts, sizeof(unsigned long long) * (kStageIters + 1)) != cudaSuccess) {
     delete c;
     return fail(FSV_ERR_RUNTIME, "stream/pinned allocation failed");
   }
@@ -311,6 +321,9 @@ extern "C" int fsv_destroy(fsv_ctx* c) {
   if (c->graph) cudaGraphDestroy(c->graph);
   if (c->comm && g_nccl.CommDestroy) g_nccl.CommDestroy(c->comm);
   if (c->h_done) cudaFreeHost(c->h_done);
+  if (c->h_stage_cnt) cudaFreeHost(c->h_stage_cnt);
+  if (c->h_stage_mode) cudaFreeHost(c->h_stage_mode);
+  if (c->h_stage_ts) cudaFreeHost(c->h_stage_ts);
   if (c->h_off_pin) cudaFreeHost(c->h_off_pin);
   for (auto e : c->chunk_ev) cudaEventDestroy(e);
   if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
@@ -1828,9 +1841,21 @@ static int solve_body(fsv_ctx* c, const fsv_config* cfg, int32_t* snapshots, int
   }
   int launched = 1;  // iterations queued so far (k_first is iteration 1)
   int done = 0;
+  int staged = 0;    // iterations whose counters/kinds/stamps are already on the host
   if (graph_mode) {
     CUDA_TRY(cudaGraphLaunch(c->graph_exec, st));
+    // end of the device work (events[2] is free in graph mode: iterations
+    // >= 2 are timed by %globaltimer stamps)
+    if ((rc = ensure_events(c, 3))) return rc;
+    CUDA_TRY(cudaEventRecord(c->events[2], st));
     CUDA_TRY(cudaMemcpyAsync(c->h_done, c->done.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+    const int stage = std::min(cap, kStageIters);
+    CUDA_TRY(cudaMemcpyAsync(c->h_stage_cnt, c->cnt.p, sizeof(unsigned long long) * stage * NCOUNT,
+                             cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaMemcpyAsync(c->h_stage_mode, c->mode.p, sizeof(int) * (stage + 1), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaMemcpyAsync(c->h_stage_ts, c->tstamp.p, sizeof(unsigned long long) * (stage + 1),
+                             cudaMemcpyDeviceToHost, st));
+    staged = stage;
     CUDA_TRY(cudaStreamSynchronize(st));
     ++c->host_syncs;
     done = *c->h_done;
@@ -1843,8 +1868,7 @@ static int solve_body(fsv_ctx* c, const fsv_config* cfg, int32_t* snapshots, int
       const int passes = std::max(1, (it - 1 + FSV_GRAPH_BODY - 1) / FSV_GRAPH_BODY);
       c->launches += (FSV_GRAPH_IF ? std::max(1, it - 1) : passes * FSV_GRAPH_BODY) * per_it;
     }
-    if (done > 0 && (rc = ensure_events(c, (size_t)done + 1))) return rc;
-    if (done > 0) CUDA_TRY(cudaEventRecord(c->events[done], st));
+
   }
   bool first_round = true;
   while (!graph_mode) {
@@ -1873,24 +1897,28 @@ static int solve_body(fsv_ctx* c, const fsv_config* cfg, int32_t* snapshots, int
     if (launched >= cap)
       return fail(FSV_ERR_RUNTIME, "did not converge within %d iterations", cap);
   }
-  CUDA_TRY(cudaStreamSynchronize(st));
+  if (!staged) CUDA_TRY(cudaStreamSynchronize(st));   // (graph mode synchronised above)
   CUDA_TRY(cudaGetLastError());
   if (done < 0) return fail(FSV_ERR_RUNTIME, "did not converge within %d iterations", -done);
   const int iters = done;
   c->iterations = iters;
   c->h_cnt.assign((size_t)iters * NCOUNT, 0ull);
-  CUDA_TRY(cudaMemcpy(c->h_cnt.data(), c->cnt.p, sizeof(unsigned long long) * iters * NCOUNT,
-                      cudaMemcpyDeviceToHost));
   c->h_mode.assign((size_t)iters + 1, 0);
-  CUDA_TRY(cudaMemcpy(c->h_mode.data(), c->mode.p, sizeof(int) * (iters + 1), cudaMemcpyDeviceToHost));
-  c->iter_ms.assign(iters, 0.f);
-  {
-    std::vector<unsigned long long> ts((size_t)iters + 1, 0ull);
+  std::vector<unsigned long long> ts((size_t)iters + 1, 0ull);
+  if (iters <= staged) {
+    std::copy(c->h_stage_cnt, c->h_stage_cnt + (size_t)iters * NCOUNT, c->h_cnt.begin());
+    std::copy(c->h_stage_mode, c->h_stage_mode + iters + 1, c->h_mode.begin());
+    std::copy(c->h_stage_ts, c->h_stage_ts + iters + 1, ts.begin());
+  } else {
+    CUDA_TRY(cudaMemcpy(c->h_cnt.data(), c->cnt.p, sizeof(unsigned long long) * iters * NCOUNT,
+                        cudaMemcpyDeviceToHost));
+    CUDA_TRY(cudaMemcpy(c->h_mode.data(), c->mode.p, sizeof(int) * (iters + 1), cudaMemcpyDeviceToHost));
     CUDA_TRY(cudaMemcpy(ts.data(), c->tstamp.p, sizeof(unsigned long long) * (iters + 1),
                         cudaMemcpyDeviceToHost));
-    for (int k = 1; k <= iters; ++k) c->iter_ms[k - 1] = (float)((double)(ts[k] - ts[k - 1]) * 1e-6);
   }
-  CUDA_TRY(cudaEventElapsedTime(&c->solve_ms, c->events[0], c->events[iters]));
+  c->iter_ms.assign(iters, 0.f);
+  for (int k = 1; k <= iters; ++k) c->iter_ms[k - 1] = (float)((double)(ts[k] - ts[k - 1]) * 1e-6);
+  CUDA_TRY(cudaEventElapsedTime(&c->solve_ms, c->events[0], c->events[graph_mode ? 2 : iters]));
   if (c->profile) {
     auto span = [&](int k, int a, int b) {
       float ms = 0.f;
