@@ -2,7 +2,7 @@
 // cores: nothing on this path is a dense contraction.
 //
 // One FastSV iteration k (all flags; algorithms.py:79-91 == driver.py:81-117)
-// maps onto three launches over buffers F = f_k, G = gf_k, N = f_{k+1}
+// maps onto two launches over buffers F = f_k, G = gf_k, N = f_{k+1}
 // (pre-initialised to gf_k, which folds the shortcut f <-min gf, E1):
 //
 //   k_hook      edge-parallel over the oriented layout (each undirected edge
@@ -11,15 +11,17 @@
 //               column side gf[u]       -> N[v], N[F[v]]  (same rules, v <- u)
 //               gf of the top-H degree vertices ("hubs") is read from shared
 //               memory; column-side writes aimed at hubs are min-reduced into
-//               a compact hub accumulator instead of random N atomics.
-//   k_hubfix    applies the hub accumulator (hub_acc[slot] -> N[h], N[F[h]]).
+//               a compact hub accumulator instead of random N atomics, which
+//               the same launch applies after a grid barrier (hub fix-up;
+//               k_hubfix when built with FSV_FUSE_HUBFIX=0). A sparse
+//               iteration takes the push branch of the same kernel.
 //   k_shortcut  vertex-parallel: gf_{k+1} = N[N], change counters, star and
 //               monotonicity checks, next N init, hub gf refresh, and the
 //               device-side convergence flag (last-block ticket).
 //
 // Iteration 1 is closed-form (F = G = id): f_1[u] = min(u, min neighbour id),
-// precomputed at upload from the sorted CSR rows, so k_first does iteration 1
-// including its shortcut phase in one vertex-parallel pass.
+// computed by every solve from the sorted CSR rows (k_f1_solve), so k_first
+// does iteration 1 including its shortcut phase in one vertex-parallel pass.
 //
 // Writes into N are min-atomics filtered by the read-only gf_k: N[x] <= gf_k[x]
 // always and gf_k[F[x]] <= gf_k[x], so val >= gf_k[x] makes both hooks
@@ -687,7 +689,7 @@ __global__ void __launch_bounds__(HOOK_THREADS, 1) k_hook(HookArgs a) {
       // Entries that differ from their row's gf, as per-entry records
       // (target, value): val < gf(row) is a row-side contribution to the row
       // vertex, val > gf(row) a column-side one to the neighbour (or its hub
-      // slot). The first REC of a lane are kept in registers.
+      // slot). At most FSV_REC records per lane are kept in registers.
       // (skipped while the warp is in dense mode: the last scan step had
       // emissions on most lanes, so the next one almost surely needs the scan)
       int nrec = 0;
