@@ -1056,7 +1056,10 @@ __device__ __forceinline__ void tail_append(long long n4, long long n, Fn&& one,
   wo += __popc(b);
 }
 
-__global__ void __launch_bounds__(SC_THREADS) k_shortcut(ShortcutArgs a) {
+#ifndef FSV_SC_MINB
+#define FSV_SC_MINB 2
+#endif
+__global__ void __launch_bounds__(SC_THREADS, FSV_SC_MINB) k_shortcut(ShortcutArgs a) {
   if (converged_exit(a.done, a.lc)) return;
   if (a.lc.graph == 1) {
     a.iter = loop_iter(a.lc, a.iter);
