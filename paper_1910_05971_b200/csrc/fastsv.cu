@@ -155,8 +155,7 @@ static constexpr long long kTierMax = (long long)FSV_TIER_MAX_M << 20;   // 8M: 
 #ifndef FSV_GRAPH_BODY
 #define FSV_GRAPH_BODY 2
 #endif
-static constexpr int kTraceCap = 4096;
-static constexpr int kStageIters = 64;    // iterations whose trace comes back with the done flag    // iteration cap of the counter array
+static constexpr int kTraceCap = 4096;    // iteration cap of the counter array
 
 struct fsv_ctx {
   int device = 0;
@@ -208,12 +207,10 @@ struct fsv_ctx {
   DBuf<unsigned int> ticket;
   DBuf<unsigned> partials;
   int* h_done = nullptr;  // pinned
-  // pinned staging of the per-iteration counters, product kinds and time
-  // stamps of the first kStageIters iterations, copied with the done flag so
-  // a graph-mode solve returns after a single host synchronisation
-  unsigned long long* h_stage_cnt = nullptr;
-  int* h_stage_mode = nullptr;
-  unsigned long long* h_stage_ts = nullptr;
+  // graph mode: the final iteration packs the done flag and the trace of the
+  // first STAGE_ITERS iterations into one report; one copy brings it back
+  DBuf<SolveReport> rep;
+  SolveReport* h_rep = nullptr;   // pinned
   int64_t* h_off_pin = nullptr;   // pinned host copy of device-built row offsets
   // hooking variants (fsv_variants.cuh): row ids of the stored entries, two
   // extra vectors, and where the labels of the last solve live
@@ -282,9 +279,8 @@ extern "C" int fsv_create(int device, fsv_ctx** out) {
   cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device);
   if (cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking) != cudaSuccess ||
       cudaMallocHost(&c->h_done, sizeof(int)) != cudaSuccess ||
-      cudaMallocHost(&c->h_stage_cnt, sizeof(unsigned long long) * kStageIters * NCOUNT) != cudaSuccess ||
-      cudaMallocHost(&c->h_stage_mode, sizeof(int) * (kStageIters + 1)) != cudaSuccess ||
-      cudaMallocHost(&c->h_stage_ts, sizeof(unsigned long long) * (kStageIters + 1)) != cudaSuccess) {
+      cudaMallocHost(&c->h_rep, sizeof(SolveReport)) != cudaSuccess ||
+      c->rep.alloc(1) != cudaSuccess) {
     delete c;
     return fail(FSV_ERR_RUNTIME, "stream/pinned allocation failed");
   }
@@ -321,9 +317,7 @@ extern "C" int fsv_destroy(fsv_ctx* c) {
   if (c->graph) cudaGraphDestroy(c->graph);
   if (c->comm && g_nccl.CommDestroy) g_nccl.CommDestroy(c->comm);
   if (c->h_done) cudaFreeHost(c->h_done);
-  if (c->h_stage_cnt) cudaFreeHost(c->h_stage_cnt);
-  if (c->h_stage_mode) cudaFreeHost(c->h_stage_mode);
-  if (c->h_stage_ts) cudaFreeHost(c->h_stage_ts);
+  if (c->h_rep) cudaFreeHost(c->h_rep);
   if (c->h_off_pin) cudaFreeHost(c->h_off_pin);
   for (auto e : c->chunk_ev) cudaEventDestroy(e);
   if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
@@ -1437,6 +1431,8 @@ static LoopCtl loop_ctl(fsv_ctx* c, int graph) {
   l.tstamp = c->tstamp.p;
   l.cond = (unsigned long long)c->graph_cond;
   l.cond_next = (graph && c->graph_half2) ? (unsigned long long)c->graph_cond_next : 0ull;
+  l.rep = graph ? c->rep.p : nullptr;
+  l.mode_base = c->mode.p;
   l.graph = graph;
   l.X = c->X;
   l.Y = c->Y;
@@ -1799,7 +1795,7 @@ static int solve_body(fsv_ctx* c, const fsv_config* cfg, int32_t* snapshots, int
   CUDA_TRY(cudaEventRecord(c->events[0], st));
   k_solve_init<<<grid_for(c, std::max<long long>(c->HT, (long long)cap * NCOUNT), 256), 256, 0, st>>>(
       c->X, c->Y, c->G, c->n, c->hacc, c->HT, c->cnt.p, (long long)cap * NCOUNT, c->done.p,
-      c->ticket.p, c->mode.p, c->policy == 2 ? 1 : 0, c->tstamp.p);
+      c->ticket.p, c->mode.p, c->policy == 2 ? 1 : 0, c->tstamp.p, c->rep.p);
   pmark(c, 1, 6);
   // iteration 1 in closed form: f_1[u] = min(u, smallest neighbour) from the
   // resident CSR rows (first column of each sorted row), every solve
@@ -1848,17 +1844,11 @@ static int solve_body(fsv_ctx* c, const fsv_config* cfg, int32_t* snapshots, int
     // >= 2 are timed by %globaltimer stamps)
     if ((rc = ensure_events(c, 3))) return rc;
     CUDA_TRY(cudaEventRecord(c->events[2], st));
-    CUDA_TRY(cudaMemcpyAsync(c->h_done, c->done.p, sizeof(int), cudaMemcpyDeviceToHost, st));
-    const int stage = std::min(cap, kStageIters);
-    CUDA_TRY(cudaMemcpyAsync(c->h_stage_cnt, c->cnt.p, sizeof(unsigned long long) * stage * NCOUNT,
-                             cudaMemcpyDeviceToHost, st));
-    CUDA_TRY(cudaMemcpyAsync(c->h_stage_mode, c->mode.p, sizeof(int) * (stage + 1), cudaMemcpyDeviceToHost, st));
-    CUDA_TRY(cudaMemcpyAsync(c->h_stage_ts, c->tstamp.p, sizeof(unsigned long long) * (stage + 1),
-                             cudaMemcpyDeviceToHost, st));
-    staged = stage;
+    CUDA_TRY(cudaMemcpyAsync(c->h_rep, c->rep.p, sizeof(SolveReport), cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaStreamSynchronize(st));
     ++c->host_syncs;
-    done = *c->h_done;
+    done = c->h_rep->done;
+    staged = c->h_rep->iters;   // 0: more than STAGE_ITERS iterations, copied below
     if (done == 0) return fail(FSV_ERR_RUNTIME, "graph loop ended without convergence");
     {
       // kernels the graph ran: iterations 2..it, rounded up to whole body
@@ -1897,7 +1887,7 @@ static int solve_body(fsv_ctx* c, const fsv_config* cfg, int32_t* snapshots, int
     if (launched >= cap)
       return fail(FSV_ERR_RUNTIME, "did not converge within %d iterations", cap);
   }
-  if (!staged) CUDA_TRY(cudaStreamSynchronize(st));   // (graph mode synchronised above)
+  if (!graph_mode) CUDA_TRY(cudaStreamSynchronize(st));   // (graph mode synchronised above)
   CUDA_TRY(cudaGetLastError());
   if (done < 0) return fail(FSV_ERR_RUNTIME, "did not converge within %d iterations", -done);
   const int iters = done;
@@ -1905,10 +1895,10 @@ static int solve_body(fsv_ctx* c, const fsv_config* cfg, int32_t* snapshots, int
   c->h_cnt.assign((size_t)iters * NCOUNT, 0ull);
   c->h_mode.assign((size_t)iters + 1, 0);
   std::vector<unsigned long long> ts((size_t)iters + 1, 0ull);
-  if (iters <= staged) {
-    std::copy(c->h_stage_cnt, c->h_stage_cnt + (size_t)iters * NCOUNT, c->h_cnt.begin());
-    std::copy(c->h_stage_mode, c->h_stage_mode + iters + 1, c->h_mode.begin());
-    std::copy(c->h_stage_ts, c->h_stage_ts + iters + 1, ts.begin());
+  if (graph_mode && iters <= staged) {
+    std::copy(c->h_rep->cnt, c->h_rep->cnt + (size_t)iters * NCOUNT, c->h_cnt.begin());
+    std::copy(c->h_rep->mode, c->h_rep->mode + iters + 1, c->h_mode.begin());
+    std::copy(c->h_rep->ts, c->h_rep->ts + iters + 1, ts.begin());
   } else {
     CUDA_TRY(cudaMemcpy(c->h_cnt.data(), c->cnt.p, sizeof(unsigned long long) * iters * NCOUNT,
                         cudaMemcpyDeviceToHost));

@@ -178,6 +178,19 @@ __host__ __device__ __forceinline__ long long acc_len(long long slots) {
 
 // ---- argument blocks --------------------------------------------------------
 
+// Report of a graph-mode solve, packed on the device by the last block of
+// the final iteration (trace of the first STAGE_ITERS iterations, done flag)
+// so the host fetches it with one copy.
+constexpr int STAGE_ITERS = 64;
+static_assert(NCOUNT == 16, "SolveReport holds 16 counters per iteration");
+struct SolveReport {
+  int done;                                        // iteration (>0 converged, <0 cap reached)
+  int iters;                                       // iterations staged below (0: more than STAGE_ITERS)
+  unsigned long long cnt[STAGE_ITERS * 16];        // NCOUNT counters per iteration
+  int mode[STAGE_ITERS + 2];
+  unsigned long long ts[STAGE_ITERS + 2];
+};
+
 // Device-side loop control. Graph mode runs the iteration loop inside a
 // CUDA-graph conditional WHILE node: kernels read the iteration number from
 // *iterp, the vertex pass's last block advances it and sets the condition.
@@ -187,6 +200,8 @@ struct LoopCtl {
   unsigned long long* tstamp;        // per-iteration end time (%globaltimer, ns)
   unsigned long long cond;           // cudaGraphConditionalHandle of the WHILE loop
   unsigned long long cond_next;      // IF handle guarding the body's next iteration (0: none)
+  SolveReport* rep;                  // graph mode: the solve's report (device memory) or null
+  int* mode_base;                    // mode[] of the whole solve (for the report)
   int graph;                         // 0 host loop, 1 inside the graph, 2 k_first before it
   int* X;                            // graph mode: the two rotating parent buffers; iteration k
   int* Y;                            // reads F = f_{k-1} and writes N = f_k by its parity
@@ -967,6 +982,7 @@ __device__ __forceinline__ void finish_counters(const unsigned (&c)[5], unsigned
     if (lane == 0) s_acc[w][k] = v;
   }
   __syncthreads();
+  __shared__ int s_stop;
   if (threadIdx.x < 5) {
     unsigned long long sum = 0;
     for (int i = 0; i < NT / 32; ++i) sum += s_acc[i][threadIdx.x];
@@ -976,6 +992,7 @@ __device__ __forceinline__ void finish_counters(const unsigned (&c)[5], unsigned
       if (sum == 0ull) atomicExch(done, iter);
       else if (max_iter > 0 && iter >= max_iter) atomicExch(done, -iter);
       else stop = false;
+      s_stop = stop ? (sum == 0ull ? iter : -iter) : 0;
       lc.tstamp[iter] = global_ns();
       if (lc.graph) *lc.iterp = iter + 1;                       // 2: iteration 1 before the graph
       if (lc.graph == 1) {
@@ -990,6 +1007,24 @@ __device__ __forceinline__ void finish_counters(const unsigned (&c)[5], unsigned
     }
   }
   if (threadIdx.x == 0) *ticket = 0u;
+  if (lc.rep) {
+    // the final iteration packs the solve's report for a single host copy
+    __syncthreads();
+    const int fin = s_stop;
+    if (fin) {
+      const int it = fin > 0 ? fin : -fin;
+      const int k = it <= STAGE_ITERS ? it : 0;
+      for (int i = threadIdx.x; i < k * NCOUNT; i += NT) lc.rep->cnt[i] = __ldcg(lc.cnt_base + i);
+      if (k)
+        for (int i = threadIdx.x; i <= k + 1; i += NT) lc.rep->mode[i] = __ldcg(lc.mode_base + i);
+      if (k)
+        for (int i = threadIdx.x; i <= k; i += NT) lc.rep->ts[i] = __ldcg(lc.tstamp + i);
+      if (threadIdx.x == 0) {
+        lc.rep->iters = k;
+        lc.rep->done = fin;
+      }
+    }
+  }
 }
 
 // ---- phase G: grandparents, counters, next N init ---------------------------
@@ -1177,7 +1212,7 @@ __global__ void __launch_bounds__(SC_THREADS) k_first(FirstArgs a) {
 // ---- solve-start initialisation ----------------------------------------------
 __global__ void k_solve_init(int* X, int* Y, int* G, long long n, int* hub_acc, int H,
                              unsigned long long* cnt, long long ncnt, int* done, unsigned* ticket,
-                             int* mode, int first_mode, unsigned long long* tstamp) {
+                             int* mode, int first_mode, unsigned long long* tstamp, SolveReport* rep) {
   const long long t0 = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const long long stride = (long long)gridDim.x * blockDim.x;
   for (long long s = t0; s < H; s += stride) hub_acc[acc_at(s)] = INF;
@@ -1187,6 +1222,7 @@ __global__ void k_solve_init(int* X, int* Y, int* G, long long n, int* hub_acc, 
     *done = 0; *ticket = 0u;
     mode[1] = first_mode;
     tstamp[0] = global_ns();
+    if (rep) { rep->done = 0; rep->iters = 0; }
   }
 }
 
