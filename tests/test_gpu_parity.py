@@ -449,3 +449,21 @@ def test_bounds_checked_build_runs_clean():
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
     assert "mismatches: 0" in r.stdout, r.stdout[-2000:]
+
+
+def test_graph_reuse_across_uploads_of_the_same_shape(solver):
+    """Re-uploads that keep every captured buffer and size keep the
+    instantiated iteration graph: alternating a graph and a relabelled copy
+    of it (same sizes, different contents) must still give each one's own
+    oracle result."""
+    n, e = gen.rmat(14, 16, seed=91)
+    perm = np.random.default_rng(92).permutation(n).astype(np.int32)
+    graphs = [fb.build_csr(n, e), fb.build_csr(n, perm[e])]
+    oracles = [oracle.fastsv_csr(n, g.row_offsets, g.col_indices) for g in graphs]
+    solver.set_hub_slots(0)
+    for rep in range(3):
+        for g, o in zip(graphs, oracles):
+            solver.upload(g)
+            labels, iters, gfc, fc, ms, _ = solver.run()
+            assert iters == o.iterations and gfc.tolist() == o.gf_changed.tolist(), rep
+            assert np.array_equal(labels, o.labels), rep
