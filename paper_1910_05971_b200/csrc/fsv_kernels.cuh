@@ -65,7 +65,7 @@ constexpr int STEP = 32 * EPL;           // entries per warp step
 constexpr int STEPS = FSV_STEPS;         // steps per span
 constexpr int SPAN = STEP * STEPS;       // entries per warp task
 constexpr int HOOK_THREADS = FSV_HOOK_THREADS;
-constexpr int PUSH_SCRATCH_BYTES = HOOK_THREADS * 20;  // s_start, s_excl (8 B) + s_val (4 B)
+constexpr int PUSH_SCRATCH_BYTES = HOOK_THREADS * 36;  // s_start, s_excl (8 B), s_val (4 B), s_list (16 B)
 // Column-side minima aimed at the HOT_ACC most connected hubs are combined in
 // shared memory per CTA and flushed once at the end: a top hub can be the
 // target of ~1e5 reductions per iteration, which would otherwise serialise
@@ -346,6 +346,11 @@ __device__ __forceinline__ void emit_row(int u, int gu, int val, const int* __re
 // graphs, where the dense iterations have most entries differing).
 // Dense task loop: the last FSV_DYN_TAIL rounds of tasks are handed out by
 // an atomic counter (0: fully static round-robin).
+// Changed-vertex lists of the vertex passes hold 4-vertex groups with a
+// change mask (one ballot per group); the push expands them.
+#ifndef FSV_DELTA_GROUPS
+#define FSV_DELTA_GROUPS 1
+#endif
 #ifndef FSV_DYN_TAIL
 #define FSV_DYN_TAIL 2
 #endif
@@ -453,15 +458,40 @@ __device__ __forceinline__ void push_entries(const int (&u)[PER], const int (&va
 
 // Phase A. w_start/w_excl/w_val: this warp's shared scratch (32 entries each).
 __device__ __forceinline__ void push_local(const PushArgs& a, long long* w_start, long long* w_excl,
-                                           int* w_val) {
+                                           int* w_val, int* w_list) {
   const int lane = threadIdx.x & 31;
   const long long nw = (long long)gridDim.x * (blockDim.x >> 5);
   constexpr int PER = PUSH_CHUNK / 32;
   unsigned long long work = 0;
   for (long long r = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < a.nregions;
        r += nw) {
+#if FSV_DELTA_GROUPS
+    // expand 32 group entries at a time into this warp's vertex list (<= 128)
+    const int gcnt = a.count[r];
+    const int* greg = a.list + r * a.rcap;
+    for (int gb = 0; gb < gcnt; gb += 32) {
+    const unsigned e = gb + lane < gcnt ? (unsigned)greg[gb + lane] : 0u;
+    const int nv = __popc(e & 15u);
+    int vincl = nv;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, vincl, o);
+      if (lane >= o) vincl += y;
+    }
+    const int cnt = __shfl_sync(0xffffffffu, vincl, 31);
+    {
+      int k = vincl - nv;
+      const int v0 = (int)((e >> 4) << 2);
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if ((e >> j) & 1u) w_list[k++] = v0 + j;
+    }
+    __syncwarp();
+    const int* reg = w_list;
+#else
     const int cnt = a.count[r];
     const int* reg = a.list + r * a.rcap;
+#endif
     for (int b = 0; b < cnt; b += 32) {
       long long deg = 0, start = 0;
       int gv = INF;
@@ -527,6 +557,10 @@ __device__ __forceinline__ void push_local(const PushArgs& a, long long* w_start
       }
       __syncwarp();
     }
+#if FSV_DELTA_GROUPS
+    __syncwarp();
+    }
+#endif
   }
 #pragma unroll
   for (int o = 16; o; o >>= 1) work += __shfl_xor_sync(0xffffffffu, work, o);
@@ -616,9 +650,10 @@ __global__ void __launch_bounds__(HOOK_THREADS, 1) k_hook(HookArgs a) {
     long long* s_start = reinterpret_cast<long long*>(s_hub);
     long long* s_excl = s_start + HOOK_THREADS;
     int* s_val = reinterpret_cast<int*>(s_excl + HOOK_THREADS);
+    int* s_list = s_val + HOOK_THREADS;            // 128 expanded vertices per warp
     const int wib = threadIdx.x >> 5;
     DBG_T(0);
-    push_local(a.push, s_start + wib * 32, s_excl + wib * 32, s_val + wib * 32);
+    push_local(a.push, s_start + wib * 32, s_excl + wib * 32, s_val + wib * 32, s_list + wib * 128);
     // grid barrier: every CTA is resident (one persistent CTA per SM)
     __syncthreads();
     DBG_T(1);
@@ -1030,6 +1065,18 @@ __device__ __forceinline__ void finish_counters(const unsigned (&c)[5], unsigned
 // ---- phase G: grandparents, counters, next N init ---------------------------
 
 // Append the vertices u0+j (j < 4, bit j of m4) to this warp's delta region.
+#if FSV_DELTA_GROUPS
+// Delta entries are 4-vertex groups: (u0/4) << 4 | bit mask of the changed
+// vertices among u0..u0+3 (one ballot per group instead of one per vertex);
+// the push expands them.
+__device__ __forceinline__ void delta_append(unsigned m4, int u0, int* region, int& wo) {
+  const unsigned lt = (1u << (threadIdx.x & 31)) - 1u;
+  const bool on = m4 != 0u;
+  const unsigned b = __ballot_sync(0xffffffffu, on);
+  if (on) region[wo + __popc(b & lt)] = (int)((((unsigned)u0 >> 2) << 4) | m4);
+  wo += __popc(b);
+}
+#else
 __device__ __forceinline__ void delta_append(unsigned m4, int u0, int* region, int& wo) {
   const unsigned lt = (1u << (threadIdx.x & 31)) - 1u;
 #pragma unroll
@@ -1040,6 +1087,7 @@ __device__ __forceinline__ void delta_append(unsigned m4, int u0, int* region, i
     wo += __popc(b);
   }
 }
+#endif
 
 // Vertex pass of iteration k >= 2 over groups of 4 consecutive vertices
 // (int4 index i): gf' = N[N], counters, next N init, delta append. Loads of
@@ -1087,8 +1135,14 @@ __device__ __forceinline__ void tail_append(long long n4, long long n, Fn&& one,
   const long long u = (n4 << 2) + (threadIdx.x & 31);
   const bool ch = (u < n) ? one(u) : false;
   const unsigned b = __ballot_sync(0xffffffffu, ch);
+#if FSV_DELTA_GROUPS
+  // the tail (< 4 vertices) is group n4; lanes 0..2 hold its vertices
+  if ((threadIdx.x & 31) == 0 && b) region[wo] = (int)(((unsigned)n4 << 4) | (b & 15u));
+  wo += b ? 1 : 0;
+#else
   if (ch) region[wo + __popc(b & ((1u << (threadIdx.x & 31)) - 1u))] = (int)u;
   wo += __popc(b);
+#endif
 }
 
 #ifndef FSV_SC_MINB
