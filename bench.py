@@ -3,15 +3,22 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2] [--impl ours|reference]
 
 A step = one full FastSV solve (iteration 1 .. convergence) of the config's
-graph, device-resident CSR layout in HBM when the timed region starts.
+graph, the device layout resident in HBM when the timed region starts.
 `value` = |E| / mean step time (|E| = undirected input edges as generated).
-`e2e` = the same metric through the public C-ABI path with host buffers:
-pinned CSR -> fsv_upload_csr (H2D + layout build) -> solve -> labels D2H.
+Beside it: `layout` (device-resident CSR -> oriented layout, and the one-shot
+CSR-resident -> labels throughput), `e2e` (pinned host CSR -> fsv_upload_csr
+-> solve -> labels D2H through the C ABI) and `api` (the public drop-in
+fastsv_la(g) on pageable numpy arrays, wall clock, RunResult with Labeling).
 
-N > 1 (torchrun): 1D row partition balanced by entries, per-iteration NCCL
-allreduce-min of the next-parent vector inside the library; step time is the
-max over ranks.  --impl reference: the reference's own CPU algorithm (numpy
-port of svcc.fastsv_la, oracle/port.py) on the host cores, rank 0 only.
+N > 1: one rank per GPU (torchrun; `--gpus N` without torchrun re-launches
+itself under torch.distributed.run), 1D row partition balanced by entries,
+per-iteration NCCL allreduce-min of the next-parent vector inside the
+library; step time is the max over ranks.
+
+--impl reference: the UNMODIFIED reference `svcc` (installed into
+baseline/_ref) runs svcc.fastsv_la(g, DriverConfig(workers=cores)) on the
+host cores, rank 0 only, on the same graph regenerated in pure numpy
+(baseline/ref_inputs.py) so no library of this repo is mapped into it.
 """
 
 from __future__ import annotations
@@ -138,57 +145,129 @@ def bytes_model(g):
     return hook, it
 
 
+def _import_svcc():
+    """The reference package from baseline/_ref (pip --target install), or None."""
+    ref = ROOT / "baseline" / "_ref"
+    if (ref / "svcc").is_dir() and str(ref) not in sys.path:
+        sys.path.insert(0, str(ref))
+    try:
+        import svcc  # noqa: F401
+        return svcc
+    except ImportError:
+        return None
+
+
 def run_reference(args, world, rank):
-    """CPU reference arm: numpy port of svcc.fastsv_la on all host cores."""
+    """CPU reference arm: the unmodified svcc.fastsv_la on all host cores."""
     if rank != 0:
         return
-    from oracle import port
     cores = len(os.sched_getaffinity(0))
-    n, pairs, g = make_graph(args.config, args.scale)
-    pg = port.PortGraph(n, g.row_offsets, g.col_indices)
+    from baseline import ref_inputs
+    t0 = time.perf_counter()
+    if args.scale is not None and args.config in (2, 5):
+        n, pairs = ref_inputs.rmat(args.scale, 16, seed=0)
+    else:
+        n, pairs = ref_inputs.baseline_graph(args.config)
+    off, cols = ref_inputs.csr(n, pairs)
+    prep_s = time.perf_counter() - t0
+    edges = int(pairs.shape[0])
+    del pairs
+    svcc = _import_svcc()
+    if svcc is not None:
+        off.flags.writeable = False
+        cols.flags.writeable = False
+        g = svcc.CsrGraph(n=n, row_offsets=off, col_indices=cols)
+        cfg = svcc.DriverConfig(workers=cores)
+
+        def step():
+            r = svcc.fastsv_la(g, cfg)
+            return r.iterations
+        kind, what = "reference", f"svcc.fastsv_la(g, DriverConfig(workers={cores})) from baseline/_ref"
+    else:
+        from oracle import port   # numpy restatement, used only when svcc is not installed
+        pg = port.PortGraph(n, off, cols)
+
+        def step():
+            return port.fastsv_la(pg, workers=cores)[1]
+        kind, what = "port", f"numpy port of svcc.fastsv_la (oracle/port.py), workers={cores}"
     for _ in range(args.warmup):
-        port.fastsv_la(pg, workers=cores)
+        iters = step()
     times = []
     for _ in range(args.steps):
         t0 = time.perf_counter()
-        _, iters, _, _ = port.fastsv_la(pg, workers=cores)
+        iters = step()
         times.append(time.perf_counter() - t0)
-    step = sum(times) / len(times)
-    edges = int(pairs.shape[0])
-    val = edges / step
+    step_s = sum(times) / len(times)
+    val = edges / step_s
+    extra = {}
+    if svcc is not None and not args.no_cpu_baseline:
+        # the vertex-level twin, single-threaded (BASELINE.md §2)
+        t0 = time.perf_counter()
+        r = svcc.fastsv(g)
+        extra = {"svcc.fastsv_1thread_s": time.perf_counter() - t0, "svcc.fastsv_iterations": r.iterations}
     line = {
         "metric": "edges/sec to convergence (|E|/time)", "value": val, "unit": "edges/s",
         "impl": "reference", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": step * 1e3, "higher_is_better": True, "scaling": "strong",
+        "ms_per_step": step_s * 1e3, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "int64", "data": "synthetic (seeded generator, BASELINE config)",
         "config": {"workload": f"config{args.config} (BASELINE.json configs[{args.config - 1}])",
-                   "n": n, "edges": edges, "m_dir": g.m, "iterations": iters,
+                   "n": n, "edges": edges, "m_dir": int(off[-1]), "iterations": iters,
                    "parallelism": "host threads (reference CPU path)"},
-        "cpu_baseline": {"value": val, "unit": "edges/s", "cores": cores, "kind": "port",
-                         "sample": f"full solve of config {args.config} per step (numpy port of "
-                                   "svcc.fastsv_la, auto kernel choice, workers=cores)"},
+        "cpu_baseline": {"value": val, "unit": "edges/s", "cores": cores, "kind": kind,
+                         "sample": f"full solve of config {args.config} per step: {what}"},
         "e2e": {"value": val, "unit": "edges/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "input_prep_s": prep_s,
+        **extra,
     }
     print(json.dumps(line), flush=True)
 
 
 def cpu_baseline_sample(g, n_edges, budget_s=20.0):
-    """Bounded timing of the reference algorithm (numpy port) on this host."""
-    from oracle import port
+    """Bounded timing of the reference itself (svcc.fastsv_la from
+    baseline/_ref, all host cores) on this host; the numpy port stands in
+    only when the reference is not installed."""
     cores = len(os.sched_getaffinity(0))
-    pg = port.PortGraph(g.n, g.row_offsets, g.col_indices)
+    svcc = _import_svcc()
+    if svcc is not None:
+        off = np.ascontiguousarray(g.row_offsets, dtype=np.int64)
+        cols = np.ascontiguousarray(g.col_indices, dtype=np.int64)
+        rg = svcc.CsrGraph(n=g.n, row_offsets=off, col_indices=cols)
+        cfg = svcc.DriverConfig(workers=cores)
+        run = lambda: svcc.fastsv_la(rg, cfg)  # noqa: E731
+        kind, what = "reference", f"svcc.fastsv_la from baseline/_ref, workers={cores}"
+    else:
+        from oracle import port
+        pg = port.PortGraph(g.n, g.row_offsets, g.col_indices)
+        run = lambda: port.fastsv_la(pg, workers=cores)  # noqa: E731
+        kind, what = "port", f"numpy port of svcc.fastsv_la, workers={cores}"
     times = []
     t_start = time.perf_counter()
     while True:
         t0 = time.perf_counter()
-        port.fastsv_la(pg, workers=cores)
+        run()
         times.append(time.perf_counter() - t0)
         if time.perf_counter() - t_start > budget_s / 2 or len(times) >= 3:
             break
     best = min(times)
-    return {"value": n_edges / best, "unit": "edges/s", "cores": cores, "kind": "port",
-            "sample": f"{len(times)} full solve(s) of the same graph, best taken "
-                      f"({best:.2f} s each; numpy port of svcc.fastsv_la, workers={cores})"}
+    return {"value": n_edges / best, "unit": "edges/s", "cores": cores, "kind": kind,
+            "sample": f"{len(times)} full solve(s) of the same graph, best taken ({best:.2f} s each; {what})"}
+
+
+def spawn_ranks(args) -> int:
+    """`--gpus N` without torchrun: re-launch under torch.distributed.run with
+    one rank per GPU; refuse (non-zero exit) when fewer GPUs are visible."""
+    import socket
+    import torch
+    have = torch.cuda.device_count()
+    if have < args.gpus:
+        print(f"bench.py: --gpus {args.gpus} needs {args.gpus} visible GPUs, found {have}", file=sys.stderr)
+        return 2
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", str(Path(__file__).resolve()), *sys.argv[1:]]
+    return subprocess.call(cmd)
 
 
 def main():
@@ -206,8 +285,14 @@ def main():
     world, rank, local = dist_env()
 
     if args.impl == "reference":
-        run_reference(args, world, rank)
+        # CPU arm: rank 0 works, the other ranks exit without work
+        run_reference(args, max(world, args.gpus) if "WORLD_SIZE" not in os.environ else world, rank)
         return
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args))
+    if world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+        sys.exit(2)
 
     import torch
     import torch.distributed as dist
@@ -221,7 +306,11 @@ def main():
     n_edges = int(pairs.shape[0])
     del pairs
     solver = fb.Solver(local, hub_slots=args.hub_slots)
-    stream = torch.cuda.current_stream()
+    # one dedicated (non-default) stream for the solver, the L2 flush and the
+    # timing events: the legacy default stream is not ordered against the
+    # library's non-blocking stream, so flush/events/solve must share this one
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
     solver.set_stream(stream.cuda_stream)
     if world > 1:
         uid = [fb.Solver.nccl_unique_id() if rank == 0 else None]
@@ -280,7 +369,7 @@ def main():
     prof = []
     for _ in range(3):
         flush_l2()
-        prof.append(solver.solve(profile=True))
+        prof.append(fb.FsvStats.from_buffer_copy(solver.solve(profile=True)))   # solve() reuses one struct
     best = min(prof, key=lambda p: p.solve_ms)
     hook_ms = best.hook_ms                 # dense k_hook launches only
     hook_launches = best.hook_launches
@@ -322,6 +411,50 @@ def main():
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
     e2e_ms = float(te.item())
     assert np.array_equal(pin_lab.numpy(), labels), "e2e labels differ from resident-solve labels"
+
+    # ---- layout: device-resident CSR -> oriented layout (fsv_upload_csr_device)
+    # The CSR (the reference's input structure, graph.py:20-52) sits in HBM;
+    # the layout build reads it in place. One-shot throughput = |E| /
+    # (layout + solve): what a single solve of a freshly resident graph costs.
+    d_off_t = torch.from_numpy(offsets.copy()).to("cuda")
+    d_cols_t = torch.from_numpy(cols_slice.copy()).to("cuda")
+    lay_times, lay_solve = [], []
+    for i in range(max(3, min(args.steps, 6))):
+        barrier()
+        flush_l2()
+        a, b, c = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+        a.record(stream)
+        solver.upload_device(n, d_off_t.data_ptr(), d_cols_t.data_ptr(), lo, hi)
+        b.record(stream)
+        solver.solve()
+        c.record(stream)
+        torch.cuda.synchronize()
+        if i:
+            lay_times.append(a.elapsed_time(b))
+            lay_solve.append(b.elapsed_time(c))
+    layout_ms = sum(lay_times) / len(lay_times)
+    oneshot_ms = layout_ms + sum(lay_solve) / len(lay_solve)
+    tl = torch.tensor([layout_ms, oneshot_ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(tl, op=dist.ReduceOp.MAX)
+    layout_ms, oneshot_ms = (float(x) for x in tl.tolist())
+    assert np.array_equal(solver.labels(), labels), "device-CSR upload labels differ"
+
+    # ---- api: the public drop-in on pageable host arrays (wall clock) ----
+    api = None
+    if world == 1:
+        fb.fastsv_la(g, device=local)   # context creation + first upload
+        api_times = []
+        for _ in range(3):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            r = fb.fastsv_la(g, device=local)
+            api_times.append((time.perf_counter() - t0) * 1e3)
+        assert np.array_equal(r.labeling.labels, labels.astype(np.int64)), "api labels differ"
+        api = {"ms_per_call": min(api_times), "value": n_edges / (min(api_times) * 1e-3), "unit": "edges/s",
+               "call": "paper_1910_05971_b200.fastsv_la(g) -> RunResult (pageable numpy CsrGraph in, "
+                       "Labeling with sizes out; upload + layout + solve + trace + device Labeling)",
+               "components": r.labeling.component_count}
 
     if rank == 0:
         peak, peak_kind = load_peaks()
@@ -369,9 +502,27 @@ def main():
                     "path": "pinned host CSR -> fsv_upload_csr (H2D + layout build) -> fsv_solve -> fsv_get_labels",
                     "h2d_bytes_per_step": int(offsets.nbytes + cols_slice.nbytes),
                     "d2h_bytes_per_step": int(4 * n)},
+            "layout": {"ms": layout_ms,
+                       "path": "device CSR (int64 offsets, int32 columns in HBM) -> fsv_upload_csr_device "
+                               "(degree order, hub table, oriented layout) ",
+                       "oneshot_ms": oneshot_ms,
+                       "value_incl_layout": n_edges / (oneshot_ms * 1e-3)},
+            "api": api,
             "gpu_launches": launches,
             "clocks": clocks,
         }
+        if world > 1:
+            # NVLink roofline of the per-iteration allreduce-min (ring bus
+            # bytes per GPU) against the measured peer bandwidth
+            ar_launches = max(iters - 1, 1)
+            ar_ms = best.allreduce_ms / ar_launches if best.allreduce_ms else None
+            bus = 2 * (world - 1) / world * 4 * n
+            line["nvlink"] = {"collective": "ncclAllReduce(int32, min) of the next-parent vector",
+                              "bytes_per_iter_per_gpu": bus, "launches": ar_launches, "launch_ms": ar_ms,
+                              "achieved": (bus / (ar_ms * 1e-3) / 1e9) if ar_ms else None,
+                              "peak": 770.0, "unit": "GB/s",
+                              "peak_kind": "measured peer copy per direction (B200_PROFILING.md)",
+                              "frac": (bus / (ar_ms * 1e-3) / 1e9 / 770.0) if ar_ms else None}
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline_sample(g, n_edges)
         print(json.dumps(line), flush=True)

@@ -35,7 +35,7 @@ extern "C" {
 #define FSV_ERR_INVARIANT 3
 #define FSV_ERR_RUNTIME 4
 
-#define FSV_ABI_VERSION 2
+#define FSV_ABI_VERSION 3
 
 typedef struct fsv_ctx fsv_ctx;
 
@@ -114,6 +114,18 @@ int fsv_set_stream(fsv_ctx* ctx, void* cuda_stream);
 int fsv_upload_csr(fsv_ctx* ctx, int64_t n, const int64_t* row_offsets,
                    const int32_t* col_indices, int64_t row_begin, int64_t row_end);
 
+/*
+ * Same from DEVICE memory (a CsrGraph already resident in HBM, e.g. torch
+ * tensors): d_row_offsets holds the n+1 int64 offsets of the full graph,
+ * d_col_indices the int32 columns of rows [row_begin, row_end) (the slice
+ * starting at row_offsets[row_begin]). Both arrays are BORROWED: the context
+ * reads them in place (sparse iterations and f_1 read the symmetric CSR) and
+ * they must stay valid and unchanged until the next upload or fsv_destroy.
+ * Only the layout is built; nothing is copied.
+ */
+int fsv_upload_csr_device(fsv_ctx* ctx, int64_t n, const int64_t* d_row_offsets,
+                          const int32_t* d_col_indices, int64_t row_begin, int64_t row_end);
+
 /* Same with int64 column ids (the reference's ID_DTYPE, graph.py:15-17). */
 int fsv_upload_csr64(fsv_ctx* ctx, int64_t n, const int64_t* row_offsets,
                      const int64_t* col_indices, int64_t row_begin, int64_t row_end);
@@ -158,6 +170,18 @@ int fsv_get_trace(fsv_ctx* ctx, int64_t* gf_changed, int64_t* f_changed,
 int fsv_get_trace_ex(fsv_ctx* ctx, int64_t* gf_changed, int64_t* f_changed,
                      float* elapsed_ms, int32_t* kernel, int64_t* flops, int32_t cap);
 
+/* The Labeling of the last solve, computed on the device (the reference's
+ * labeling_from_parents, graph.py:109-125; the star check already ran in
+ * the final vertex pass and failed the solve with FSV_ERR_INVARIANT):
+ *   labels: n int64 (the reference's ID_DTYPE), or NULL
+ *   reps, sizes: the component representatives in ascending order (the
+ *           minimum id of each component) and their vertex counts, `cap`
+ *           entries each, or NULL
+ *   count:  receives the component count (Labeling.component_count).
+ * Call with reps = sizes = NULL first to size the buffers. */
+int fsv_get_labeling(fsv_ctx* ctx, int64_t* labels, int64_t* reps, int64_t* sizes, int64_t cap,
+                     int64_t* count);
+
 /* One call: solve + labels + iteration count + trace (the fastsv_la shape). */
 int fsv_run(fsv_ctx* ctx, const fsv_config* cfg, int32_t* labels,
             int32_t* iterations, int64_t* gf_changed, int64_t* f_changed,
@@ -177,6 +201,23 @@ int fsv_nccl_unique_id(void* id128);
 /* Attach a communicator; per iteration the next-parent vector is merged with
  * ncclAllReduce(ncclInt32, ncclMin) after the hooking phase. */
 int fsv_nccl_attach(fsv_ctx* ctx, const void* id128, int nranks, int rank);
+
+/* ---- emulated rank group (one device; tests of the partitioned path) ----
+ * `count` (1..8) contexts on ONE device, each uploaded with a disjoint row
+ * range of the same graph (together covering [0, n): the 1D partition of the
+ * multi-GPU path), solved in lockstep on rank 0's stream: every rank's
+ * hooking kernels, then one kernel that min-merges the ranks' next-parent
+ * vectors (what ncclAllReduce(ncclInt32, ncclMin) does across processes,
+ * SURVEY §8a E4), then every rank's vertex pass. f_1 is assembled the same
+ * way. Runs the rank-partitioned kernels (row-filtered push, per-rank hub
+ * fix-up, f_1 assembly, host-batched loop) with fewer GPUs than ranks; no
+ * kernel waits on another. Results are replicated: each context's labels
+ * and trace equal the single-context solve; stats/snapshots are rank 0's
+ * (trace flops are the group's sum). */
+int fsv_group_solve(fsv_ctx* const* ctxs, int count, const fsv_config* cfg, fsv_stats* stats);
+int fsv_group_run_snapshots(fsv_ctx* const* ctxs, int count, const fsv_config* cfg, int32_t* labels,
+                            int32_t* iterations, int64_t* gf_changed, int64_t* f_changed,
+                            int32_t* snapshots, int32_t snap_cap);
 
 #ifdef __cplusplus
 }

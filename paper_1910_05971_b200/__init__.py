@@ -11,12 +11,13 @@ from .driver import (DriverConfig, HookingConfig, IterationTrace, RunResult, Sol
                      default_solver, device_count, fastsv, fastsv_la, require_device,
                      simplified_sv, sv_level_config)
 from .errors import DeviceError, InputError, InvariantError, SvccError, VerificationError
-from .graph import CsrGraph, Labeling, build_csr, labeling_from_parents
+from ._native import FsvStats
+from .graph import ComponentSizes, CsrGraph, Labeling, build_csr, labeling_from_parents
 
 __version__ = "0.1.0"
 
 __all__ = [
-    "CsrGraph", "Labeling", "build_csr", "labeling_from_parents",
+    "CsrGraph", "Labeling", "ComponentSizes", "build_csr", "labeling_from_parents", "FsvStats",
     "DriverConfig", "HookingConfig", "IterationTrace", "RunResult", "Solver",
     "choose_kernel", "fastsv_la", "fastsv", "connected_components", "default_solver",
     "simplified_sv", "sv_level_config", "ablation_results", "ablation_suite",

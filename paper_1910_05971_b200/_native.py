@@ -47,12 +47,14 @@ FASTSV_SYMBOLS = {
     "fsv_set_stream": (c_int, [c_void_p, c_void_p]),
     "fsv_upload_csr": (c_int, [c_void_p, c_int64, c_void_p, c_void_p, c_int64, c_int64]),
     "fsv_upload_csr64": (c_int, [c_void_p, c_int64, c_void_p, c_void_p, c_int64, c_int64]),
+    "fsv_upload_csr_device": (c_int, [c_void_p, c_int64, c_void_p, c_void_p, c_int64, c_int64]),
     "fsv_upload_edges": (c_int, [c_void_p, c_int64, c_int64, c_void_p, c_int64, c_int64]),
     "fsv_upload_edges64": (c_int, [c_void_p, c_int64, c_int64, c_void_p, c_int64, c_int64]),
     "fsv_get_csr": (c_int, [c_void_p, c_void_p, c_void_p, POINTER(c_int64)]),
     "fsv_solve": (c_int, [c_void_p, POINTER(FsvConfig), POINTER(FsvStats)]),
     "fsv_get_labels": (c_int, [c_void_p, c_void_p]),
     "fsv_get_labels64": (c_int, [c_void_p, c_void_p]),
+    "fsv_get_labeling": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_int64, POINTER(c_int64)]),
     "fsv_get_trace": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_int32]),
     "fsv_get_trace_ex": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int32]),
     "fsv_run": (c_int, [c_void_p, POINTER(FsvConfig), c_void_p, POINTER(c_int32), c_void_p,
@@ -61,6 +63,9 @@ FASTSV_SYMBOLS = {
                                   c_void_p, c_void_p, c_void_p, c_int32]),
     "fsv_nccl_unique_id": (c_int, [c_void_p]),
     "fsv_nccl_attach": (c_int, [c_void_p, c_void_p, c_int, c_int]),
+    "fsv_group_solve": (c_int, [c_void_p, c_int, POINTER(FsvConfig), POINTER(FsvStats)]),
+    "fsv_group_run_snapshots": (c_int, [c_void_p, c_int, POINTER(FsvConfig), c_void_p, POINTER(c_int32),
+                                        c_void_p, c_void_p, c_void_p, c_int32]),
 }
 
 GRAPHGEN_SYMBOLS = {

@@ -16,6 +16,7 @@
 
 #include <cub/cub.cuh>
 #include <cuda/std/functional>
+#include <thrust/iterator/counting_iterator.h>
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <nccl.h>
@@ -176,6 +177,10 @@ struct fsv_ctx {
   DBuf<int> csr_off32;       // int32 copy when the offsets fit (f_1 pass)
   bool off32 = false;
   DBuf<int> csr_cols;
+  // the symmetric CSR the solve reads: csr_off/csr_cols, or the caller's
+  // device arrays of a borrowed upload (fsv_upload_csr_device)
+  const int64_t* offp = nullptr;
+  const int* colsp = nullptr;
   int64_t col_base = 0, row_begin = 0, row_end = 0;
   int64_t csr_local = 0;   // entries of this rank's rows in csr_cols
   // changed-gf lists of the vertex pass (one region per warp)
@@ -235,6 +240,15 @@ struct fsv_ctx {
   std::vector<unsigned long long> h_cnt;
   std::vector<float> iter_ms;
   int labels_ready = 0;
+  // device Labeling of the last solve (fsv_get_labeling), built on demand
+  bool labeling_ready = false;
+  struct {
+    DBuf<unsigned> cnt;
+    DBuf<int> reps32;
+    DBuf<int64_t> reps, sizes, labels;
+    DBuf<unsigned char> tmp;
+    long long count = 0;
+  } lab;
   int host_syncs = 0, launches = 0;
   int hub_limit = kHubMax;
   // device loop control + CUDA-graph (conditional WHILE) of the iteration loop
@@ -477,19 +491,26 @@ __global__ void k_orient_encode(const int64_t* __restrict__ off, const ColT* __r
 
 // Pieces of rows longer than HUGE_ROW: one warp per piece (listed by the
 // host), 8 entries per lane in flight; kept counts summed per row.
+// Runs after the offsets were checked non-decreasing (k_degree), so the
+// counts are bounded by construction; the bounds are still enforced (ctr[2]
+// flags an overflow, the upload then fails instead of writing past a buffer).
 __global__ void k_find_huge(const int64_t* __restrict__ off, long long row_begin, long long rows,
                             long long* __restrict__ hrow, int4* __restrict__ pieces,
-                            unsigned long long* ctr) {
+                            unsigned long long* ctr, long long max_huge, long long max_pieces) {
   for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < rows;
        r += (long long)gridDim.x * blockDim.x) {
     const long long u = row_begin + r;
     const long long d = off[u + 1] - off[u];
     if (d <= HUGE_ROW) continue;
-    const int np = (int)((d + PIECE - 1) / PIECE);
-    const int h = (int)atomicAdd(ctr, 1ull);
+    const long long np = (d + PIECE - 1) / PIECE;
+    const unsigned long long h = atomicAdd(ctr, 1ull);
     const unsigned long long b = atomicAdd(ctr + 1, (unsigned long long)np);
+    if ((long long)h >= max_huge || (long long)(b + np) > max_pieces) {
+      ctr[2] = 1ull;
+      continue;
+    }
     hrow[h] = r;
-    for (int j = 0; j < np; ++j) pieces[b + j] = make_int4((int)u, j, j + 1, h);
+    for (long long j = 0; j < np; ++j) pieces[b + j] = make_int4((int)u, (int)j, (int)j + 1, (int)h);
   }
 }
 
@@ -856,29 +877,63 @@ DBuf<int32_t>& cols_buffer<int32_t>(fsv_ctx* c) { return c->csr_cols; }
 template <>
 DBuf<int64_t>& cols_buffer<int64_t>(fsv_ctx* c) { return c->ws.cols64; }
 
-// h_off: host copy of the full row offsets. Columns come from host h_cols
-// (copied up in chunks), or, when d_src is set, from a device array holding
-// every row's columns whose offsets are already in csr_off (fsv_upload_edges).
+// Row offsets of an upload as the host sees them: the full host array, or
+// (h == nullptr) device-resident offsets of which the host only fetched the
+// entries at 0, row_begin, row_end and n.
+struct HostOff {
+  const int64_t* h = nullptr;
+  int64_t idx[4] = {-1, -1, -1, -1}, val[4] = {0, 0, 0, 0};
+  int64_t operator[](int64_t i) const {
+    if (h) return h[i];
+    for (int k = 0; k < 4; ++k)
+      if (idx[k] == i) return val[k];
+    return -1;
+  }
+};
+
+// Offsets come from host h_off (copied up), or, when h_off is NULL, from the
+// device array d_off_src (fsv_upload_edges: the context's own csr_off;
+// fsv_upload_csr_device: the caller's). Columns come from host h_cols
+// (copied up in chunks) or from the device array d_src, indexed by global
+// entry (d_src_slice = false: every row's columns, fsv_upload_edges) or by
+// entry within this rank's rows (d_src_slice = true). borrow = true uses the
+// caller's device arrays in place for the context's lifetime (no copy).
 template <typename ColT>
-static int upload_impl(fsv_ctx* c, int64_t n, const int64_t* h_off, const ColT* h_cols,
-                       int64_t row_begin, int64_t row_end, const ColT* d_src = nullptr) {
+static int upload_impl(fsv_ctx* c, int64_t n, const int64_t* h_off_arr, const ColT* h_cols,
+                       int64_t row_begin, int64_t row_end, const ColT* d_src = nullptr,
+                       const int64_t* d_off_src = nullptr, bool d_src_slice = false, bool borrow = false) {
   if (!c) return fail(FSV_ERR_CONTRACT, "NULL context");
   if (n < 0) return fail(FSV_ERR_INPUT, "vertex count must be non-negative, got %lld", (long long)n);
   if (n >= (int64_t)IDMASK) return fail(FSV_ERR_INPUT, "n=%lld exceeds the device id range", (long long)n);
-  if (!h_off) return fail(FSV_ERR_CONTRACT, "row_offsets is NULL");
+  if (!h_off_arr && !d_off_src) return fail(FSV_ERR_CONTRACT, "row_offsets is NULL");
   if (row_begin < 0 || row_end < row_begin || row_end > n)
     return fail(FSV_ERR_CONTRACT, "row range [%lld, %lld) invalid for n=%lld", (long long)row_begin,
                 (long long)row_end, (long long)n);
+  CUDA_TRY(cudaSetDevice(c->device));
+  cudaStream_t st = c->stream;
+  HostOff h_off;
+  h_off.h = h_off_arr;
+  if (!h_off_arr) {
+    const int64_t ix[4] = {0, row_begin, row_end, n};
+    for (int k = 0; k < 4; ++k) {
+      h_off.idx[k] = ix[k];
+      CUDA_TRY(cudaMemcpyAsync(&h_off.val[k], d_off_src + ix[k], sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    }
+    CUDA_TRY(cudaStreamSynchronize(st));
+  }
   if (h_off[0] != 0) return fail(FSV_ERR_INPUT, "row_offsets[0] must be 0");
   if (h_off[n] < h_off[0]) return fail(FSV_ERR_INPUT, "row_offsets must be non-decreasing");
   const int64_t e_begin = h_off[row_begin], e_end = h_off[row_end];
   const int64_t mloc = e_end - e_begin;
-  if (mloc < 0 || e_begin < 0) return fail(FSV_ERR_INPUT, "row_offsets must be non-decreasing");
+  if (mloc < 0 || e_begin < 0 || e_end > h_off[n]) return fail(FSV_ERR_INPUT, "row_offsets must be non-decreasing");
   if (mloc > 0 && !h_cols && !d_src) return fail(FSV_ERR_CONTRACT, "col_indices is NULL");
-  CUDA_TRY(cudaSetDevice(c->device));
-  cudaStream_t st = c->stream;
+  if (borrow && (!d_src || !d_src_slice || !d_off_src || h_off_arr))
+    return fail(FSV_ERR_CONTRACT, "borrowed uploads take device offsets and a device column slice");
+  // the device column source indexed by global entry
+  const ColT* d_src_g = d_src ? (d_src_slice ? d_src - e_begin : d_src) : nullptr;
   c->ready = false;
   c->labels_ready = 0;
+  c->labeling_ready = false;
   c->graph_dirty = true;
 
   const long long rows = row_end - row_begin;
@@ -890,10 +945,22 @@ static int upload_impl(fsv_ctx* c, int64_t n, const int64_t* h_off, const ColT* 
   std::vector<cudaEvent_t> dbg_copy_ev, dbg_enc_ev;
   DBuf<int64_t>& d_off = c->csr_off;
   DBuf<ColT>& d_cols = cols_buffer<ColT>(c);
-  CUDA_TRY(d_off.alloc((size_t)n + 1));
-  CUDA_TRY(d_cols.alloc((size_t)mloc));
-  if (!d_src)
-    CUDA_TRY(cudaMemcpyAsync(d_off.p, h_off, sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice, st));
+  // offp/colp: the offsets and this rank's columns the layout build reads
+  const int64_t* offp = nullptr;
+  const ColT* colp = nullptr;
+  if (borrow) {
+    offp = d_off_src;
+    colp = d_src;
+  } else {
+    if (d_off_src != d_off.p || !d_off.p) CUDA_TRY(d_off.alloc((size_t)n + 1));
+    CUDA_TRY(d_cols.alloc((size_t)mloc));
+    if (h_off_arr)
+      CUDA_TRY(cudaMemcpyAsync(d_off.p, h_off_arr, sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice, st));
+    else if (d_off_src != d_off.p)
+      CUDA_TRY(cudaMemcpyAsync(d_off.p, d_off_src, sizeof(int64_t) * (n + 1), cudaMemcpyDeviceToDevice, st));
+    offp = d_off.p;
+    colp = d_cols.p;
+  }
   // columns go up in row-aligned chunks on the copy stream, so the degree
   // sort and the orientation of earlier chunks overlap the transfer
   std::vector<int64_t> chunk_rows;  // row boundaries, chunk k = [chunk_rows[k], chunk_rows[k+1])
@@ -901,7 +968,7 @@ static int upload_impl(fsv_ctx* c, int64_t n, const int64_t* h_off, const ColT* 
     // eighths of the entries, the last eighth cut geometrically (1/16, 1/32,
     // 1/64, 1/64) so the work trailing the final copy is small
     std::vector<int64_t> cut;  // chunk ends in 1/64ths of mloc
-    if (mloc >= ((int64_t)1 << 24) && !d_src) cut = {8, 16, 24, 32, 40, 48, 56, 60, 62, 63, 64};
+    if (mloc >= ((int64_t)1 << 24) && !d_src && h_off.h) cut = {8, 16, 24, 32, 40, 48, 56, 60, 62, 63, 64};
     else cut = {64};
     if (const char* env = d_src ? nullptr : getenv("FSV_UPLOAD_CHUNKS")) {   // dev: K equal chunks
       const int k_eq = std::max(1, std::min(64, atoi(env)));
@@ -912,7 +979,7 @@ static int upload_impl(fsv_ctx* c, int64_t n, const int64_t* h_off, const ColT* 
     chunk_rows.push_back(row_begin);
     for (int k = 0; k + 1 < K; ++k) {
       const int64_t target = e_begin + (int64_t)((__int128)mloc * cut[k] / 64);
-      int64_t r = std::lower_bound(h_off + row_begin, h_off + row_end, target) - h_off;
+      int64_t r = std::lower_bound(h_off.h + row_begin, h_off.h + row_end, target) - h_off.h;   // K > 1: host offsets
       r = std::max<int64_t>(r, chunk_rows.back());
       chunk_rows.push_back(std::min<int64_t>(r, row_end));
     }
@@ -927,11 +994,17 @@ static int upload_impl(fsv_ctx* c, int64_t n, const int64_t* h_off, const ColT* 
     CUDA_TRY(cudaStreamWaitEvent(c->copy_stream, off_ready, 0));
     for (int k = 0; k < K; ++k) {
       const int64_t lo = h_off[chunk_rows[k]] - e_begin, hi = h_off[chunk_rows[k + 1]] - e_begin;
+      // only non-decreasing offsets are accepted (checked on the device
+      // below); until then no copy may leave [0, mloc)
+      if (lo < 0 || hi > mloc || (hi < lo && !d_src)) {
+        cudaStreamSynchronize(c->copy_stream);
+        return fail(FSV_ERR_INPUT, "row_offsets must be non-decreasing");
+      }
       if (hi > lo && !d_src)
         CUDA_TRY(cudaMemcpyAsync(d_cols.p + lo, h_cols + lo, sizeof(ColT) * (hi - lo),
                                  cudaMemcpyHostToDevice, c->copy_stream));
-      else if (hi > lo && d_src + e_begin + lo != d_cols.p + lo)   // this rank's slice of a device CSR
-        CUDA_TRY(cudaMemcpyAsync(d_cols.p + lo, d_src + e_begin + lo, sizeof(ColT) * (hi - lo),
+      else if (hi > lo && !borrow && d_src_g + e_begin + lo != d_cols.p + lo)   // this rank's slice of a device CSR
+        CUDA_TRY(cudaMemcpyAsync(d_cols.p + lo, d_src_g + e_begin + lo, sizeof(ColT) * (hi - lo),
                                  cudaMemcpyDeviceToDevice, c->copy_stream));
       CUDA_TRY(cudaEventRecord(c->chunk_ev[k], c->copy_stream));
       if (udbg) {
@@ -947,13 +1020,10 @@ static int upload_impl(fsv_ctx* c, int64_t n, const int64_t* h_off, const ColT* 
   const long long max_pieces = mloc / PIECE + max_huge + 1;
   CUDA_TRY(c->ws.pieces.alloc((size_t)max_pieces));
   CUDA_TRY(c->ws.hrow.alloc((size_t)max_huge));
-  CUDA_TRY(c->ws.hkept.alloc((size_t)max_huge + 2));   // [0..max_huge) kept, then 2 counters
+  CUDA_TRY(c->ws.hkept.alloc((size_t)max_huge + 3));   // [0..max_huge) kept, then 3 counters
   CUDA_TRY(c->ws.piece_kept.alloc((size_t)max_pieces));
-  CUDA_TRY(cudaMemsetAsync(c->ws.hkept.p, 0, sizeof(unsigned long long) * (max_huge + 2), st));
-  unsigned long long* huge_ctr = c->ws.hkept.p + max_huge;      // [0] huge rows, [1] pieces
-  if (rows)
-    k_find_huge<<<grid_for(c, rows, 256), 256, 0, st>>>(d_off.p, row_begin, rows, c->ws.hrow.p,
-                                                        c->ws.pieces.p, huge_ctr);
+  CUDA_TRY(cudaMemsetAsync(c->ws.hkept.p, 0, sizeof(unsigned long long) * (max_huge + 3), st));
+  unsigned long long* huge_ctr = c->ws.hkept.p + max_huge;      // [0] huge rows, [1] pieces, [2] overflow
 
   // degrees (+ offsets check), stable degree order, positions, hubs
   DBuf<unsigned long long>& d_bad = c->ws.bad;
@@ -966,7 +1036,7 @@ static int upload_impl(fsv_ctx* c, int64_t n, const int64_t* h_off, const ColT* 
   auto& pos = c->ws.slot_of;
   CUDA_TRY(deg.alloc(n)); CUDA_TRY(ids.alloc(n));
   CUDA_TRY(deg_sorted.alloc(n)); CUDA_TRY(ids_sorted.alloc(n)); CUDA_TRY(pos.alloc(n));
-  if (n) k_degree<<<grid_for(c, n, 256), 256, 0, st>>>(d_off.p, n, deg.p, ids.p, d_bad.p + 1);
+  if (n) k_degree<<<grid_for(c, n, 256), 256, 0, st>>>(offp, n, deg.p, ids.p, d_bad.p + 1);
   int H = 0;
   {
     // one temp buffer for the sort and the per-chunk scans (no reallocation
@@ -997,6 +1067,11 @@ static int upload_impl(fsv_ctx* c, int64_t n, const int64_t* h_off, const ColT* 
     CUDA_TRY(cudaMemcpyAsync(&h_badoff, d_bad.p + 1, sizeof h_badoff, cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaStreamSynchronize(st));
     if (h_badoff != ~0ull) return fail(FSV_ERR_INPUT, "row_offsets must be non-decreasing");
+    // offsets are non-decreasing from here on: the huge-row piece list
+    // (which sizes its writes by per-row differences) is safe to build
+    if (rows)
+      k_find_huge<<<grid_for(c, rows, 256), 256, 0, st>>>(offp, row_begin, rows, c->ws.hrow.p,
+                                                          c->ws.pieces.p, huge_ctr, max_huge, max_pieces);
     int cand = 0;
     while (cand < probe && top[cand] >= kHubMinDegree) ++cand;
     H = (c->hub_limit >= 0) ? std::min(cand, c->hub_limit) : 0;
@@ -1058,9 +1133,9 @@ static int upload_impl(fsv_ctx* c, int64_t n, const int64_t* h_off, const ColT* 
     CUDA_TRY(cudaStreamWaitEvent(st, c->chunk_ev[k], 0));
     if (nr) {
       k_orient_encode<ColT><<<grid_for(c, (nr + 31) / 32 * 32, 256, 16), 256, 0, st>>>(
-          d_off.p, d_cols.p, e_begin, u0, nr, n, pos.p, HT, etmp.p, cnt.p + r0, nzflag.p + r0, d_bad.p);
+          offp, colp, e_begin, u0, nr, n, pos.p, HT, etmp.p, cnt.p + r0, nzflag.p + r0, d_bad.p);
       k_piece_encode<ColT><<<c->sm_count * 16, 256, 0, st>>>(
-          c->ws.pieces.p, huge_ctr + 1, u0, u1, d_off.p, d_cols.p, e_begin, n, pos.p, HT, etmp.p,
+          c->ws.pieces.p, huge_ctr + 1, u0, u1, offp, colp, e_begin, n, pos.p, HT, etmp.p,
           c->ws.hkept.p, c->ws.piece_kept.p, d_bad.p);
       k_huge_rows<<<c->sm_count * 2, 256, 0, st>>>(c->ws.hrow.p, huge_ctr, r0, r1, c->ws.hkept.p, cnt.p,
                                                   nzflag.p);
@@ -1075,9 +1150,9 @@ static int upload_impl(fsv_ctx* c, int64_t n, const int64_t* h_off, const ColT* 
                                    c->ws.carry_r.p, k);
     if (nr) {
       k_orient_compact<<<grid_for(c, (nr + 31) / 32 * 32, 256, 16), 256, 0, st>>>(
-          d_off.p, e_begin, u0, nr, etmp.p, out_off.p + r0, nzidx.p + r0, c->ecolp, nzrows.p, nzoff.p);
+          offp, e_begin, u0, nr, etmp.p, out_off.p + r0, nzidx.p + r0, c->ecolp, nzrows.p, nzoff.p);
       k_piece_compact<<<c->sm_count * 16, 256, 0, st>>>(
-          c->ws.pieces.p, huge_ctr + 1, u0, u1, d_off.p, e_begin, etmp.p, c->ws.hrow.p, out_off.p,
+          c->ws.pieces.p, huge_ctr + 1, u0, u1, offp, e_begin, etmp.p, c->ws.hrow.p, out_off.p,
           c->ws.piece_kept.p, c->ecolp);
     }
     if (udbg) {
@@ -1088,18 +1163,34 @@ static int upload_impl(fsv_ctx* c, int64_t n, const int64_t* h_off, const ColT* 
   umark(3);
   long long E = 0;
   int R = 0;
-  unsigned long long h_bad = 0;
+  unsigned long long h_bad = 0, h_overflow = 0;
   CUDA_TRY(cudaMemcpyAsync(&E, c->ws.carry_e.p + K, sizeof E, cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaMemcpyAsync(&R, c->ws.carry_r.p + K, sizeof R, cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaMemcpyAsync(&h_bad, d_bad.p, sizeof h_bad, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaMemcpyAsync(&h_overflow, huge_ctr + 2, sizeof h_overflow, cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaStreamSynchronize(st));
+  if (h_overflow) return fail(FSV_ERR_INPUT, "row_offsets must be non-decreasing");
   if (h_bad != ~0ull) {
     // graph.py:71-75 semantics: report an offending entry
     const int64_t e = e_begin + (int64_t)h_bad;
-    const int64_t* it = std::upper_bound(h_off, h_off + n + 1, e);
-    const long long u = (long long)(it - h_off) - 1;
-    return fail(FSV_ERR_INPUT, "edge (%lld, %lld) out of range for n=%lld", u,
-                h_cols ? (long long)h_cols[h_bad] : -1LL, (long long)n);
+    std::vector<int64_t> hv;
+    const int64_t* hp = h_off.h;
+    if (!hp) {   // device offsets: fetch them for the message (error path only)
+      hv.resize((size_t)n + 1);
+      CUDA_TRY(cudaMemcpy(hv.data(), offp, sizeof(int64_t) * (n + 1), cudaMemcpyDeviceToHost));
+      hp = hv.data();
+    }
+    const int64_t* it = std::upper_bound(hp, hp + n + 1, e);
+    const long long u = (long long)(it - hp) - 1;
+    long long v = -1;
+    if (h_cols) {
+      v = (long long)h_cols[h_bad];
+    } else {
+      ColT cv = 0;
+      CUDA_TRY(cudaMemcpy(&cv, colp + h_bad, sizeof(ColT), cudaMemcpyDeviceToHost));
+      v = (long long)cv;
+    }
+    return fail(FSV_ERR_INPUT, "edge (%lld, %lld) out of range for n=%lld", u, v, (long long)n);
   }
   const long long Epad = (E + SPAN - 1) / SPAN * SPAN;
   umark(4);
@@ -1123,10 +1214,15 @@ static int upload_impl(fsv_ctx* c, int64_t n, const int64_t* h_off, const ColT* 
   if constexpr (sizeof(ColT) != 4) {
     CUDA_TRY(c->csr_cols.alloc((size_t)std::max<int64_t>(mloc, 1)));
     if (mloc)
-      k_narrow<<<grid_for(c, mloc, 256), 256, 0, st>>>(d_cols.p, mloc, c->csr_cols.p);
+      k_narrow<<<grid_for(c, mloc, 256), 256, 0, st>>>(colp, mloc, c->csr_cols.p);
   }
   c->col_base = e_begin;
   c->csr_local = mloc;
+  c->offp = offp;
+  if constexpr (sizeof(ColT) == 4)
+    c->colsp = reinterpret_cast<const int*>(colp);
+  else
+    c->colsp = c->csr_cols.p;
   c->var_rows_ready = false;
   c->row_begin = row_begin;
   c->row_end = row_end;
@@ -1194,7 +1290,7 @@ static int upload_impl(fsv_ctx* c, int64_t n, const int64_t* h_off, const ColT* 
   c->off32 = h_off[n] < (int64_t(1) << 31);
   if (c->off32) {
     CUDA_TRY(c->csr_off32.alloc((size_t)n + 1));
-    k_narrow<<<grid_for(c, n + 1, 256), 256, 0, st>>>(d_off.p, n + 1, c->csr_off32.p);
+    k_narrow<<<grid_for(c, n + 1, 256), 256, 0, st>>>(offp, n + 1, c->csr_off32.p);
     CUDA_TRY(cudaStreamSynchronize(st));
     CUDA_TRY(cudaGetLastError());
   }
@@ -1216,6 +1312,17 @@ extern "C" int fsv_set_hub_slots(fsv_ctx* c, int slots) {
 extern "C" int fsv_upload_csr(fsv_ctx* c, int64_t n, const int64_t* off, const int32_t* cols,
                               int64_t row_begin, int64_t row_end) {
   return upload_impl<int32_t>(c, n, off, cols, row_begin, row_end);
+}
+
+extern "C" int fsv_upload_csr_device(fsv_ctx* c, int64_t n, const int64_t* d_off, const int32_t* d_cols,
+                                     int64_t row_begin, int64_t row_end) {
+  if (!d_off) return fail(FSV_ERR_CONTRACT, "row_offsets is NULL");
+  if (!d_cols) {
+    // an empty column slice needs no pointer
+    static const int32_t none = 0;
+    d_cols = &none;   // never read: the upload checks mloc first
+  }
+  return upload_impl<int32_t>(c, n, nullptr, nullptr, row_begin, row_end, d_cols, d_off, true, true);
 }
 
 extern "C" int fsv_upload_csr64(fsv_ctx* c, int64_t n, const int64_t* off, const int64_t* cols,
@@ -1242,6 +1349,7 @@ static int upload_edges_impl(fsv_ctx* c, int64_t n, int64_t m, const IdT* h_pair
   cudaStream_t st = c->stream;
   c->ready = false;
   c->labels_ready = 0;
+  c->labeling_ready = false;
   int b = 1;
   while ((1LL << b) < n) ++b;        // ids < n <= 2^b
   const long long m2 = 2 * m;
@@ -1340,21 +1448,11 @@ static int upload_edges_impl(fsv_ctx* c, int64_t n, int64_t m, const IdT* h_pair
     k_csr_from_keys<<<grid_for(c, n + 1, 256, 16), 256, 0, st>>>(nullptr, d_cnt + 1, n, b, c->csr_off.p,
                                                                  c->csr_cols.p);
   }
-  // host copy of the offsets for the layout build's row bookkeeping
-  if (c->h_off_cap < (size_t)n + 1) {
-    if (c->h_off_pin) cudaFreeHost(c->h_off_pin);
-    c->h_off_pin = nullptr;
-    c->h_off_cap = 0;
-    EDGE_TRY(cudaMallocHost(&c->h_off_pin, sizeof(int64_t) * ((size_t)n + 1)));
-    c->h_off_cap = (size_t)n + 1;
-  }
-  EDGE_TRY(cudaMemcpyAsync(c->h_off_pin, c->csr_off.p, sizeof(int64_t) * (n + 1), cudaMemcpyDeviceToHost, st));
-  EDGE_TRY(cudaStreamSynchronize(st));
   if (ka) { cudaFreeAsync(ka, st); ka = nullptr; }
   if (kb) { cudaFreeAsync(kb, st); kb = nullptr; }
   if (d_tmp) { cudaFreeAsync(d_tmp, st); d_tmp = nullptr; }
   const int32_t* src = d_full ? d_full : c->csr_cols.p;
-  const int rc = upload_impl<int32_t>(c, n, c->h_off_pin, nullptr, row_begin, row_end, src);
+  const int rc = upload_impl<int32_t>(c, n, nullptr, nullptr, row_begin, row_end, src, c->csr_off.p);
   release();
 #undef EDGE_TRY
   return rc;
@@ -1377,10 +1475,10 @@ extern "C" int fsv_get_csr(fsv_ctx* c, int64_t* row_offsets, int32_t* cols, int6
   if (csr_entries) *csr_entries = mloc;
   CUDA_TRY(cudaSetDevice(c->device));
   if (row_offsets)
-    CUDA_TRY(cudaMemcpyAsync(row_offsets, c->csr_off.p, sizeof(int64_t) * (c->n + 1), cudaMemcpyDeviceToHost,
+    CUDA_TRY(cudaMemcpyAsync(row_offsets, c->offp, sizeof(int64_t) * (c->n + 1), cudaMemcpyDeviceToHost,
                              c->stream));
   if (cols && mloc)
-    CUDA_TRY(cudaMemcpyAsync(cols, c->csr_cols.p, sizeof(int32_t) * mloc, cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(cudaMemcpyAsync(cols, c->colsp, sizeof(int32_t) * mloc, cudaMemcpyDeviceToHost, c->stream));
   CUDA_TRY(cudaStreamSynchronize(c->stream));
   return FSV_OK;
 }
@@ -1439,10 +1537,34 @@ static LoopCtl loop_ctl(fsv_ctx* c, int graph) {
   return l;
 }
 
-// Queue iteration k (host loop), or, with graph = true, one half of the
-// graph body whose buffer parity is that of k (the iteration number itself
-// is read by the kernels from device memory).
-static int launch_iteration(fsv_ctx* c, int k, int max_iter, bool graph = false) {
+// Min-merge of the R partial next-parent vectors of an emulated rank group
+// (fsv_group_solve): the elementwise min over ranks is written back to every
+// rank's buffer, exactly what ncclAllReduce(ncclInt32, ncclMin) produces in
+// the multi-process path. One launch over all ranks' data, no
+// kernel waits on another.
+constexpr int kGroupMax = 8;
+struct MergeArgs {
+  int* buf[kGroupMax];
+  int count;
+  long long n;
+  const int* done;   // skip once converged (speculative host-loop launches)
+};
+
+__global__ void k_group_min_merge(MergeArgs a) {
+  if (a.done && *(volatile const int*)a.done) return;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < a.n; i += stride) {
+    int v = a.buf[0][i];
+    for (int r = 1; r < a.count; ++r) v = min(v, a.buf[r][i]);
+    for (int r = 0; r < a.count; ++r)
+      if (a.buf[r][i] != v) a.buf[r][i] = v;
+  }
+}
+
+// Queue the hooking phase of iteration k (host loop), or, with graph = true,
+// of one half of the graph body whose buffer parity is that of k (the
+// iteration number itself is read by the kernels from device memory).
+static int launch_hook(fsv_ctx* c, int k, bool graph) {
   cudaStream_t st = c->stream;
   const LoopCtl lc = loop_ctl(c, graph ? 1 : 0);
   if (c->profile) {
@@ -1465,7 +1587,7 @@ static int launch_iteration(fsv_ctx* c, int k, int max_iter, bool graph = false)
     PushArgs& p = a.push;
     p.list = c->dlist.p; p.count = c->dcount.p; p.rcap = c->rcap;
     p.nregions = c->dgrid * (SC_THREADS / 32);
-    p.off = c->csr_off.p; p.cols = c->csr_cols.p; p.col_base = c->col_base;
+    p.off = c->offp; p.cols = c->colsp; p.col_base = c->col_base;
     p.row_begin = (int)c->row_begin; p.row_end = (int)c->row_end;
     p.F = F; p.G = c->G; p.N = N; p.mode = c->mode.p; p.iter = k;
     unsigned long long* slot = c->cnt.p + (size_t)(k - 1) * NCOUNT;
@@ -1498,23 +1620,66 @@ static int launch_iteration(fsv_ctx* c, int k, int max_iter, bool graph = false)
     pmark(c, k, 3);
     ++c->launches;
   }
+  return FSV_OK;
+}
+
+// The exchange between the hooking phase and the vertex pass: nothing on one
+// rank, ncclAllReduce(min) of the next-parent vector with a communicator, or
+// the device min-merge of an emulated rank group.
+static int launch_exchange(fsv_ctx* const* cs, int count, int k) {
+  fsv_ctx* c = cs[0];
+  if (count > 1) {
+    MergeArgs m{};
+    for (int r = 0; r < count; ++r) m.buf[r] = bufN(cs[r], k);
+    m.count = count;
+    m.n = c->n;
+    m.done = c->done.p;
+    if (c->n) {
+      k_group_min_merge<<<grid_for(c, c->n, 256), 256, 0, c->stream>>>(m);
+      ++c->launches;
+    }
+    return FSV_OK;
+  }
   if (c->comm && c->n) {
     pmark(c, k, 8);
-    NCCL_TRY(g_nccl.AllReduce(N, N, (size_t)c->n, ncclInt32, ncclMin, c->comm, st));
+    NCCL_TRY(g_nccl.AllReduce(bufN(c, k), bufN(c, k), (size_t)c->n, ncclInt32, ncclMin, c->comm, c->stream));
     pmark(c, k, 9);
   }
+  return FSV_OK;
+}
+
+// The vertex pass of iteration k: grandparents, counters, convergence flag.
+static int launch_vertex(fsv_ctx* c, int k, int max_iter, bool graph) {
+  const LoopCtl lc = loop_ctl(c, graph ? 1 : 0);
   ShortcutArgs s;
-  s.F = F; s.G = c->G; s.N = N; s.n = c->n; s.hub_id = c->hub_id.p; s.G_hub = c->G_hub.p;
+  s.F = bufF(c, k); s.G = c->G; s.N = bufN(c, k); s.n = c->n; s.hub_id = c->hub_id.p; s.G_hub = c->G_hub.p;
   s.H = c->HT; s.cnt = c->cnt.p + (size_t)(k - 1) * NCOUNT; s.ticket = c->ticket.p; s.done = c->done.p;
   s.partials = c->partials.p;
   s.dl = delta_out(c);
   s.iter = k; s.max_iter = max_iter;
   s.lc = lc;
   pmark(c, k, 6);
-  k_shortcut<<<vertex_grid(c), SC_THREADS, 0, st>>>(s);
+  k_shortcut<<<vertex_grid(c), SC_THREADS, 0, c->stream>>>(s);
   pmark(c, k, 7);
   ++c->launches;
   return FSV_OK;
+}
+
+static int launch_iteration(fsv_ctx* c, int k, int max_iter, bool graph = false) {
+  int rc = launch_hook(c, k, graph);
+  if (!rc) rc = launch_exchange(&c, 1, k);
+  if (!rc) rc = launch_vertex(c, k, max_iter, graph);
+  return rc;
+}
+
+// One iteration of an emulated rank group: every rank's hooking phase, the
+// device min-merge, every rank's (replicated) vertex pass.
+static int launch_group_iteration(fsv_ctx* const* cs, int count, int k, int max_iter) {
+  int rc = FSV_OK;
+  for (int r = 0; r < count && !rc; ++r) rc = launch_hook(cs[r], k, false);
+  if (!rc) rc = launch_exchange(cs, count, k);
+  for (int r = 0; r < count && !rc; ++r) rc = launch_vertex(cs[r], k, max_iter, false);
+  return rc;
 }
 
 // The buffers, sizes and launch shapes baked into the captured iteration
@@ -1524,7 +1689,7 @@ static std::vector<long long> graph_key(const fsv_ctx* c) {
   auto P = [](const void* p) { return (long long)(uintptr_t)p; };
   return {P(c->ecolp), c->Epad, P(c->span_row.p), P(c->X), P(c->Y), P(c->G), P(c->G_hub.p), c->H, c->HT,
           P(c->hacc), P(c->hub_id.p), P(c->done.p), P(c->mode.p), P(c->dlist.p), P(c->dcount.p), c->rcap,
-          c->dgrid, P(c->csr_off.p), P(c->csr_cols.p), c->col_base, c->row_begin, c->row_end, P(c->cnt.p),
+          c->dgrid, P(c->offp), P(c->colsp), c->col_base, c->row_begin, c->row_end, P(c->cnt.p),
           P(c->chunks.p), P(c->iterbuf.p), P(c->tstamp.p), P(c->ticket.p), P(c->partials.p), c->n,
           c->sm_count};
 }
@@ -1630,7 +1795,7 @@ template <bool STO, bool AGG, bool GP>
 static void launch_var_hook(fsv_ctx* c, const int* F, const int* G, int* N) {
   const long long m = c->csr_local;
   if (m)
-    k_var_hook<STO, AGG, GP><<<grid_for(c, m, 256, 16), 256, 0, c->stream>>>(c->var_rows.p, c->csr_cols.p, m, F,
+    k_var_hook<STO, AGG, GP><<<grid_for(c, m, 256, 16), 256, 0, c->stream>>>(c->var_rows.p, c->colsp, m, F,
                                                                               G, N);
 }
 
@@ -1648,7 +1813,7 @@ static int solve_variant(fsv_ctx* c, const fsv_config& d, int cap, int32_t* snap
   if (!c->var_rows_ready) {
     CUDA_TRY(c->var_rows.alloc((size_t)std::max<long long>(c->csr_local, 1)));
     if (c->csr_local)
-      k_row_ids<<<grid_for(c, n * 32, 256, 16), 256, 0, st>>>(c->csr_off.p, c->col_base, 0, n, c->var_rows.p);
+      k_row_ids<<<grid_for(c, n * 32, 256, 16), 256, 0, st>>>(c->offp, c->col_base, 0, n, c->var_rows.p);
     c->var_rows_ready = true;
   }
   const size_t nv = (size_t)n + 64;
@@ -1728,14 +1893,16 @@ static int solve_variant(fsv_ctx* c, const fsv_config& d, int cap, int32_t* snap
   return FSV_OK;
 }
 
-static int solve_body(fsv_ctx* c, const fsv_config* cfg, int32_t* snapshots, int32_t snap_cap);
+static int solve_body(fsv_ctx* const* cs, int count, const fsv_config* cfg, int32_t* snapshots,
+                      int32_t snap_cap);
 
 // Checked builds clear the registered ranges after every solve, so upload
 // kernels (which read other buffers through the same helpers) are unchecked.
-static int solve_impl(fsv_ctx* c, const fsv_config* cfg, int32_t* snapshots, int32_t snap_cap) {
-  const int rc = solve_body(c, cfg, snapshots, snap_cap);
+static int solve_impl_group(fsv_ctx* const* cs, int count, const fsv_config* cfg, int32_t* snapshots,
+                            int32_t snap_cap) {
+  const int rc = solve_body(cs, count, cfg, snapshots, snap_cap);
 #ifdef FSV_CHECKS
-  if (c) {
+  if (cs && cs[0]) {
     const ChkRanges none{};
     cudaMemcpyToSymbol(g_chk, &none, sizeof none);
   }
@@ -1743,9 +1910,62 @@ static int solve_impl(fsv_ctx* c, const fsv_config* cfg, int32_t* snapshots, int
   return rc;
 }
 
-static int solve_body(fsv_ctx* c, const fsv_config* cfg, int32_t* snapshots, int32_t snap_cap) {
-  if (!c) return fail(FSV_ERR_CONTRACT, "NULL context");
-  if (!c->ready) return fail(FSV_ERR_CONTRACT, "no graph uploaded");
+static int solve_impl(fsv_ctx* c, const fsv_config* cfg, int32_t* snapshots, int32_t snap_cap) {
+  return solve_impl_group(&c, 1, cfg, snapshots, snap_cap);
+}
+
+// A rank group runs every rank's kernels on rank 0's stream, in order; the
+// contexts' own streams are restored afterwards.
+struct StreamGuard {
+  fsv_ctx* const* cs;
+  int count;
+  cudaStream_t saved[kGroupMax];
+  StreamGuard(fsv_ctx* const* cs_, int count_) : cs(cs_), count(count_) {
+    for (int r = 0; r < count; ++r) {
+      saved[r] = cs[r]->stream;
+      cs[r]->stream = cs[0]->stream;
+    }
+  }
+  ~StreamGuard() {
+    for (int r = 0; r < count; ++r) cs[r]->stream = saved[r];
+  }
+};
+
+// The group must be one graph split into disjoint row ranges covering
+// [0, n) on one device (the 1D partition of SURVEY §8e).
+static int check_group(fsv_ctx* const* cs, int count) {
+  if (count < 1 || count > kGroupMax) return fail(FSV_ERR_CONTRACT, "group size %d not in 1..%d", count, kGroupMax);
+  for (int r = 0; r < count; ++r) {
+    if (!cs[r]) return fail(FSV_ERR_CONTRACT, "NULL context");
+    if (!cs[r]->ready) return fail(FSV_ERR_CONTRACT, "no graph uploaded");
+  }
+  if (count == 1) return FSV_OK;
+  std::vector<std::pair<int64_t, int64_t>> ranges;
+  for (int r = 0; r < count; ++r) {
+    const fsv_ctx* c = cs[r];
+    for (int q = 0; q < r; ++q)
+      if (cs[q] == c) return fail(FSV_ERR_CONTRACT, "a context appears twice in the group");
+    if (c->device != cs[0]->device) return fail(FSV_ERR_CONTRACT, "group contexts must share one device");
+    if (c->n != cs[0]->n) return fail(FSV_ERR_CONTRACT, "group contexts must hold the same graph (n differs)");
+    if (c->comm) return fail(FSV_ERR_CONTRACT, "group contexts cannot carry a communicator");
+    ranges.emplace_back(c->row_begin, c->row_end);
+  }
+  std::sort(ranges.begin(), ranges.end());
+  int64_t at = 0;
+  for (auto& rg : ranges) {
+    if (rg.first != at) return fail(FSV_ERR_CONTRACT, "group row ranges must be disjoint and cover [0, n)");
+    at = rg.second;
+  }
+  if (at != cs[0]->n) return fail(FSV_ERR_CONTRACT, "group row ranges must be disjoint and cover [0, n)");
+  return FSV_OK;
+}
+
+static int solve_body(fsv_ctx* const* cs, int count, const fsv_config* cfg, int32_t* snapshots,
+                      int32_t snap_cap) {
+  if (!cs || !cs[0]) return fail(FSV_ERR_CONTRACT, "NULL context");
+  int rc = check_group(cs, count);
+  if (rc) return rc;
+  fsv_ctx* c = cs[0];
   CUDA_TRY(cudaSetDevice(c->device));
   fsv_config d{};
   if (cfg) d = *cfg;
@@ -1753,36 +1973,44 @@ static int solve_body(fsv_ctx* c, const fsv_config* cfg, int32_t* snapshots, int
   const int cap = d.max_iters > 0 ? std::min(d.max_iters, kTraceCap) : kTraceCap;
   int batch = d.batch > 0 ? d.batch : 4;
   if (snapshots) batch = 1;
-  cudaStream_t st = c->stream;
-  int rc = ensure_events(c, 2);
-  if (rc) return rc;
-  c->launches = 0;
-  c->host_syncs = 0;
-  c->labels_ready = 0;
-  c->profile = d.profile != 0;
   if (d.sparse_policy < 0 || d.sparse_policy > 3)
     return fail(FSV_ERR_CONTRACT, "sparse_policy must be 0..3");
   if (d.sparse_policy == 3 && !(d.sparse_threshold >= 0.0 && d.sparse_threshold <= 1.0))
     return fail(FSV_ERR_CONTRACT, "sparse_threshold must be in [0, 1]");
-  c->policy = d.sparse_policy;
-  c->threshold = d.sparse_policy == 3 ? d.sparse_threshold : 0.1;
-  c->hook_ms = c->hubfix_ms = c->shortcut_ms = c->first_ms = c->allreduce_ms = c->push_ms = 0.f;
-  c->hook_launches = 0;
+  if (count > 1 && d.hooking) return fail(FSV_ERR_CONTRACT, "hooking variants run on a single context");
+  if (count > 1 && d.profile) return fail(FSV_ERR_CONTRACT, "profile is not supported for rank groups");
+  if ((rc = ensure_events(c, 2))) return rc;
+  for (int r = 0; r < count; ++r) {
+    fsv_ctx* x = cs[r];
+    x->launches = 0;
+    x->host_syncs = 0;
+    x->labels_ready = 0;
+    x->labeling_ready = false;
+    x->profile = d.profile != 0;
+    x->policy = d.sparse_policy;
+    x->threshold = d.sparse_policy == 3 ? d.sparse_threshold : 0.1;
+    x->hook_ms = x->hubfix_ms = x->shortcut_ms = x->first_ms = x->allreduce_ms = x->push_ms = 0.f;
+    x->hook_launches = 0;
+  }
   if (d.hooking) {
     if ((d.hooking & ~(FSV_HOOKING_SET | 15)) || !(d.hooking & FSV_HOOKING_SET))
       return fail(FSV_ERR_CONTRACT, "hooking must be 0 or FSV_HOOKING_SET | flag bits, got 0x%x", d.hooking);
     return solve_variant(c, d, cap, snapshots, snap_cap);
   }
-  c->variant = false;
-  c->labels_src = c->G;
+  StreamGuard guard(cs, count);
+  cudaStream_t st = c->stream;
+  for (int r = 0; r < count; ++r) {
+    cs[r]->variant = false;
+    cs[r]->labels_src = cs[r]->G;
+  }
 #ifdef FSV_CHECKS
-  {  // checked build: the buffers the solve kernels may load from / reduce into
+  if (count == 1) {  // checked build: the buffers the solve kernels may load from / reduce into
     ChkRanges r{};
     auto add_ld = [&](const int* p, size_t len) { if (p && r.nl < 12) { r.lo[r.nl] = p; r.hi[r.nl++] = p + len; } };
     auto add_red = [&](const int* p, size_t len) { if (p && r.nr < 4) { r.rlo[r.nr] = p; r.rhi[r.nr++] = p + len; } };
     add_red(c->xb.p, c->xb.n); add_red(c->f1.p, c->f1.n); add_red(c->hacc, (size_t)acc_len(c->HT));
     add_ld(c->xb.p, c->xb.n); add_ld(c->f1.p, c->f1.n); add_ld(c->gb.p, c->gb.n);
-    add_ld(c->G_hub.p, c->G_hub.n); add_ld(c->hub_id.p, c->hub_id.n); add_ld(c->csr_cols.p, c->csr_cols.n);
+    add_ld(c->G_hub.p, c->G_hub.n); add_ld(c->hub_id.p, c->hub_id.n); add_ld(c->colsp, (size_t)c->csr_local);
     add_ld(c->span_row.p, c->span_row.n);
     CUDA_TRY(cudaMemcpyToSymbolAsync(g_chk, &r, sizeof r, 0, cudaMemcpyHostToDevice, st));
   }
@@ -1790,45 +2018,64 @@ static int solve_body(fsv_ctx* c, const fsv_config* cfg, int32_t* snapshots, int
   if (c->profile && (rc = ensure_pevents(c, 2 * kPev))) return rc;
 
   // graph mode: the whole iteration loop is one conditional-WHILE graph launch
-  const bool graph_mode = c->use_graph && !snapshots && !c->profile && !c->comm && d.batch == 0;
+  const bool graph_mode = count == 1 && c->use_graph && !snapshots && !c->profile && !c->comm && d.batch == 0;
   if (graph_mode && (rc = ensure_graph(c, cap))) return rc;
   CUDA_TRY(cudaEventRecord(c->events[0], st));
-  k_solve_init<<<grid_for(c, std::max<long long>(c->HT, (long long)cap * NCOUNT), 256), 256, 0, st>>>(
-      c->X, c->Y, c->G, c->n, c->hacc, c->HT, c->cnt.p, (long long)cap * NCOUNT, c->done.p,
-      c->ticket.p, c->mode.p, c->policy == 2 ? 1 : 0, c->tstamp.p, c->rep.p);
+  for (int r = 0; r < count; ++r) {
+    fsv_ctx* x = cs[r];
+    k_solve_init<<<grid_for(x, std::max<long long>(x->HT, (long long)cap * NCOUNT), 256), 256, 0, st>>>(
+        x->X, x->Y, x->G, x->n, x->hacc, x->HT, x->cnt.p, (long long)cap * NCOUNT, x->done.p,
+        x->ticket.p, x->mode.p, x->policy == 2 ? 1 : 0, x->tstamp.p, x->rep.p);
+  }
   pmark(c, 1, 6);
   // iteration 1 in closed form: f_1[u] = min(u, smallest neighbour) from the
-  // resident CSR rows (first column of each sorted row), every solve
-  if (c->n && !c->comm && c->row_begin == 0 && c->row_end == c->n) {
+  // resident CSR rows (first column of each sorted row), every solve; a
+  // partitioned graph assembles it from the ranks' rows by a min-merge
+  const bool dist = c->comm != nullptr || count > 1;
+  if (c->n && !dist && c->row_begin == 0 && c->row_end == c->n) {
     if (c->off32)
-      k_f1_solve<int><<<grid_for(c, c->n / 4 + 1, 256, 32), 256, 0, st>>>(c->csr_off32.p, c->csr_cols.p,
+      k_f1_solve<int><<<grid_for(c, c->n / 4 + 1, 256, 32), 256, 0, st>>>(c->csr_off32.p, c->colsp,
                                                                         c->n, c->f1.p);
     else
-      k_f1_solve<int64_t><<<grid_for(c, c->n / 4 + 1, 256, 32), 256, 0, st>>>(c->csr_off.p, c->csr_cols.p,
+      k_f1_solve<int64_t><<<grid_for(c, c->n / 4 + 1, 256, 32), 256, 0, st>>>(c->offp, c->colsp,
                                                                             c->n, c->f1.p);
     ++c->launches;
   } else if (c->n) {
-    k_f1<int><<<grid_for(c, c->n, 256, 64), 256, 0, st>>>(c->csr_off.p, c->csr_cols.p, c->col_base,
-                                                      c->row_begin, c->row_end, c->n, c->f1.p,
-                                                      c->comm != nullptr);
-    ++c->launches;
+    for (int r = 0; r < count; ++r) {
+      fsv_ctx* x = cs[r];
+      k_f1<int><<<grid_for(x, x->n, 256, 64), 256, 0, st>>>(x->offp, x->colsp, x->col_base,
+                                                        x->row_begin, x->row_end, x->n, x->f1.p, dist);
+      ++x->launches;
+    }
     if (c->comm) {
       NCCL_TRY(g_nccl.AllReduce(c->f1.p, c->f1.p, (size_t)c->n, ncclInt32, ncclMin, c->comm, st));
-      k_f1_fix<<<grid_for(c, c->n, 256), 256, 0, st>>>(c->f1.p, c->n);
+    } else if (count > 1) {
+      MergeArgs m{};
+      for (int r = 0; r < count; ++r) m.buf[r] = cs[r]->f1.p;
+      m.count = count;
+      m.n = c->n;
+      m.done = nullptr;
+      k_group_min_merge<<<grid_for(c, c->n, 256), 256, 0, st>>>(m);
       ++c->launches;
     }
+    if (dist)
+      for (int r = 0; r < count; ++r) {
+        k_f1_fix<<<grid_for(cs[r], cs[r]->n, 256), 256, 0, st>>>(cs[r]->f1.p, cs[r]->n);
+        ++cs[r]->launches;
+      }
   }
-  {
+  for (int r = 0; r < count; ++r) {
+    fsv_ctx* x = cs[r];
     FirstArgs fa;
-    fa.f1 = c->f1.p; fa.G = c->G; fa.X = c->X; fa.n = c->n;
-    fa.hub_id = c->hub_id.p; fa.G_hub = c->G_hub.p; fa.H = c->HT; fa.cnt = c->cnt.p;
-    fa.partials = c->partials.p; fa.ticket = c->ticket.p; fa.done = c->done.p; fa.max_iter = cap;
-    fa.dl = delta_out(c);
-    fa.lc = loop_ctl(c, graph_mode ? 2 : 0);
-    k_first<<<vertex_grid(c), SC_THREADS, 0, st>>>(fa);
+    fa.f1 = x->f1.p; fa.G = x->G; fa.X = x->X; fa.n = x->n;
+    fa.hub_id = x->hub_id.p; fa.G_hub = x->G_hub.p; fa.H = x->HT; fa.cnt = x->cnt.p;
+    fa.partials = x->partials.p; fa.ticket = x->ticket.p; fa.done = x->done.p; fa.max_iter = cap;
+    fa.dl = delta_out(x);
+    fa.lc = loop_ctl(x, graph_mode ? 2 : 0);
+    k_first<<<vertex_grid(x), SC_THREADS, 0, st>>>(fa);
+    x->launches += 2;
   }
   pmark(c, 1, 7);
-  c->launches += 2;
   if ((rc = ensure_events(c, 2))) return rc;
   CUDA_TRY(cudaEventRecord(c->events[1], st));
   if (snapshots) {
@@ -1858,7 +2105,6 @@ static int solve_body(fsv_ctx* c, const fsv_config* cfg, int32_t* snapshots, int
       const int passes = std::max(1, (it - 1 + FSV_GRAPH_BODY - 1) / FSV_GRAPH_BODY);
       c->launches += (FSV_GRAPH_IF ? std::max(1, it - 1) : passes * FSV_GRAPH_BODY) * per_it;
     }
-
   }
   bool first_round = true;
   while (!graph_mode) {
@@ -1867,7 +2113,7 @@ static int solve_body(fsv_ctx* c, const fsv_config* cfg, int32_t* snapshots, int
     first_round = false;
     const int upto = std::min(cap, launched + more);
     for (int k = launched + 1; k <= upto; ++k) {
-      if ((rc = launch_iteration(c, k, cap))) return rc;
+      if ((rc = launch_group_iteration(cs, count, k, cap))) return rc;
       if ((rc = ensure_events(c, (size_t)k + 1))) return rc;
       CUDA_TRY(cudaEventRecord(c->events[k], st));
     }
@@ -1891,24 +2137,55 @@ static int solve_body(fsv_ctx* c, const fsv_config* cfg, int32_t* snapshots, int
   CUDA_TRY(cudaGetLastError());
   if (done < 0) return fail(FSV_ERR_RUNTIME, "did not converge within %d iterations", -done);
   const int iters = done;
-  c->iterations = iters;
-  c->h_cnt.assign((size_t)iters * NCOUNT, 0ull);
-  c->h_mode.assign((size_t)iters + 1, 0);
-  std::vector<unsigned long long> ts((size_t)iters + 1, 0ull);
-  if (graph_mode && iters <= staged) {
-    std::copy(c->h_rep->cnt, c->h_rep->cnt + (size_t)iters * NCOUNT, c->h_cnt.begin());
-    std::copy(c->h_rep->mode, c->h_rep->mode + iters + 1, c->h_mode.begin());
-    std::copy(c->h_rep->ts, c->h_rep->ts + iters + 1, ts.begin());
-  } else {
-    CUDA_TRY(cudaMemcpy(c->h_cnt.data(), c->cnt.p, sizeof(unsigned long long) * iters * NCOUNT,
-                        cudaMemcpyDeviceToHost));
-    CUDA_TRY(cudaMemcpy(c->h_mode.data(), c->mode.p, sizeof(int) * (iters + 1), cudaMemcpyDeviceToHost));
-    CUDA_TRY(cudaMemcpy(ts.data(), c->tstamp.p, sizeof(unsigned long long) * (iters + 1),
-                        cudaMemcpyDeviceToHost));
-  }
-  c->iter_ms.assign(iters, 0.f);
-  for (int k = 1; k <= iters; ++k) c->iter_ms[k - 1] = (float)((double)(ts[k] - ts[k - 1]) * 1e-6);
   CUDA_TRY(cudaEventElapsedTime(&c->solve_ms, c->events[0], c->events[graph_mode ? 2 : iters]));
+  for (int r = 0; r < count; ++r) {
+    fsv_ctx* x = cs[r];
+    int xdone = done;
+    if (r > 0) {
+      CUDA_TRY(cudaMemcpy(&xdone, x->done.p, sizeof(int), cudaMemcpyDeviceToHost));
+      if (xdone != done)
+        return fail(FSV_ERR_INVARIANT, "rank %d stopped at iteration %d, rank 0 at %d", r, xdone, done);
+    }
+    x->iterations = iters;
+    x->solve_ms = c->solve_ms;
+    x->h_cnt.assign((size_t)iters * NCOUNT, 0ull);
+    x->h_mode.assign((size_t)iters + 1, 0);
+    std::vector<unsigned long long> ts((size_t)iters + 1, 0ull);
+    if (graph_mode && iters <= staged) {
+      std::copy(x->h_rep->cnt, x->h_rep->cnt + (size_t)iters * NCOUNT, x->h_cnt.begin());
+      std::copy(x->h_rep->mode, x->h_rep->mode + iters + 1, x->h_mode.begin());
+      std::copy(x->h_rep->ts, x->h_rep->ts + iters + 1, ts.begin());
+    } else {
+      CUDA_TRY(cudaMemcpy(x->h_cnt.data(), x->cnt.p, sizeof(unsigned long long) * iters * NCOUNT,
+                          cudaMemcpyDeviceToHost));
+      CUDA_TRY(cudaMemcpy(x->h_mode.data(), x->mode.p, sizeof(int) * (iters + 1), cudaMemcpyDeviceToHost));
+      CUDA_TRY(cudaMemcpy(ts.data(), x->tstamp.p, sizeof(unsigned long long) * (iters + 1),
+                          cudaMemcpyDeviceToHost));
+    }
+    x->iter_ms.assign(iters, 0.f);
+    for (int k = 1; k <= iters; ++k) x->iter_ms[k - 1] = (float)((double)(ts[k] - ts[k - 1]) * 1e-6);
+    x->components = (int)x->h_cnt[(size_t)(iters - 1) * NCOUNT + C_ROOTS];
+    x->labels_ready = 1;
+  }
+  // the pushed-entry count (trace flops of a sparse iteration) is rank-local:
+  // every rank reports the group's sum
+  if (count > 1)
+    for (int k = 0; k < iters; ++k) {
+      unsigned long long sum = 0;
+      for (int r = 0; r < count; ++r) sum += cs[r]->h_cnt[(size_t)k * NCOUNT + C_FLOPS];
+      for (int r = 0; r < count; ++r) cs[r]->h_cnt[(size_t)k * NCOUNT + C_FLOPS] = sum;
+    }
+  if (c->comm && c->nranks > 1 && iters > 0) {
+    DBuf<unsigned long long> fl;
+    CUDA_TRY(fl.alloc((size_t)iters));
+    std::vector<unsigned long long> h((size_t)iters);
+    for (int k = 0; k < iters; ++k) h[(size_t)k] = c->h_cnt[(size_t)k * NCOUNT + C_FLOPS];
+    CUDA_TRY(cudaMemcpyAsync(fl.p, h.data(), sizeof(unsigned long long) * iters, cudaMemcpyHostToDevice, st));
+    NCCL_TRY(g_nccl.AllReduce(fl.p, fl.p, (size_t)iters, ncclUint64, ncclSum, c->comm, st));
+    CUDA_TRY(cudaMemcpyAsync(h.data(), fl.p, sizeof(unsigned long long) * iters, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    for (int k = 0; k < iters; ++k) c->h_cnt[(size_t)k * NCOUNT + C_FLOPS] = h[(size_t)k];
+  }
   if (c->profile) {
     auto span = [&](int k, int a, int b) {
       float ms = 0.f;
@@ -1929,8 +2206,6 @@ static int solve_body(fsv_ctx* c, const fsv_config* cfg, int32_t* snapshots, int
       c->shortcut_ms += span(k, 6, 7);
     }
   }
-  c->components = (int)c->h_cnt[(size_t)(iters - 1) * NCOUNT + C_ROOTS];
-  c->labels_ready = 1;
   for (int k = 0; k < iters; ++k)
     if (c->h_cnt[(size_t)k * NCOUNT + C_VIOL])
       return fail(FSV_ERR_INVARIANT, "parent vector increased during kernel iteration");
@@ -1969,6 +2244,122 @@ extern "C" int fsv_solve(fsv_ctx* c, const fsv_config* cfg, fsv_stats* stats) {
   return rc;
 }
 
+// ---- Labeling on the device (labeling_from_parents, graph.py:109-125) -----
+// The star check and the component count come from the last vertex pass
+// (C_NONSTAR, C_ROOTS). Sizes: warp-aggregated counts per representative
+// (the giant component of a skewed graph would otherwise serialise one
+// counter), then the representatives (label[u] == u, ascending) compacted
+// with their sizes, and the labels widened to int64 (the reference's ID_DTYPE).
+__global__ void k_comp_sizes(const int* __restrict__ L, long long n, unsigned* __restrict__ cnt) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long base = (long long)blockIdx.x * blockDim.x; base < n; base += stride) {  // block-uniform
+    const long long u = base + threadIdx.x;
+    const bool on = u < n;
+    const int l = on ? __ldg(L + u) : -1;
+    const unsigned active = __ballot_sync(0xffffffffu, on);
+    if (on) {
+      const unsigned peers = __match_any_sync(active, l);
+      if ((int)(threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(cnt + l, (unsigned)__popc(peers));
+    }
+  }
+}
+
+struct IsRoot {
+  const int* L;
+  __device__ __forceinline__ bool operator()(int u) const { return __ldg(L + u) == u; }
+};
+
+__global__ void k_comp_out(const int* __restrict__ reps32, const int* __restrict__ num, const unsigned* __restrict__ cnt,
+                           int64_t* __restrict__ reps, int64_t* __restrict__ sizes) {
+  const long long C = *num;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < C; i += (long long)gridDim.x * blockDim.x) {
+    const int r = reps32[i];
+    reps[i] = r;
+    sizes[i] = cnt[r];
+  }
+}
+
+__global__ void k_widen(const int* __restrict__ in, long long n, int64_t* __restrict__ out) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    out[i] = in[i];
+}
+
+static int build_labeling(fsv_ctx* c) {
+  if (c->labeling_ready) return FSV_OK;
+  const long long n = c->n;
+  cudaStream_t st = c->stream;
+  const int* L = c->labels_src ? c->labels_src : c->G;
+  CUDA_TRY(c->lab.cnt.alloc((size_t)std::max<long long>(n, 1)));
+  CUDA_TRY(c->lab.reps32.alloc((size_t)std::max<long long>(n, 1) + 1));   // + selected count
+  CUDA_TRY(c->lab.reps.alloc((size_t)std::max<long long>(n, 1)));
+  CUDA_TRY(c->lab.sizes.alloc((size_t)std::max<long long>(n, 1)));
+  CUDA_TRY(c->lab.labels.alloc((size_t)std::max<long long>(n, 1)));
+  int* d_num = c->lab.reps32.p + std::max<long long>(n, 1);
+  CUDA_TRY(cudaMemsetAsync(c->lab.cnt.p, 0, sizeof(unsigned) * (size_t)std::max<long long>(n, 1), st));
+  CUDA_TRY(cudaMemsetAsync(d_num, 0, sizeof(int), st));
+  if (n) {
+    k_comp_sizes<<<grid_for(c, n, 256), 256, 0, st>>>(L, n, c->lab.cnt.p);
+    size_t bytes = 0;
+    thrust::counting_iterator<int> ids(0);
+    CUDA_TRY(cub::DeviceSelect::If(nullptr, bytes, ids, c->lab.reps32.p, d_num, (int)n, IsRoot{L}, st));
+    CUDA_TRY(c->lab.tmp.alloc(std::max<size_t>(bytes, 1)));
+    CUDA_TRY(cub::DeviceSelect::If(c->lab.tmp.p, bytes, ids, c->lab.reps32.p, d_num, (int)n, IsRoot{L}, st));
+    k_comp_out<<<grid_for(c, n, 256), 256, 0, st>>>(c->lab.reps32.p, d_num, c->lab.cnt.p, c->lab.reps.p,
+                                                     c->lab.sizes.p);
+    k_widen<<<grid_for(c, n, 256), 256, 0, st>>>(L, n, c->lab.labels.p);
+  }
+  int num = 0;
+  CUDA_TRY(cudaMemcpyAsync(&num, d_num, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  c->lab.count = num;
+  c->labeling_ready = true;
+  return FSV_OK;
+}
+
+extern "C" int fsv_get_labeling(fsv_ctx* c, int64_t* labels, int64_t* reps, int64_t* sizes, int64_t cap,
+                                int64_t* count) {
+  if (!c || !c->labels_ready) return fail(FSV_ERR_CONTRACT, "no solve result available");
+  CUDA_TRY(cudaSetDevice(c->device));
+  int rc = build_labeling(c);
+  if (rc) return rc;
+  const long long C = c->lab.count;
+  if (count) *count = C;
+  if ((reps || sizes) && cap < C)
+    return fail(FSV_ERR_CONTRACT, "capacity %lld < %lld components", (long long)cap, C);
+  cudaStream_t st = c->stream;
+  if (labels && c->n)
+    CUDA_TRY(cudaMemcpyAsync(labels, c->lab.labels.p, sizeof(int64_t) * c->n, cudaMemcpyDeviceToHost, st));
+  if (reps && C) CUDA_TRY(cudaMemcpyAsync(reps, c->lab.reps.p, sizeof(int64_t) * C, cudaMemcpyDeviceToHost, st));
+  if (sizes && C) CUDA_TRY(cudaMemcpyAsync(sizes, c->lab.sizes.p, sizeof(int64_t) * C, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  return FSV_OK;
+}
+
+// Emulated rank group (tests): `count` contexts on one device, each holding
+// one row range of the same graph, solved in lockstep with a device min-merge
+// in place of the allreduce; see include/fastsv.h.
+extern "C" int fsv_group_solve(fsv_ctx* const* ctxs, int count, const fsv_config* cfg, fsv_stats* stats) {
+  if (!ctxs) return fail(FSV_ERR_CONTRACT, "NULL context array");
+  int rc = solve_impl_group(ctxs, count, cfg, nullptr, 0);
+  if (ctxs[0] && count >= 1) fill_stats(ctxs[0], stats);
+  return rc;
+}
+
+extern "C" int fsv_group_run_snapshots(fsv_ctx* const* ctxs, int count, const fsv_config* cfg, int32_t* labels,
+                                       int32_t* iterations, int64_t* gfc, int64_t* fc, int32_t* snapshots,
+                                       int32_t snap_cap) {
+  if (!ctxs) return fail(FSV_ERR_CONTRACT, "NULL context array");
+  if (!snapshots) return fail(FSV_ERR_CONTRACT, "snapshots is NULL");
+  int rc = solve_impl_group(ctxs, count, cfg, snapshots, snap_cap);
+  fsv_ctx* c = ctxs[0];
+  if (c && c->labels_ready) {
+    if (iterations) *iterations = c->iterations;
+    fsv_get_trace(c, gfc, fc, nullptr, snap_cap);
+  }
+  if (rc) return rc;
+  return labels ? fsv_get_labels(c, labels) : FSV_OK;
+}
+
 extern "C" int fsv_get_labels(fsv_ctx* c, int32_t* labels) {
   if (!c || !c->labels_ready) return fail(FSV_ERR_CONTRACT, "no solve result available");
   if (!c->n) return FSV_OK;
@@ -1983,6 +2374,7 @@ extern "C" int fsv_get_labels(fsv_ctx* c, int32_t* labels) {
 extern "C" int fsv_get_labels64(fsv_ctx* c, int64_t* labels) {
   if (!c || !c->labels_ready) return fail(FSV_ERR_CONTRACT, "no solve result available");
   if (!c->n) return FSV_OK;
+  if (!labels) return fail(FSV_ERR_CONTRACT, "labels is NULL");
   std::vector<int32_t> tmp((size_t)c->n);
   int rc = fsv_get_labels(c, tmp.data());
   if (rc) return rc;

@@ -22,7 +22,7 @@ import numpy as np
 from . import _native
 from ._native import FsvConfig, FsvStats
 from .errors import DeviceError, InputError, raise_for_status
-from .graph import ID_DTYPE, CsrGraph, Labeling, labeling_from_parents
+from .graph import ID_DTYPE, ComponentSizes, CsrGraph, Labeling
 
 _FORCE_MODES = ("auto", "dense_only", "sparse_only")
 
@@ -217,6 +217,21 @@ class Solver:
         _check(fn(self._ctx, int(n), ctypes.c_void_p(offsets_ptr), ctypes.c_void_p(cols_ptr),
                   int(row_begin), int(n if row_end is None else row_end)))
         self.n = int(n)
+        # CsrGraph.m: stored directed entries = row_offsets[n] (graph.py:34-37)
+        self.m = int(ctypes.c_int64.from_address(int(offsets_ptr) + 8 * int(n)).value)
+
+    def upload_device(self, n: int, offsets_ptr: int, cols_ptr: int, row_begin: int = 0,
+                      row_end: int | None = None, m: int | None = None) -> None:
+        """Build the layout from a CSR already in device memory (int64 offsets
+        of the full graph, int32 columns of rows [row_begin, row_end)). The
+        arrays are borrowed, not copied: keep them alive and unchanged until
+        the next upload or close() (fsv_upload_csr_device)."""
+        _check(self._lib.fsv_upload_csr_device(self._ctx, int(n), ctypes.c_void_p(int(offsets_ptr)),
+                                               ctypes.c_void_p(int(cols_ptr)), int(row_begin),
+                                               int(n if row_end is None else row_end)))
+        self.n = int(n)
+        if m is not None:
+            self.m = int(m)
 
     # -- solve ------------------------------------------------------------
     @staticmethod
@@ -244,11 +259,34 @@ class Solver:
         return self.stats
 
     def labels(self, out: np.ndarray | None = None) -> np.ndarray:
+        """Labels of the last solve: int32 (device id type) by default, int64
+        (widened on the device) when ``out`` is an int64 array."""
         if out is None:
             out = np.empty(self.n, dtype=np.int32)
-        fn = self._lib.fsv_get_labels if out.dtype == np.int32 else self._lib.fsv_get_labels64
-        _check(fn(self._ctx, out.ctypes.data if out.size else None))
+        if out.dtype == np.int32:
+            _check(self._lib.fsv_get_labels(self._ctx, out.ctypes.data if out.size else None))
+        else:
+            cnt = ctypes.c_int64(0)
+            _check(self._lib.fsv_get_labeling(self._ctx, out.ctypes.data if out.size else None, None, None, 0,
+                                              ctypes.byref(cnt)))
         return out
+
+    def labeling(self) -> Labeling:
+        """The reference's Labeling (graph.py:100-125) of the last solve, built
+        on the device: int64 labels, component count, and the sizes of the
+        components (fsv_get_labeling); no host pass over n."""
+        cnt = ctypes.c_int64(0)
+        _check(self._lib.fsv_get_labeling(self._ctx, None, None, None, 0, ctypes.byref(cnt)))
+        c = int(cnt.value)
+        labels = np.empty(self.n, dtype=ID_DTYPE)
+        reps = np.empty(c, dtype=ID_DTYPE)
+        sizes = np.empty(c, dtype=ID_DTYPE)
+        _check(self._lib.fsv_get_labeling(self._ctx, labels.ctypes.data if self.n else None,
+                                          reps.ctypes.data if c else None, sizes.ctypes.data if c else None,
+                                          c, ctypes.byref(cnt)))
+        for a in (labels, reps, sizes):
+            a.flags.writeable = False
+        return Labeling(labels=labels, component_count=c, sizes=ComponentSizes(reps, sizes))
 
     def labels_into(self, ptr: int) -> None:
         _check(self._lib.fsv_get_labels(self._ctx, ctypes.c_void_p(ptr)))
@@ -268,12 +306,13 @@ class Solver:
         return gfc[:k], fc[:k], ms[:k]
 
     def run(self, batch: int = 0, max_iters: int = 0, snapshots: bool = False, snap_cap: int = 256,
-            policy: int = 0, threshold: float = 0.1, full_trace: bool = False, hooking: int = 0):
-        """Solve + copy out: (labels int32, iterations, gf_changed, f_changed,
-        per-iteration ms, snapshots or None[, kernel, flops])."""
+            policy: int = 0, threshold: float = 0.1, full_trace: bool = False, hooking: int = 0,
+            with_labels: bool = True):
+        """Solve + copy out: (labels int32 or None, iterations, gf_changed,
+        f_changed, per-iteration ms, snapshots or None[, kernel, flops])."""
         cfg = self._config(batch, max_iters, False, policy, threshold, hooking)
         n = self.n
-        labels = np.empty(n, dtype=np.int32)
+        labels = np.empty(n if with_labels else 0, dtype=np.int32)
         iters = ctypes.c_int32(0)
         if snapshots:
             cap = int(snap_cap)
@@ -281,19 +320,55 @@ class Solver:
             gfc = np.zeros(cap, dtype=np.int64)
             fc = np.zeros(cap, dtype=np.int64)
             _check(self._lib.fsv_run_snapshots(self._ctx, ctypes.byref(cfg),
-                                               labels.ctypes.data if n else None, ctypes.byref(iters),
+                                               labels.ctypes.data if n and with_labels else None,
+                                               ctypes.byref(iters),
                                                gfc.ctypes.data, fc.ctypes.data,
                                                snap.ctypes.data if n else ctypes.c_void_p(1), cap))
         else:
             _check(self._lib.fsv_solve(self._ctx, ctypes.byref(cfg), ctypes.byref(self.stats)))
             iters.value = self.stats.iterations
-            if n:
+            if n and with_labels:
                 self.labels(labels)
             snap = None
         k = int(iters.value)
         gfc2, fc2, ms, kern, flops = self.trace(k, full=True)
-        out = (labels, k, gfc2, fc2, ms, (snap[:k] if snap is not None else None))
+        out = (labels if with_labels else None, k, gfc2, fc2, ms, (snap[:k] if snap is not None else None))
         return out + (kern, flops) if full_trace else out
+
+
+def group_run(solvers, snapshots: bool = False, snap_cap: int = 256, policy: int = 0,
+              threshold: float = 0.1, batch: int = 0):
+    """Emulated rank group on one device (fsv_group_solve): each Solver holds
+    one row range of the same graph (``upload(g, lo, hi, cols)``); the group
+    is solved in lockstep with a device min-merge in place of the NCCL
+    allreduce, running the rank-partitioned kernels. Returns rank 0's
+    (labels, iterations, gf_changed, f_changed, snapshots or None, kernel,
+    flops) and every rank's labels."""
+    lib = _native.fastsv_lib()
+    arr = (ctypes.c_void_p * len(solvers))(*[s._ctx.value for s in solvers])
+    cfg = Solver._config(batch, 0, False, policy, threshold, 0)
+    s0 = solvers[0]
+    n = s0.n
+    if snapshots:
+        cap = int(snap_cap)
+        snap = np.empty((cap, n), dtype=np.int32)
+        gfc = np.zeros(cap, dtype=np.int64)
+        fc = np.zeros(cap, dtype=np.int64)
+        labels = np.empty(n, dtype=np.int32)
+        iters = ctypes.c_int32(0)
+        _check(lib.fsv_group_run_snapshots(arr, len(solvers), ctypes.byref(cfg),
+                                           labels.ctypes.data if n else None, ctypes.byref(iters),
+                                           gfc.ctypes.data, fc.ctypes.data,
+                                           snap.ctypes.data if n else ctypes.c_void_p(1), cap))
+        k = int(iters.value)
+        snap = snap[:k]
+    else:
+        _check(lib.fsv_group_solve(arr, len(solvers), ctypes.byref(cfg), ctypes.byref(s0.stats)))
+        k = int(s0.stats.iterations)
+        snap = None
+    gfc, fc, _, kern, flops = s0.trace(k, full=True)
+    all_labels = [s.labels() for s in solvers]
+    return all_labels[0], k, gfc, fc, snap, kern, flops, all_labels
 
 
 _solvers: dict = {}
@@ -307,6 +382,7 @@ def default_solver(device: int = 0) -> Solver:
     return s
 
 
+TRACE_CAP = 4096   # iteration cap of the device trace (kTraceCap in csrc/fastsv.cu)
 _POLICY = {"auto": 3, "dense_only": 1, "sparse_only": 2}
 _KIND = {0: "dense", 1: "sparse", 2: "none"}
 
@@ -323,7 +399,7 @@ def hooking_code(cfg: "HookingConfig") -> int:
             | (HOOK_EARLY_TERMINATION if cfg.early_termination else 0))
 
 
-def _result(g, labels, iters, gfc, fc, ms, snaps, kern, flops) -> RunResult:
+def _result(labeling, iters, gfc, fc, ms, snaps, kern, flops) -> RunResult:
     trace = [IterationTrace(iteration=i + 1, gf_changed=int(gfc[i]), f_changed=int(fc[i]),
                             kernel=_KIND.get(int(kern[i]), "dense"),
                             elapsed=float(ms[i]) / 1e3, flops=int(flops[i]))
@@ -335,18 +411,30 @@ def _result(g, labels, iters, gfc, fc, ms, snaps, kern, flops) -> RunResult:
             a = s.astype(ID_DTYPE)
             a.flags.writeable = False
             snapshots.append(a)
-    return RunResult(labeling=labeling_from_parents(labels.astype(ID_DTYPE)), iterations=int(iters),
-                     trace=trace, snapshots=snapshots)
+    return RunResult(labeling=labeling, iterations=int(iters), trace=trace, snapshots=snapshots)
 
 
 def _solve_graph(g, record_snapshots: bool, batch: int, device: int, policy: int = 0,
                  threshold: float = 0.1, hooking: int = 0) -> RunResult:
     solver = default_solver(device)
     solver.upload(g)
-    labels, iters, gfc, fc, ms, snaps, kern, flops = solver.run(
-        batch=batch, snapshots=record_snapshots, snap_cap=max(64, 4 * int(np.log2(max(g.n, 2))) + 16),
-        policy=policy, threshold=threshold, full_trace=True, hooking=hooking)
-    return _result(g, labels, iters, gfc, fc, ms, snaps, kern, flops)
+    # the reference records snapshots without a limit (driver.py:109-112):
+    # start from a bound that covers FastSV's O(log n) iterations and grow it
+    # for slow-converging variants (sv1..sv4) until the trace cap
+    cap = max(64, 4 * int(np.log2(max(g.n, 2))) + 16)
+    while True:
+        try:
+            _, iters, gfc, fc, ms, snaps, kern, flops = solver.run(
+                batch=batch, snapshots=record_snapshots, snap_cap=cap, policy=policy,
+                threshold=threshold, full_trace=True, hooking=hooking, with_labels=False)
+            break
+        except ValueError as e:
+            if not record_snapshots or "iterations ran" not in str(e) or cap >= TRACE_CAP:
+                raise
+            cap = min(4 * cap, TRACE_CAP)
+    # Labeling (labels, count, sizes) built on the device; the star check ran
+    # in the final vertex pass (graph.py:109-125)
+    return _result(solver.labeling(), iters, gfc, fc, ms, snaps, kern, flops)
 
 
 def fastsv_la(g, cfg: DriverConfig | None = None, record_snapshots: bool = False,

@@ -10,6 +10,7 @@ also accepts a reference ``svcc.CsrGraph`` with int64 columns unchanged.
 
 from __future__ import annotations
 
+from collections.abc import Mapping
 from dataclasses import dataclass, field
 from functools import cached_property
 
@@ -94,6 +95,55 @@ def build_csr(n, edges) -> CsrGraph:
     offsets.flags.writeable = False
     cols.flags.writeable = False
     return CsrGraph(n=int(n), row_offsets=offsets, col_indices=cols)
+
+
+class ComponentSizes(Mapping):
+    """``Labeling.sizes`` (representative -> vertex count) backed by the arrays
+    the device computed (fsv_get_labeling): representatives ascending, sizes
+    aligned. Behaves as the reference's read-only dict (lookup, iteration in
+    ascending representative order, len, equality with a dict); a dict is
+    only built when one is iterated as items."""
+
+    __slots__ = ("_reps", "_counts")
+
+    def __init__(self, reps: np.ndarray, counts: np.ndarray):
+        self._reps = reps
+        self._counts = counts
+
+    @property
+    def representatives(self) -> np.ndarray:
+        return self._reps
+
+    @property
+    def counts(self) -> np.ndarray:
+        return self._counts
+
+    def __getitem__(self, key):
+        i = int(np.searchsorted(self._reps, key))
+        if i < self._reps.size and self._reps[i] == key:
+            return int(self._counts[i])
+        raise KeyError(key)
+
+    def __len__(self):
+        return int(self._reps.size)
+
+    def __iter__(self):
+        return iter(self._reps.tolist())
+
+    def items(self):
+        return zip(self._reps.tolist(), self._counts.tolist())
+
+    def __eq__(self, other):
+        if isinstance(other, ComponentSizes):
+            return np.array_equal(self._reps, other._reps) and np.array_equal(self._counts, other._counts)
+        if isinstance(other, Mapping):
+            return len(self) == len(other) and dict(self.items()) == dict(other.items())
+        return NotImplemented
+
+    __hash__ = None
+
+    def __repr__(self):
+        return f"ComponentSizes({len(self)} components)"
 
 
 @dataclass(frozen=True)

@@ -36,6 +36,18 @@ def record(n, edges):
 
 
 def main():
+    path = HERE / "csr_digests.json"
+    if len(sys.argv) > 2 and sys.argv[1] == "--configs":
+        # add (or refresh) BASELINE configs only, keeping the rest:
+        #   python tests/golden/make_csr_golden.py --configs 2 4   (minutes each)
+        out = json.loads(path.read_text())
+        for index in map(int, sys.argv[2:]):
+            t = time.time()
+            n, pairs = gen.baseline_graph(index)
+            out["configs"][str(index)] = dict(record(n, pairs), pairs_digest=gen.pairs_digest(pairs))
+            print(f"config {index}: reference build_csr {time.time() - t:.1f} s", flush=True)
+        path.write_text(json.dumps(out, indent=0) + "\n")
+        return
     out = {"suite": {}, "configs": {}}
     for c in load_suite():
         out["suite"][c.name] = record(c.n, c.edges.reshape(-1, 2))
@@ -44,7 +56,7 @@ def main():
         n, pairs = gen.baseline_graph(index)
         out["configs"][str(index)] = dict(record(n, pairs), pairs_digest=gen.pairs_digest(pairs))
         print(f"config {index}: reference build_csr {time.time() - t:.1f} s", flush=True)
-    (HERE / "csr_digests.json").write_text(json.dumps(out, indent=0) + "\n")
+    path.write_text(json.dumps(out, indent=0) + "\n")
     print(f"{len(out['suite'])} suite graphs, configs {list(out['configs'])}")
 
 

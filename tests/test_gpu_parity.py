@@ -467,3 +467,50 @@ def test_graph_reuse_across_uploads_of_the_same_shape(solver):
             labels, iters, gfc, fc, ms, _ = solver.run()
             assert iters == o.iterations and gfc.tolist() == o.gf_changed.tolist(), rep
             assert np.array_equal(labels, o.labels), rep
+
+
+def test_device_labeling_matches_reference_labeling(solver):
+    """Labeling built on the device (fsv_get_labeling: int64 labels, count,
+    sizes) equals the reference's labeling_from_parents (graph.py:109-125)
+    on the golden suite and on skewed/forest graphs."""
+    graphs = [(c.n, c.edges) for c in load_suite()[::3]]
+    graphs += [gen.rmat(14, 16, seed=9), gen.forest(3000, 1, 64, 2, seed=2), (1, []), (7, [])]
+    for n, e in graphs:
+        g = fb.build_csr(n, e)
+        solver.set_hub_slots(0)
+        solver.upload(g)
+        solver.solve()
+        lab = solver.labeling()
+        ref = fb.labeling_from_parents(solver.labels().astype(np.int64))
+        assert lab.labels.dtype == np.int64 and np.array_equal(lab.labels, ref.labels)
+        assert lab.component_count == ref.component_count
+        assert lab.sizes == ref.sizes and dict(lab.sizes.items()) == ref.sizes
+        assert sum(lab.sizes.values()) == n
+        if n:
+            r = int(lab.labels[0])
+            assert lab.sizes[r] == ref.sizes[r]
+    r = fb.fastsv_la(fb.build_csr(6, [(0, 1), (1, 2), (0, 2), (3, 4), (4, 5), (3, 5)]))
+    assert r.labeling.sizes == {0: 3, 3: 3} and r.labeling.component_count == 2
+
+
+def test_config5_full_size_matches_oracle_record():
+    """BASELINE config 5 (RMAT-27: 2^31 pairs, ~4.2e9 directed entries, int64
+    offsets) on one B200: the edge list goes up, the CSR is built on the
+    device (fsv_upload_edges), and the solve must reproduce the golden record
+    of the C oracle (tests/golden/make_config5_golden.py; the Python
+    reference is infeasible at this size): iteration count,
+    gf_changed / f_changed per iteration, component count, label digest."""
+    rec = load_configs().get(5)
+    if rec is None:
+        pytest.skip("tests/golden/configs.json has no config 5 record yet")
+    n, pairs = gen.baseline_graph(5)
+    assert gen.pairs_digest(pairs) == rec["pairs_digest"]
+    with fb.Solver(0) as solver:       # its own context: ~60 GB of device memory, freed after
+        solver.upload_edges(n, pairs)
+        del pairs
+        assert solver.m == rec["m_dir"]
+        labels, iters, gfc, fc, ms, _ = solver.run()
+        assert iters == rec["iterations"]
+        assert gfc.tolist() == rec["gf_changed"] and fc.tolist() == rec["f_changed"]
+        assert solver.stats.component_count == rec["component_count"]
+        assert gen.pairs_digest(labels) == rec["labels_digest"] == rec["uf_labels_digest"]
