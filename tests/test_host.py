@@ -131,3 +131,17 @@ def test_build_csr_matches_reference_arrays():
     for c in load_suite():
         g = fb.build_csr(c.n, c.edges)
         assert csr_digest(g.row_offsets, g.col_indices) == gold[c.name]["digest"], c.name
+
+
+@pytest.mark.parametrize("index", [1, 2, 3, 4])
+def test_build_csr_matches_reference_arrays_baseline_configs(index):
+    """BASELINE configs 1-4 at full size: the host builder's CSR equals the
+    one svcc.build_csr produced (digests made by the reference itself,
+    tests/golden/make_csr_golden.py --configs; 244 s for config 2 there)."""
+    from golden_io import csr_digest, load_csr_digests
+    rec = load_csr_digests()["configs"][str(index)]
+    n, pairs = gen.baseline_graph(index)
+    assert gen.pairs_digest(pairs) == rec["pairs_digest"]
+    g = fb.build_csr(n, pairs)
+    assert g.m == rec["m_dir"]
+    assert csr_digest(g.row_offsets, g.col_indices) == rec["digest"]
