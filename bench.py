@@ -512,17 +512,23 @@ def main():
             "clocks": clocks,
         }
         if world > 1:
-            # NVLink roofline of the per-iteration allreduce-min (ring bus
-            # bytes per GPU) against the measured peer bandwidth
-            ar_launches = max(iters - 1, 1)
-            ar_ms = best.allreduce_ms / ar_launches if best.allreduce_ms else None
-            bus = 2 * (world - 1) / world * 4 * n
-            line["nvlink"] = {"collective": "ncclAllReduce(int32, min) of the next-parent vector",
-                              "bytes_per_iter_per_gpu": bus, "launches": ar_launches, "launch_ms": ar_ms,
-                              "achieved": (bus / (ar_ms * 1e-3) / 1e9) if ar_ms else None,
+            # NVLink roofline of the per-iteration exchange (dense iterations:
+            # allreduce-min, ring bus bytes 2(P-1)/P*4n per GPU, SURVEY §8d;
+            # sparse iterations: the delta lists) against the measured peer
+            # bandwidth; bytes are the library's own count of what it sent
+            xs = best.dense_exchanges + best.delta_exchanges
+            x_ms = best.allreduce_ms / xs if (best.allreduce_ms and xs) else None
+            x_bytes = best.exchange_bytes / xs if xs else None
+            line["nvlink"] = {"collective": "ncclAllReduce(int32, min) of the next-parent vector (dense iterations); "
+                                            "ncclAllGather of (index, value) deltas (sparse iterations)",
+                              "dense_exchanges": int(best.dense_exchanges),
+                              "delta_exchanges": int(best.delta_exchanges),
+                              "bytes_per_exchange_per_gpu": x_bytes, "exchange_ms": x_ms,
+                              "dense_allreduce_bus_bytes": 2 * (world - 1) / world * 4 * n,
+                              "achieved": (x_bytes / (x_ms * 1e-3) / 1e9) if x_ms else None,
                               "peak": 770.0, "unit": "GB/s",
                               "peak_kind": "measured peer copy per direction (B200_PROFILING.md)",
-                              "frac": (bus / (ar_ms * 1e-3) / 1e9 / 770.0) if ar_ms else None}
+                              "frac": (x_bytes / (x_ms * 1e-3) / 1e9 / 770.0) if x_ms else None}
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline_sample(g, n_edges)
         print(json.dumps(line), flush=True)

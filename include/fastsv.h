@@ -35,7 +35,7 @@ extern "C" {
 #define FSV_ERR_INVARIANT 3
 #define FSV_ERR_RUNTIME 4
 
-#define FSV_ABI_VERSION 3
+#define FSV_ABI_VERSION 4
 
 typedef struct fsv_ctx fsv_ctx;
 
@@ -57,7 +57,13 @@ typedef struct fsv_config {
    * (algorithms.py:66-76,145-149, trace-identical to all flags off). The
    * variant trace reports kernel "none" (0) and flops 0, as the reference. */
   int32_t hooking;
-  int32_t reserved;
+  /* multi-rank exchange of the next-parent vector:
+   * 0 = dense iterations allreduce-min, sparse iterations exchange only the
+   *     entries each rank lowered (allgather of (index, value) lists, bytes
+   *     proportional to the delta; host in the loop per iteration);
+   * 1 = allreduce-min every iteration (the loop may run as one CUDA graph
+   *     with the collective captured). Results are identical. */
+  int32_t exchange;
 } fsv_config;
 
 #define FSV_HOOKING_SET 0x100
@@ -82,6 +88,10 @@ typedef struct fsv_stats {
   float hook_ms, hubfix_ms, shortcut_ms, first_ms, allreduce_ms, push_ms;
   int32_t hook_launches;
   int32_t sparse_iterations;  /* iterations that ran the sparse push */
+  /* multi-rank: exchanges by kind and bytes this rank sent (allreduce: ring
+   * bus bytes 2(P-1)/P*4n; delta: 8 bytes per pair to each other rank) */
+  int32_t dense_exchanges, delta_exchanges;
+  int64_t exchange_bytes;
 } fsv_stats;
 
 const char* fsv_last_error(void);
@@ -155,6 +165,9 @@ int fsv_get_csr(fsv_ctx* ctx, int64_t* row_offsets, int32_t* cols, int64_t* csr_
 
 /* Run FastSV to convergence on the resident graph. Labels stay on device. */
 int fsv_solve(fsv_ctx* ctx, const fsv_config* cfg, fsv_stats* stats);
+
+/* The fsv_stats of the last solve (as fsv_solve fills them). */
+int fsv_get_stats(fsv_ctx* ctx, fsv_stats* stats);
 
 /* Copy results of the last solve to host buffers.
  *   labels: n int32 (or int64 via fsv_get_labels64)

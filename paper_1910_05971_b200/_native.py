@@ -24,7 +24,7 @@ FSV_OK, FSV_ERR_INPUT, FSV_ERR_CONTRACT, FSV_ERR_INVARIANT, FSV_ERR_RUNTIME = 0,
 class FsvConfig(ctypes.Structure):
     _fields_ = [("max_iters", c_int32), ("batch", c_int32), ("profile", c_int32),
                 ("sparse_policy", c_int32), ("sparse_threshold", c_double), ("hooking", c_int32),
-                ("reserved", c_int32)]
+                ("exchange", c_int32)]
 
 
 class FsvStats(ctypes.Structure):
@@ -33,7 +33,8 @@ class FsvStats(ctypes.Structure):
                 ("host_syncs", c_int32), ("kernel_launches", c_int32), ("solve_ms", c_float),
                 ("hook_ms", c_float), ("hubfix_ms", c_float), ("shortcut_ms", c_float),
                 ("first_ms", c_float), ("allreduce_ms", c_float), ("push_ms", c_float),
-                ("hook_launches", c_int32), ("sparse_iterations", c_int32)]
+                ("hook_launches", c_int32), ("sparse_iterations", c_int32),
+                ("dense_exchanges", c_int32), ("delta_exchanges", c_int32), ("exchange_bytes", c_int64)]
 
 
 # symbol -> (restype, argtypes); mirrors include/fastsv.h one to one
@@ -52,6 +53,7 @@ FASTSV_SYMBOLS = {
     "fsv_upload_edges64": (c_int, [c_void_p, c_int64, c_int64, c_void_p, c_int64, c_int64]),
     "fsv_get_csr": (c_int, [c_void_p, c_void_p, c_void_p, POINTER(c_int64)]),
     "fsv_solve": (c_int, [c_void_p, POINTER(FsvConfig), POINTER(FsvStats)]),
+    "fsv_get_stats": (c_int, [c_void_p, POINTER(FsvStats)]),
     "fsv_get_labels": (c_int, [c_void_p, c_void_p]),
     "fsv_get_labels64": (c_int, [c_void_p, c_void_p]),
     "fsv_get_labeling": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_int64, POINTER(c_int64)]),

@@ -68,8 +68,8 @@ def build_fastsv(force=False, verbose=False, extra_flags=()) -> Path:
     deps = srcs + [CSRC / h for h in CUDA_HEADERS] + [INCLUDE / "fastsv.h"]
     if force or _stale(LIB_FASTSV, deps):
         cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared",
-               "-cudart", "static", "-I", INCLUDE, "-Xptxas", "-v" if verbose else "-O3",
-               *extra_flags, "-o", LIB_FASTSV, *srcs, "-ldl", "-lpthread"]
+               "-cudart", "static", "-Xcompiler", "-fopenmp", "-I", INCLUDE, "-Xptxas", "-v" if verbose else "-O3",
+               *extra_flags, "-o", LIB_FASTSV, *srcs, "-ldl", "-lpthread", "-lgomp"]
         _run(cmd, verbose)
     return LIB_FASTSV
 
@@ -85,8 +85,8 @@ def build_fastsv_checked(force=False, verbose=False) -> Path:
     deps = srcs + [CSRC / h for h in CUDA_HEADERS] + [INCLUDE / "fastsv.h"]
     if force or _stale(LIB_FASTSV_CHECKED, deps):
         cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared",
-               "-cudart", "static", "-I", INCLUDE, "-DFSV_CHECKS", "-o", LIB_FASTSV_CHECKED, *srcs,
-               "-ldl", "-lpthread"]
+               "-cudart", "static", "-Xcompiler", "-fopenmp", "-I", INCLUDE, "-DFSV_CHECKS", "-o", LIB_FASTSV_CHECKED, *srcs,
+               "-ldl", "-lpthread", "-lgomp"]
         _run(cmd, verbose)
     return LIB_FASTSV_CHECKED
 

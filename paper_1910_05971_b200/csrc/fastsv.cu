@@ -20,6 +20,7 @@
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <nccl.h>
+#include <omp.h>
 
 #include <algorithm>
 #include <cstdarg>
@@ -78,6 +79,7 @@ struct NcclApi {
   ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
   ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                             cudaStream_t) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
 };
@@ -92,9 +94,10 @@ static int nccl_load() {
   g_nccl.GetUniqueId = (decltype(g_nccl.GetUniqueId))dlsym(h, "ncclGetUniqueId");
   g_nccl.CommInitRank = (decltype(g_nccl.CommInitRank))dlsym(h, "ncclCommInitRank");
   g_nccl.AllReduce = (decltype(g_nccl.AllReduce))dlsym(h, "ncclAllReduce");
+  g_nccl.AllGather = (decltype(g_nccl.AllGather))dlsym(h, "ncclAllGather");
   g_nccl.CommDestroy = (decltype(g_nccl.CommDestroy))dlsym(h, "ncclCommDestroy");
   g_nccl.GetErrorString = (decltype(g_nccl.GetErrorString))dlsym(h, "ncclGetErrorString");
-  if (!g_nccl.GetUniqueId || !g_nccl.CommInitRank || !g_nccl.AllReduce || !g_nccl.CommDestroy)
+  if (!g_nccl.GetUniqueId || !g_nccl.CommInitRank || !g_nccl.AllReduce || !g_nccl.AllGather || !g_nccl.CommDestroy)
     return fail(FSV_ERR_RUNTIME, "NCCL library lacks required symbols");
   g_nccl.loaded = true;
   return FSV_OK;
@@ -216,14 +219,17 @@ struct fsv_ctx {
   // first STAGE_ITERS iterations into one report; one copy brings it back
   DBuf<SolveReport> rep;
   SolveReport* h_rep = nullptr;   // pinned
-  int64_t* h_off_pin = nullptr;   // pinned host copy of device-built row offsets
+  // pageable host transfers: ring of pinned staging buffers (staged_h2d/d2h)
+  void* stage_buf[4] = {nullptr, nullptr, nullptr, nullptr};
+  cudaEvent_t stage_ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  bool stage_used[4] = {false, false, false, false};
+  int stage_next = 0;
   // hooking variants (fsv_variants.cuh): row ids of the stored entries, two
   // extra vectors, and where the labels of the last solve live
   DBuf<int> var_rows, var_t, var_g;
   bool var_rows_ready = false;
   bool variant = false;
   const int* labels_src = nullptr;
-  size_t h_off_cap = 0;
   std::vector<cudaEvent_t> events;
   // profile mode: events around every kernel of iteration k: [k][0..7]
   std::vector<cudaEvent_t> pev;
@@ -268,6 +274,14 @@ struct fsv_ctx {
   // multi-GPU
   ncclComm_t comm = nullptr;
   int nranks = 1, rank = 0;
+  bool graph_comm_failed = false;   // NCCL refused capture into the loop body: host loop
+  // sparse-iteration delta exchange: this rank's lowered entries (index,
+  // value), their count, and the gathered lists of all ranks
+  DBuf<int2> dx_list, dx_all;
+  DBuf<unsigned> dx_cnt;
+  unsigned* h_dx_cnt = nullptr;     // pinned, kGroupMax + 256 entries
+  long long xbytes = 0;             // bytes this rank sent over the exchange in the last solve
+  int delta_x = 0, dense_x = 0;     // exchanges of each kind in the last solve
 };
 
 static int ensure_events(fsv_ctx* c, size_t count) {
@@ -276,6 +290,100 @@ static int ensure_events(fsv_ctx* c, size_t count) {
     CUDA_TRY(cudaEventCreate(&e));
     c->events.push_back(e);
   }
+  return FSV_OK;
+}
+
+// ---- pageable host transfers ------------------------------------------------
+// The drop-in receives plain numpy arrays (pageable memory). A cudaMemcpy
+// from pageable memory is staged by the driver through one host thread;
+// here host threads copy 8 MB pieces into a ring of pinned buffers while the
+// copy engine moves the previous pieces, so the transfer runs near the
+// pinned rate. Pinned/registered buffers take the direct path.
+constexpr size_t kStageBytes = 8u << 20;
+constexpr int kStageBufs = 4;
+
+static bool is_pageable(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return true;
+  }
+  return a.type == cudaMemoryTypeUnregistered;
+}
+
+static int stage_init(fsv_ctx* c) {
+  for (int i = 0; i < kStageBufs; ++i) {
+    if (!c->stage_buf[i]) CUDA_TRY(cudaMallocHost(&c->stage_buf[i], kStageBytes));
+    if (!c->stage_ev[i]) CUDA_TRY(cudaEventCreateWithFlags(&c->stage_ev[i], cudaEventDisableTiming));
+  }
+  return FSV_OK;
+}
+
+static void par_memcpy(void* dst, const void* src, size_t bytes) {
+  constexpr size_t piece = 512u << 10;
+  const long long np = (long long)((bytes + piece - 1) / piece);
+  const int T = (int)std::min<long long>(np, std::min(16, omp_get_max_threads()));
+  if (T <= 1) {
+    memcpy(dst, src, bytes);
+    return;
+  }
+#pragma omp parallel for num_threads(T) schedule(static)
+  for (long long i = 0; i < np; ++i) {
+    const size_t o = (size_t)i * piece;
+    memcpy((char*)dst + o, (const char*)src + o, std::min(piece, bytes - o));
+  }
+}
+
+// Host (pageable) -> device through the staging ring, ordered on stream s.
+static int staged_h2d(fsv_ctx* c, void* dst, const void* src, size_t bytes, cudaStream_t s) {
+  int rc = stage_init(c);
+  if (rc) return rc;
+  for (size_t o = 0; o < bytes; o += kStageBytes) {
+    const size_t b = std::min(kStageBytes, bytes - o);
+    const int k = c->stage_next;
+    c->stage_next = (k + 1) % kStageBufs;
+    if (c->stage_used[k]) CUDA_TRY(cudaEventSynchronize(c->stage_ev[k]));
+    par_memcpy(c->stage_buf[k], (const char*)src + o, b);
+    CUDA_TRY(cudaMemcpyAsync((char*)dst + o, c->stage_buf[k], b, cudaMemcpyHostToDevice, s));
+    CUDA_TRY(cudaEventRecord(c->stage_ev[k], s));
+    c->stage_used[k] = true;
+  }
+  return FSV_OK;
+}
+
+// Device -> host (pageable): up to kStageBufs pieces in flight, each copied
+// out by the host threads as it lands. Returns when dst holds the data.
+static int staged_d2h(fsv_ctx* c, void* dst, const void* src, size_t bytes, cudaStream_t s) {
+  int rc = stage_init(c);
+  if (rc) return rc;
+  const size_t np = (bytes + kStageBytes - 1) / kStageBytes;
+  auto issue = [&](size_t i) -> int {
+    const size_t o = i * kStageBytes, b = std::min(kStageBytes, bytes - o);
+    const int k = (int)(i % kStageBufs);
+    CUDA_TRY(cudaMemcpyAsync(c->stage_buf[k], (const char*)src + o, b, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaEventRecord(c->stage_ev[k], s));
+    return FSV_OK;
+  };
+  for (size_t i = 0; i < std::min<size_t>(np, kStageBufs); ++i)
+    if ((rc = issue(i))) return rc;
+  for (size_t i = 0; i < np; ++i) {
+    const int k = (int)(i % kStageBufs);
+    CUDA_TRY(cudaEventSynchronize(c->stage_ev[k]));
+    const size_t o = i * kStageBytes, b = std::min(kStageBytes, bytes - o);
+    par_memcpy((char*)dst + o, c->stage_buf[k], b);
+    if (i + kStageBufs < np && (rc = issue(i + kStageBufs))) return rc;
+  }
+  for (int k = 0; k < kStageBufs; ++k) c->stage_used[k] = false;   // ring drained
+  return FSV_OK;
+}
+
+// Device -> host copy into a caller buffer of any kind (synchronous).
+static int copy_out(fsv_ctx* c, void* dst, const void* src, size_t bytes) {
+  if (!bytes) return FSV_OK;
+  if (bytes >= (1u << 20) && is_pageable(dst)) return staged_d2h(c, dst, src, bytes, c->stream);
+  CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
   return FSV_OK;
 }
 
@@ -332,7 +440,11 @@ extern "C" int fsv_destroy(fsv_ctx* c) {
   if (c->comm && g_nccl.CommDestroy) g_nccl.CommDestroy(c->comm);
   if (c->h_done) cudaFreeHost(c->h_done);
   if (c->h_rep) cudaFreeHost(c->h_rep);
-  if (c->h_off_pin) cudaFreeHost(c->h_off_pin);
+  if (c->h_dx_cnt) cudaFreeHost(c->h_dx_cnt);
+  for (int i = 0; i < 4; ++i) {
+    if (c->stage_buf[i]) cudaFreeHost(c->stage_buf[i]);
+    if (c->stage_ev[i]) cudaEventDestroy(c->stage_ev[i]);
+  }
   for (auto e : c->chunk_ev) cudaEventDestroy(e);
   if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
   if (c->own_stream) cudaStreamDestroy(c->own_stream);
@@ -391,6 +503,9 @@ constexpr uint32_t DROP = 0xffffffffu;
 #ifndef FSV_PIECE
 #define FSV_PIECE 1024
 #endif
+#ifndef FSV_LONG_ROW
+#define FSV_LONG_ROW 32          // rows longer than this are encoded/compacted by a whole warp
+#endif
 constexpr long long HUGE_ROW = FSV_HUGE_ROW;  // rows longer than this are cut into pieces
 constexpr long long PIECE = FSV_PIECE;        // entries per piece
 
@@ -425,7 +540,7 @@ __global__ void k_orient_encode(const int64_t* __restrict__ off, const ColT* __r
     }
     const bool huge = hi - lo > HUGE_ROW;        // cut into pieces (k_piece_encode)
     if (huge) hi = lo;
-    const bool is_long = hi - lo > 32;
+    const bool is_long = hi - lo > FSV_LONG_ROW;
     long long k = 0;
     if (!is_long) {
       // 4 entries of the lane's row in flight (column loads, then pos gathers)
@@ -645,7 +760,7 @@ __global__ void k_orient_compact(const int64_t* __restrict__ off, long long col_
       }
     }
     if (hi - lo > HUGE_ROW) hi = lo;     // entries placed by k_piece_compact
-    const bool is_long = has && hi - lo > 32;
+    const bool is_long = has && hi - lo > FSV_LONG_ROW;
     if (has && !is_long) {
       long long o = o0 + 1;
       for (long long e = lo; e < hi; e += 4) {
@@ -954,8 +1069,12 @@ static int upload_impl(fsv_ctx* c, int64_t n, const int64_t* h_off_arr, const Co
   } else {
     if (d_off_src != d_off.p || !d_off.p) CUDA_TRY(d_off.alloc((size_t)n + 1));
     CUDA_TRY(d_cols.alloc((size_t)mloc));
-    if (h_off_arr)
+    if (h_off_arr && is_pageable(h_off_arr)) {
+      int rc = staged_h2d(c, d_off.p, h_off_arr, sizeof(int64_t) * (n + 1), st);
+      if (rc) return rc;
+    } else if (h_off_arr) {
       CUDA_TRY(cudaMemcpyAsync(d_off.p, h_off_arr, sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice, st));
+    }
     else if (d_off_src != d_off.p)
       CUDA_TRY(cudaMemcpyAsync(d_off.p, d_off_src, sizeof(int64_t) * (n + 1), cudaMemcpyDeviceToDevice, st));
     offp = d_off.p;
@@ -963,6 +1082,7 @@ static int upload_impl(fsv_ctx* c, int64_t n, const int64_t* h_off_arr, const Co
   }
   // columns go up in row-aligned chunks on the copy stream, so the degree
   // sort and the orientation of earlier chunks overlap the transfer
+  const bool cols_pageable = h_cols && !d_src && mloc > 0 && is_pageable(h_cols);
   std::vector<int64_t> chunk_rows;  // row boundaries, chunk k = [chunk_rows[k], chunk_rows[k+1])
   {
     // eighths of the entries, the last eighth cut geometrically (1/16, 1/32,
@@ -992,7 +1112,10 @@ static int upload_impl(fsv_ctx* c, int64_t n, const int64_t* h_off_arr, const Co
     cudaEvent_t off_ready = c->chunk_ev[0];
     CUDA_TRY(cudaEventRecord(off_ready, st));              // d_off allocation/reuse ordering
     CUDA_TRY(cudaStreamWaitEvent(c->copy_stream, off_ready, 0));
-    for (int k = 0; k < K; ++k) {
+    // pageable host columns: staged pieces issued chunk by chunk inside the
+    // orientation loop below (the host copies chunk k+1 while the device
+    // orients chunk k); pinned ones all go up now
+    for (int k = 0; k < K && !cols_pageable; ++k) {
       const int64_t lo = h_off[chunk_rows[k]] - e_begin, hi = h_off[chunk_rows[k + 1]] - e_begin;
       // only non-decreasing offsets are accepted (checked on the device
       // below); until then no copy may leave [0, mloc)
@@ -1130,6 +1253,13 @@ static int upload_impl(fsv_ctx* c, int64_t n, const int64_t* h_off_arr, const Co
   for (int k = 0; k < K; ++k) {
     const long long u0 = chunk_rows[k], u1 = chunk_rows[k + 1], nr = u1 - u0;
     const long long r0 = u0 - row_begin, r1 = u1 - row_begin;
+    if (cols_pageable) {
+      const int64_t lo = h_off[u0] - e_begin, hi = h_off[u1] - e_begin;
+      if (lo < 0 || hi > mloc || hi < lo) return fail(FSV_ERR_INPUT, "row_offsets must be non-decreasing");
+      int rc = staged_h2d(c, d_cols.p + lo, h_cols + lo, sizeof(ColT) * (hi - lo), c->copy_stream);
+      if (rc) return rc;
+      CUDA_TRY(cudaEventRecord(c->chunk_ev[k], c->copy_stream));
+    }
     CUDA_TRY(cudaStreamWaitEvent(st, c->chunk_ev[k], 0));
     if (nr) {
       k_orient_encode<ColT><<<grid_for(c, (nr + 31) / 32 * 32, 256, 16), 256, 0, st>>>(
@@ -1682,6 +1812,156 @@ static int launch_group_iteration(fsv_ctx* const* cs, int count, int k, int max_
   return rc;
 }
 
+// ---- sparse-iteration delta exchange (multi-rank) -----------
+// A sparse (push) iteration lowers few entries of N, and N starts as the
+// replicated gf_k on every rank (E1), so a rank's contribution to the merged
+// N is exactly its entries with N[i] < gf_k[i]. Each rank compacts those
+// (i, N[i]) pairs, the lists are all-gathered (ncclAllGather, bytes on the
+// wire proportional to the largest list) and every rank min-reduces the other
+// ranks' pairs into its N — the same elementwise min the dense allreduce
+// computes (the reference's reason for SpMSpV is to move only the delta,
+// kernels.py:71-102). Falls back to the allreduce when the
+// lists are not smaller.
+__global__ void k_delta_compact(const int* __restrict__ N, const int* __restrict__ G, long long n,
+                                int2* __restrict__ out, unsigned* __restrict__ cnt) {
+  const int lane = threadIdx.x & 31;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long base = (long long)blockIdx.x * blockDim.x; base < n; base += stride) {   // block-uniform
+    const long long i = base + threadIdx.x;
+    const bool on = i < n && __ldg(N + i) < __ldg(G + i);
+    const unsigned b = __ballot_sync(0xffffffffu, on);
+    if (!b) continue;
+    unsigned at = 0;
+    if (lane == 0) at = atomicAdd(cnt, (unsigned)__popc(b));
+    at = __shfl_sync(0xffffffffu, at, 0);
+    if (on) out[at + __popc(b & ((1u << lane) - 1u))] = make_int2((int)i, __ldg(N + i));
+  }
+}
+
+// N <-min the pairs of every other rank: lists[r][0 .. counts[r]) of the
+// gathered buffer (cap pairs per rank).
+__global__ void k_delta_apply(const int2* __restrict__ all, const unsigned* __restrict__ counts, int nranks,
+                              long long cap, int self, int* __restrict__ N) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (int r = 0; r < nranks; ++r) {
+    if (r == self) continue;
+    const long long cr = counts[r];
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < cr; e += stride) {
+      const int2 x = all[r * cap + e];
+      red_min(N + x.x, x.y);
+    }
+  }
+}
+
+// Emulated group: rank `self`'s N <-min every other rank's list.
+struct GroupDelta {
+  const int2* list[kGroupMax];
+  const unsigned* cnt[kGroupMax];
+  int count;
+};
+__global__ void k_group_delta_apply(GroupDelta a, int self, int* __restrict__ N) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (int r = 0; r < a.count; ++r) {
+    if (r == self) continue;
+    const long long cr = *a.cnt[r];
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < cr; e += stride) {
+      const int2 x = a.list[r][e];
+      red_min(N + x.x, x.y);
+    }
+  }
+}
+
+static int ensure_delta_buffers(fsv_ctx* c, long long pairs_all) {
+  CUDA_TRY(c->dx_list.alloc((size_t)std::max<long long>(c->n, 1)));
+  CUDA_TRY(c->dx_cnt.alloc(kGroupMax + 256));
+  if (pairs_all > 0) CUDA_TRY(c->dx_all.alloc((size_t)pairs_all));
+  if (!c->h_dx_cnt) CUDA_TRY(cudaMallocHost(&c->h_dx_cnt, sizeof(unsigned) * (kGroupMax + 256)));
+  return FSV_OK;
+}
+
+// Exchange of a sparse iteration k across the group / communicator. Host
+// synchronising (the list sizes decide the transfer); all ranks take the same
+// branch because they see the same counts.
+static int launch_delta_exchange(fsv_ctx* const* cs, int count, int k) {
+  fsv_ctx* c = cs[0];
+  cudaStream_t st = c->stream;
+  const long long n = c->n;
+  const int P = count > 1 ? count : c->nranks;
+  int rc = FSV_OK;
+  for (int r = 0; r < count; ++r) {
+    fsv_ctx* x = cs[r];
+    if ((rc = ensure_delta_buffers(x, 0))) return rc;
+    CUDA_TRY(cudaMemsetAsync(x->dx_cnt.p, 0, sizeof(unsigned) * (kGroupMax + 1), st));
+    if (n) k_delta_compact<<<grid_for(x, n, 256), 256, 0, st>>>(bufN(x, k), x->G, n, x->dx_list.p, x->dx_cnt.p);
+    ++x->launches;
+  }
+  unsigned* hc = c->h_dx_cnt;
+  if (count > 1) {
+    for (int r = 0; r < count; ++r)
+      CUDA_TRY(cudaMemcpyAsync(hc + r, cs[r]->dx_cnt.p, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+  } else {
+    // counts of every rank: one 4-byte allgather
+    NCCL_TRY(g_nccl.AllGather(c->dx_cnt.p, c->dx_cnt.p + 1, 1, ncclUint32, c->comm, st));
+    CUDA_TRY(cudaMemcpyAsync(hc, c->dx_cnt.p + 1, sizeof(unsigned) * P, cudaMemcpyDeviceToHost, st));
+  }
+  CUDA_TRY(cudaStreamSynchronize(st));
+  ++c->host_syncs;
+  unsigned cmax = 0;
+  for (int r = 0; r < P; ++r) cmax = std::max(cmax, hc[r]);
+  // delta only when the gathered lists are smaller than the allreduce's
+  // bus bytes per rank (2 (P-1)/P * 4n)
+  const double delta_bytes = 8.0 * (double)cmax * (double)P;
+  const double dense_bytes = 2.0 * (P - 1) / P * 4.0 * (double)n;
+  if (delta_bytes >= dense_bytes) {
+    for (int r = 0; r < count; ++r) ++cs[r]->dense_x;
+    if (count == 1) c->xbytes += (long long)dense_bytes;
+    return launch_exchange(cs, count, k);
+  }
+  for (int r = 0; r < count; ++r) ++cs[r]->delta_x;
+  if (count > 1) {
+    GroupDelta gd{};
+    gd.count = count;
+    for (int r = 0; r < count; ++r) {
+      gd.list[r] = cs[r]->dx_list.p;
+      gd.cnt[r] = cs[r]->dx_cnt.p;
+    }
+    for (int r = 0; r < count; ++r) {
+      k_group_delta_apply<<<grid_for(c, std::max<long long>(cmax, 1), 256), 256, 0, st>>>(gd, r, bufN(cs[r], k));
+      ++c->launches;
+    }
+    return FSV_OK;
+  }
+  if (cmax == 0) return FSV_OK;
+  if ((rc = ensure_delta_buffers(c, (long long)cmax * P))) return rc;
+  NCCL_TRY(g_nccl.AllGather(c->dx_list.p, c->dx_all.p, (size_t)cmax * 2, ncclInt32, c->comm, st));
+  k_delta_apply<<<grid_for(c, (long long)cmax * (P - 1), 256), 256, 0, st>>>(c->dx_all.p, c->dx_cnt.p + 1, P,
+                                                                             (long long)cmax, c->rank, bufN(c, k));
+  ++c->launches;
+  c->xbytes += (long long)(8.0 * cmax * (P - 1));
+  return FSV_OK;
+}
+
+// One iteration of a multi-rank solve with the host in the loop (the
+// iteration's product kind is known on the host): dense iterations merge by
+// allreduce / device min-merge, sparse ones by the delta exchange.
+static int launch_multi_iteration(fsv_ctx* const* cs, int count, int k, int max_iter, bool sparse) {
+  int rc = FSV_OK;
+  fsv_ctx* c = cs[0];
+  for (int r = 0; r < count && !rc; ++r) rc = launch_hook(cs[r], k, false);
+  if (rc) return rc;
+  pmark(c, k, 8);
+  if (sparse) {
+    rc = launch_delta_exchange(cs, count, k);
+  } else {
+    for (int r = 0; r < count; ++r) ++cs[r]->dense_x;
+    if (count == 1 && c->comm) c->xbytes += (long long)(2.0 * (c->nranks - 1) / c->nranks * 4.0 * (double)c->n);
+    rc = launch_exchange(cs, count, k);
+  }
+  pmark(c, k, 9);
+  for (int r = 0; r < count && !rc; ++r) rc = launch_vertex(cs[r], k, max_iter, false);
+  return rc;
+}
+
 // The buffers, sizes and launch shapes baked into the captured iteration
 // loop. A re-upload that leaves all of them unchanged (the same graph again:
 // the workspaces only grow) keeps the instantiated graph.
@@ -1691,7 +1971,7 @@ static std::vector<long long> graph_key(const fsv_ctx* c) {
           P(c->hacc), P(c->hub_id.p), P(c->done.p), P(c->mode.p), P(c->dlist.p), P(c->dcount.p), c->rcap,
           c->dgrid, P(c->offp), P(c->colsp), c->col_base, c->row_begin, c->row_end, P(c->cnt.p),
           P(c->chunks.p), P(c->iterbuf.p), P(c->tstamp.p), P(c->ticket.p), P(c->partials.p), c->n,
-          c->sm_count};
+          c->sm_count, P(c->comm)};
 }
 
 // Builds (or reuses) the CUDA graph of the iteration loop: one conditional
@@ -2018,8 +2298,20 @@ static int solve_body(fsv_ctx* const* cs, int count, const fsv_config* cfg, int3
   if (c->profile && (rc = ensure_pevents(c, 2 * kPev))) return rc;
 
   // graph mode: the whole iteration loop is one conditional-WHILE graph launch
-  const bool graph_mode = count == 1 && c->use_graph && !snapshots && !c->profile && !c->comm && d.batch == 0;
-  if (graph_mode && (rc = ensure_graph(c, cap))) return rc;
+  // (a communicator's ncclAllReduce is captured into the loop body too: every
+  // rank runs the same iterations since the convergence flag is replicated;
+  // if NCCL refuses capture into the conditional body, the host loop runs)
+  if (d.exchange < 0 || d.exchange > 1) return fail(FSV_ERR_CONTRACT, "exchange must be 0 or 1");
+  const bool delta = d.exchange == 0;
+  bool graph_mode = count == 1 && c->use_graph && !snapshots && !c->profile && d.batch == 0 &&
+                    (!c->comm || c->nranks == 1 || (!c->graph_comm_failed && !delta));
+  if (graph_mode && (rc = ensure_graph(c, cap))) {
+    if (!c->comm) return rc;
+    cudaGetLastError();
+    c->graph_comm_failed = true;
+    graph_mode = false;
+    rc = FSV_OK;
+  }
   CUDA_TRY(cudaEventRecord(c->events[0], st));
   for (int r = 0; r < count; ++r) {
     fsv_ctx* x = cs[r];
@@ -2106,8 +2398,34 @@ static int solve_body(fsv_ctx* const* cs, int count, const fsv_config* cfg, int3
       c->launches += (FSV_GRAPH_IF ? std::max(1, it - 1) : passes * FSV_GRAPH_BODY) * per_it;
     }
   }
+  // multi-rank solves keep the host in the loop one iteration at a time:
+  // the next iteration's product kind (written by the vertex pass) decides
+  // its exchange (dense allreduce or sparse delta lists)
+  const bool multi = !graph_mode && (count > 1 || (c->comm && c->nranks > 1));
+  for (int r = 0; r < count; ++r) {
+    cs[r]->xbytes = 0;
+    cs[r]->delta_x = cs[r]->dense_x = 0;
+  }
+  while (!graph_mode && multi) {
+    int hm[2] = {0, 0};
+    CUDA_TRY(cudaMemcpyAsync(c->h_done, c->done.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaMemcpyAsync(&hm[0], c->mode.p + launched + 1, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    ++c->host_syncs;
+    done = *c->h_done;
+    if (snapshots && launched > 1) {
+      if (launched > snap_cap) return fail(FSV_ERR_CONTRACT, "more than %d iterations ran", snap_cap);
+      if ((rc = copy_snapshot(c, launched, snapshots + (size_t)(launched - 1) * c->n))) return rc;
+    }
+    if (done != 0) break;
+    if (launched >= cap) return fail(FSV_ERR_RUNTIME, "did not converge within %d iterations", cap);
+    const int k = ++launched;
+    if ((rc = launch_multi_iteration(cs, count, k, cap, delta && hm[0] == 1))) return rc;
+    if ((rc = ensure_events(c, (size_t)k + 1))) return rc;
+    CUDA_TRY(cudaEventRecord(c->events[k], st));
+  }
   bool first_round = true;
-  while (!graph_mode) {
+  while (!graph_mode && !multi) {
     // the first round also holds iteration 1, so it queues batch-1 more
     const int more = first_round ? batch - 1 : batch;
     first_round = false;
@@ -2236,6 +2554,15 @@ static void fill_stats(fsv_ctx* c, fsv_stats* s) {
   int sp = 0;
   for (int k = 2; k <= c->iterations && k < (int)c->h_mode.size(); ++k) sp += c->h_mode[k] == 1;
   s->sparse_iterations = sp;
+  s->dense_exchanges = c->dense_x;
+  s->delta_exchanges = c->delta_x;
+  s->exchange_bytes = c->xbytes;
+}
+
+extern "C" int fsv_get_stats(fsv_ctx* c, fsv_stats* stats) {
+  if (!c || !stats) return fail(FSV_ERR_CONTRACT, "NULL argument");
+  fill_stats(c, stats);
+  return FSV_OK;
 }
 
 extern "C" int fsv_solve(fsv_ctx* c, const fsv_config* cfg, fsv_stats* stats) {
@@ -2326,12 +2653,9 @@ extern "C" int fsv_get_labeling(fsv_ctx* c, int64_t* labels, int64_t* reps, int6
   if (count) *count = C;
   if ((reps || sizes) && cap < C)
     return fail(FSV_ERR_CONTRACT, "capacity %lld < %lld components", (long long)cap, C);
-  cudaStream_t st = c->stream;
-  if (labels && c->n)
-    CUDA_TRY(cudaMemcpyAsync(labels, c->lab.labels.p, sizeof(int64_t) * c->n, cudaMemcpyDeviceToHost, st));
-  if (reps && C) CUDA_TRY(cudaMemcpyAsync(reps, c->lab.reps.p, sizeof(int64_t) * C, cudaMemcpyDeviceToHost, st));
-  if (sizes && C) CUDA_TRY(cudaMemcpyAsync(sizes, c->lab.sizes.p, sizeof(int64_t) * C, cudaMemcpyDeviceToHost, st));
-  CUDA_TRY(cudaStreamSynchronize(st));
+  if (labels && c->n && (rc = copy_out(c, labels, c->lab.labels.p, sizeof(int64_t) * c->n))) return rc;
+  if (reps && C && (rc = copy_out(c, reps, c->lab.reps.p, sizeof(int64_t) * C))) return rc;
+  if (sizes && C && (rc = copy_out(c, sizes, c->lab.sizes.p, sizeof(int64_t) * C))) return rc;
   return FSV_OK;
 }
 
@@ -2365,10 +2689,7 @@ extern "C" int fsv_get_labels(fsv_ctx* c, int32_t* labels) {
   if (!c->n) return FSV_OK;
   if (!labels) return fail(FSV_ERR_CONTRACT, "labels is NULL");
   CUDA_TRY(cudaSetDevice(c->device));
-  CUDA_TRY(cudaMemcpyAsync(labels, c->labels_src ? c->labels_src : c->G, sizeof(int) * c->n,
-                           cudaMemcpyDeviceToHost, c->stream));
-  CUDA_TRY(cudaStreamSynchronize(c->stream));
-  return FSV_OK;
+  return copy_out(c, labels, c->labels_src ? c->labels_src : c->G, sizeof(int) * c->n);
 }
 
 extern "C" int fsv_get_labels64(fsv_ctx* c, int64_t* labels) {

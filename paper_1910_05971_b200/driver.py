@@ -236,9 +236,10 @@ class Solver:
     # -- solve ------------------------------------------------------------
     @staticmethod
     def _config(batch: int = 0, max_iters: int = 0, profile: bool = False,
-                policy: int = 0, threshold: float = 0.1, hooking: int = 0) -> FsvConfig:
+                policy: int = 0, threshold: float = 0.1, hooking: int = 0, exchange: int = 0) -> FsvConfig:
         cfg = FsvConfig()
         cfg.hooking = int(hooking)
+        cfg.exchange = int(exchange)
         cfg.batch = int(batch)
         cfg.max_iters = int(max_iters)
         cfg.profile = int(bool(profile))
@@ -247,14 +248,15 @@ class Solver:
         return cfg
 
     def solve(self, batch: int = 0, max_iters: int = 0, profile: bool = False,
-              policy: int = 0, threshold: float = 0.1, hooking: int = 0) -> FsvStats:
+              policy: int = 0, threshold: float = 0.1, hooking: int = 0, exchange: int = 0) -> FsvStats:
         """Run to convergence; labels stay on the device. ``profile`` brackets
         every kernel with CUDA events (per-kernel *_ms in the stats).
         ``policy``: 0 reference default (auto, 0.1), 1 dense only, 2 sparse
         only, 3 auto with ``threshold`` (svcc.choose_kernel). ``hooking``: 0
         all-flags FastSV, else HOOKING_SET | flag bits (a HookingConfig
-        variant; HOOKING_SET alone is simplified_sv)."""
-        cfg = self._config(batch, max_iters, profile, policy, threshold, hooking)
+        variant; HOOKING_SET alone is simplified_sv). ``exchange`` (multi-rank
+        only): 0 sparse iterations exchange delta lists, 1 allreduce always."""
+        cfg = self._config(batch, max_iters, profile, policy, threshold, hooking, exchange)
         _check(self._lib.fsv_solve(self._ctx, ctypes.byref(cfg), ctypes.byref(self.stats)))
         return self.stats
 
@@ -337,7 +339,7 @@ class Solver:
 
 
 def group_run(solvers, snapshots: bool = False, snap_cap: int = 256, policy: int = 0,
-              threshold: float = 0.1, batch: int = 0):
+              threshold: float = 0.1, batch: int = 0, exchange: int = 0):
     """Emulated rank group on one device (fsv_group_solve): each Solver holds
     one row range of the same graph (``upload(g, lo, hi, cols)``); the group
     is solved in lockstep with a device min-merge in place of the NCCL
@@ -346,7 +348,7 @@ def group_run(solvers, snapshots: bool = False, snap_cap: int = 256, policy: int
     flops) and every rank's labels."""
     lib = _native.fastsv_lib()
     arr = (ctypes.c_void_p * len(solvers))(*[s._ctx.value for s in solvers])
-    cfg = Solver._config(batch, 0, False, policy, threshold, 0)
+    cfg = Solver._config(batch, 0, False, policy, threshold, 0, exchange)
     s0 = solvers[0]
     n = s0.n
     if snapshots:
@@ -362,6 +364,7 @@ def group_run(solvers, snapshots: bool = False, snap_cap: int = 256, policy: int
                                            snap.ctypes.data if n else ctypes.c_void_p(1), cap))
         k = int(iters.value)
         snap = snap[:k]
+        _check(lib.fsv_get_stats(s0._ctx, ctypes.byref(s0.stats)))
     else:
         _check(lib.fsv_group_solve(arr, len(solvers), ctypes.byref(cfg), ctypes.byref(s0.stats)))
         k = int(s0.stats.iterations)
@@ -444,7 +447,8 @@ def fastsv_la(g, cfg: DriverConfig | None = None, record_snapshots: bool = False
     Per-iteration parent vectors, iteration count, gf_changed/f_changed and
     labels are bit-identical to the reference for every DriverConfig."""
     cfg = cfg or DriverConfig()
-    return _solve_graph(g, record_snapshots, cfg.batch, device, _POLICY[cfg.force_kernel],
+    # svcc.DriverConfig works too (it has no B200 `batch` field)
+    return _solve_graph(g, record_snapshots, getattr(cfg, "batch", 0), device, _POLICY[cfg.force_kernel],
                         cfg.sparse_threshold)
 
 

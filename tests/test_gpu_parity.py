@@ -219,8 +219,14 @@ def test_single_rank_nccl_path_matches():
         s.attach_nccl(fb.Solver.nccl_unique_id(), 1, 0)
         s.upload(g)
         labels, iters, gfc, fc, ms, _ = s.run()
-    assert iters == o.iterations and gfc.tolist() == o.gf_changed.tolist()
-    assert np.array_equal(labels, o.labels)
+        assert iters == o.iterations and gfc.tolist() == o.gf_changed.tolist()
+        assert np.array_equal(labels, o.labels)
+        # the collective captured into the CUDA-graph loop (one host sync per
+        # solve) when NCCL accepts capture there, else the host loop
+        print("nccl single-rank host_syncs:", s.stats.host_syncs)
+        for batch in (1, 3):
+            labels2, iters2, gfc2, *_ = s.run(batch=batch)
+            assert iters2 == iters and np.array_equal(labels2, labels)
 
 
 def test_row_partition_upload_two_contexts_emulate_ranks():
@@ -514,3 +520,25 @@ def test_config5_full_size_matches_oracle_record():
         assert gfc.tolist() == rec["gf_changed"] and fc.tolist() == rec["f_changed"]
         assert solver.stats.component_count == rec["component_count"]
         assert gen.pairs_digest(labels) == rec["labels_digest"] == rec["uf_labels_digest"]
+
+
+def test_repeated_solves_are_deterministic(solver):
+    """Functional race detector: the BSP schedule makes every
+    solve's trace identical, whatever the interleaving of the atomics. 40
+    solves each of config 3 (15 iterations: the config whose iteration count
+    a rejected round-1 kernel variant once got wrong) and config 2 (hub
+    table, record path, push), alternating the CUDA-graph loop and the
+    host-batched loop, must all reproduce the reference's golden record."""
+    for index in (3, 2):
+        rec = load_configs()[index]
+        n, pairs = gen.baseline_graph(index)
+        g = fb.build_csr(n, pairs)
+        solver.set_hub_slots(0)
+        solver.upload(g)
+        for i in range(40):
+            st = solver.solve(batch=0 if i % 2 == 0 else 3)
+            assert st.iterations == rec["iterations"], (index, i)
+            gfc, fc, _ = solver.trace()
+            assert gfc.tolist() == rec["gf_changed"] and fc.tolist() == rec["f_changed"], (index, i)
+            if i % 8 == 0:
+                assert gen.pairs_digest(solver.labels()) == rec["labels_digest"], (index, i)

@@ -186,3 +186,31 @@ def test_group_contract_errors():
     finally:
         a.close()
         b.close()
+
+
+@pytest.mark.parametrize("ranks", [2, 4])
+def test_group_sparse_delta_exchange(ranks):
+    """Sparse (push) iterations exchange only the entries each rank lowered
+    (k_delta_compact -> gathered lists -> k_group_delta_apply), dense ones
+    min-merge the whole vector; both exchanges give the oracle's snapshots,
+    and the delta exchange really ran (exchange=0) or never ran (exchange=1)."""
+    n, e = gen.rmat(14, 16, seed=1)
+    g = fb.build_csr(n, e)
+    o = oracle.fastsv_csr(n, g.row_offsets, g.col_indices, snapshots=True)
+    for policy in (0, 2):
+        for exchange in (0, 1):
+            solvers = make_group(g, ranks)
+            try:
+                labels, iters, gfc, fc, snaps, kern, flops, all_labels = group_run(
+                    solvers, snapshots=True, snap_cap=64, policy=policy, exchange=exchange)
+                st = solvers[0].stats
+                assert iters == o.iterations and np.array_equal(snaps, o.snapshots), (policy, exchange)
+                assert all(np.array_equal(x, labels) for x in all_labels)
+                sparse = int(sum(1 for k in kern[1:] if k == 1))
+                if exchange == 0:
+                    assert st.delta_exchanges + st.dense_exchanges == iters - 1
+                    assert st.delta_exchanges <= sparse and (sparse == 0 or st.delta_exchanges > 0)
+                else:
+                    assert st.delta_exchanges == 0 and st.dense_exchanges == iters - 1
+            finally:
+                close_all(solvers)
