@@ -462,14 +462,44 @@ extern "C" int fsv_set_stream(fsv_ctx* c, void* s) {
 // upload pipeline kernels
 
 // degrees + ids for the sort, and the offsets sanity check (non-decreasing)
+constexpr uint32_t DROP = 0xffffffffu;
+#ifndef FSV_HUGE_ROW
+#define FSV_HUGE_ROW 512
+#endif
+#ifndef FSV_PIECE
+#define FSV_PIECE 1024
+#endif
+#ifndef FSV_LONG_ROW
+#define FSV_LONG_ROW 32          // rows longer than this are encoded/compacted by a whole warp
+#endif
+constexpr long long HUGE_ROW = FSV_HUGE_ROW;  // rows longer than this are cut into pieces
+constexpr long long PIECE = FSV_PIECE;        // entries per piece
+
+// Also lists the pieces of this rank's rows longer than HUGE_ROW (what
+// k_find_huge does, in the same pass over the offsets). The offsets are not
+// validated yet here, so the list is bounded (ctr[2] flags an overflow) and
+// the upload fails on the non-decreasing check before anything reads it.
 __global__ void k_degree(const int64_t* __restrict__ off, long long n, int* __restrict__ deg,
-                         int* __restrict__ ids, unsigned long long* bad) {
+                         int* __restrict__ ids, unsigned long long* bad, long long row_begin, long long row_end,
+                         long long* __restrict__ hrow, int4* __restrict__ pieces, unsigned long long* ctr,
+                         long long max_huge, long long max_pieces) {
   for (long long u = blockIdx.x * (long long)blockDim.x + threadIdx.x; u < n;
        u += (long long)gridDim.x * blockDim.x) {
     const int64_t d = off[u + 1] - off[u];
     if (d < 0) atomicMin(bad, (unsigned long long)u);
     deg[u] = (int)d;
     ids[u] = (int)u;
+    if (d > HUGE_ROW && u >= row_begin && u < row_end) {
+      const long long np = (d + PIECE - 1) / PIECE;
+      const unsigned long long h = atomicAdd(ctr, 1ull);
+      const unsigned long long b = atomicAdd(ctr + 1, (unsigned long long)np);
+      if ((long long)h >= max_huge || (long long)(b + np) > max_pieces) {
+        ctr[2] = 1ull;
+        continue;
+      }
+      hrow[h] = u - row_begin;
+      for (long long j = 0; j < np; ++j) pieces[b + j] = make_int4((int)u, (int)j, (int)j + 1, (int)h);
+    }
   }
 }
 
@@ -496,18 +526,6 @@ __global__ void k_count_ge(const int* __restrict__ sorted_desc, long long n, int
   *out = lo;
 }
 
-constexpr uint32_t DROP = 0xffffffffu;
-#ifndef FSV_HUGE_ROW
-#define FSV_HUGE_ROW 512
-#endif
-#ifndef FSV_PIECE
-#define FSV_PIECE 1024
-#endif
-#ifndef FSV_LONG_ROW
-#define FSV_LONG_ROW 32          // rows longer than this are encoded/compacted by a whole warp
-#endif
-constexpr long long HUGE_ROW = FSV_HUGE_ROW;  // rows longer than this are cut into pieces
-constexpr long long PIECE = FSV_PIECE;        // entries per piece
 
 __device__ __forceinline__ uint32_t encode_col(int v, int pv, int H) {
   return pv < H ? (HUB | (uint32_t)pv) : (uint32_t)v;
@@ -606,29 +624,6 @@ __global__ void k_orient_encode(const int64_t* __restrict__ off, const ColT* __r
 
 // Pieces of rows longer than HUGE_ROW: one warp per piece (listed by the
 // host), 8 entries per lane in flight; kept counts summed per row.
-// Runs after the offsets were checked non-decreasing (k_degree), so the
-// counts are bounded by construction; the bounds are still enforced (ctr[2]
-// flags an overflow, the upload then fails instead of writing past a buffer).
-__global__ void k_find_huge(const int64_t* __restrict__ off, long long row_begin, long long rows,
-                            long long* __restrict__ hrow, int4* __restrict__ pieces,
-                            unsigned long long* ctr, long long max_huge, long long max_pieces) {
-  for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < rows;
-       r += (long long)gridDim.x * blockDim.x) {
-    const long long u = row_begin + r;
-    const long long d = off[u + 1] - off[u];
-    if (d <= HUGE_ROW) continue;
-    const long long np = (d + PIECE - 1) / PIECE;
-    const unsigned long long h = atomicAdd(ctr, 1ull);
-    const unsigned long long b = atomicAdd(ctr + 1, (unsigned long long)np);
-    if ((long long)h >= max_huge || (long long)(b + np) > max_pieces) {
-      ctr[2] = 1ull;
-      continue;
-    }
-    hrow[h] = r;
-    for (long long j = 0; j < np; ++j) pieces[b + j] = make_int4((int)u, (int)j, (int)j + 1, (int)h);
-  }
-}
-
 template <typename ColT>
 __global__ void k_piece_encode(const int4* __restrict__ pieces, const unsigned long long* npieces_p,
                                long long u0, long long u1, const int64_t* __restrict__ off,
@@ -1159,8 +1154,16 @@ static int upload_impl(fsv_ctx* c, int64_t n, const int64_t* h_off_arr, const Co
   auto& pos = c->ws.slot_of;
   CUDA_TRY(deg.alloc(n)); CUDA_TRY(ids.alloc(n));
   CUDA_TRY(deg_sorted.alloc(n)); CUDA_TRY(ids_sorted.alloc(n)); CUDA_TRY(pos.alloc(n));
-  if (n) k_degree<<<grid_for(c, n, 256), 256, 0, st>>>(offp, n, deg.p, ids.p, d_bad.p + 1);
+  if (n)
+    k_degree<<<grid_for(c, n, 256), 256, 0, st>>>(offp, n, deg.p, ids.p, d_bad.p + 1, row_begin, row_end,
+                                                  c->ws.hrow.p, c->ws.pieces.p, huge_ctr, max_huge, max_pieces);
   int H = 0;
+  // a valid CSR row has fewer than n entries (deduplicated, no self-loop),
+  // so the degree sort needs bit_length(n - 1) key bits (22 for RMAT-22:
+  // three onesweep passes instead of four). A malformed row with more only
+  // changes which endpoint keeps an edge, never that exactly one does.
+  int deg_bits = 1;
+  while (deg_bits < 32 && ((int64_t)1 << deg_bits) < n) ++deg_bits;
   {
     // one temp buffer for the sort and the per-chunk scans (no reallocation
     // while the pipeline runs: cudaFree would synchronise the device)
@@ -1170,7 +1173,7 @@ static int upload_impl(fsv_ctx* c, int64_t n, const int64_t* h_off_arr, const Co
       max_nr = std::max<long long>(max_nr, chunk_rows[k + 1] - chunk_rows[k]);
     if (n)
       cub::DeviceRadixSort::SortPairsDescending(nullptr, sort_bytes, deg.p, deg_sorted.p, ids.p,
-                                                ids_sorted.p, (int)n, 0, 32, st);
+                                                ids_sorted.p, (int)n, 0, deg_bits, st);
     cub::DeviceScan::ExclusiveScan(nullptr, b1, (long long*)nullptr, (long long*)nullptr, cuda::std::plus<>{},
                                    cub::FutureValue<long long>(nullptr), (int)max_nr, st);
     cub::DeviceScan::ExclusiveScan(nullptr, b2, (int*)nullptr, (int*)nullptr, cuda::std::plus<>{},
@@ -1181,7 +1184,7 @@ static int upload_impl(fsv_ctx* c, int64_t n, const int64_t* h_off_arr, const Co
     size_t tmp_bytes = c->ws.tmp.n;
     auto& tmp = c->ws.tmp;
     CUDA_TRY(cub::DeviceRadixSort::SortPairsDescending(tmp.p, tmp_bytes, deg.p, deg_sorted.p, ids.p,
-                                                       ids_sorted.p, (int)n, 0, 32, st));
+                                                       ids_sorted.p, (int)n, 0, deg_bits, st));
     // hubs: the first positions with degree >= kHubMinDegree, at most kHubMax
     const int probe = (int)std::min<int64_t>(n, kHubMax);
     std::vector<int> top(probe);
@@ -1190,11 +1193,6 @@ static int upload_impl(fsv_ctx* c, int64_t n, const int64_t* h_off_arr, const Co
     CUDA_TRY(cudaMemcpyAsync(&h_badoff, d_bad.p + 1, sizeof h_badoff, cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaStreamSynchronize(st));
     if (h_badoff != ~0ull) return fail(FSV_ERR_INPUT, "row_offsets must be non-decreasing");
-    // offsets are non-decreasing from here on: the huge-row piece list
-    // (which sizes its writes by per-row differences) is safe to build
-    if (rows)
-      k_find_huge<<<grid_for(c, rows, 256), 256, 0, st>>>(offp, row_begin, rows, c->ws.hrow.p,
-                                                          c->ws.pieces.p, huge_ctr, max_huge, max_pieces);
     int cand = 0;
     while (cand < probe && top[cand] >= kHubMinDegree) ++cand;
     H = (c->hub_limit >= 0) ? std::min(cand, c->hub_limit) : 0;
