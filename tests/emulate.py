@@ -17,6 +17,13 @@ logic and the collective semantics can be tested on CPU:
 
 ``allreduce_min`` is injected so the same code runs single-process (identity)
 or across gloo ranks (torch.distributed.all_reduce with ReduceOp.MIN).
+
+Sparse iterations (the reference's rule, gf_changed < 0.1 n, driver.py:51-61)
+may instead take the library's delta exchange (fsv_config.exchange = 0): each
+rank's (index, value) pairs of the entries it lowered (N[i] < gf_k[i]) are
+all-gathered (``allgather_pairs``: counts first, then the lists padded to the
+largest, as k_delta_compact + two ncclAllGathers) and min-reduced into N
+(k_delta_apply), falling back to the allreduce when the lists are not smaller.
 """
 
 from __future__ import annotations
@@ -82,9 +89,26 @@ def hook(rows, cols, F, G, N):
     _scatter_min(N, t[ok2], val[ok2])
 
 
+def delta_exchange(N, G, allgather_pairs, nranks):
+    """The sparse-iteration exchange; returns (N merged, bytes this rank sent)."""
+    idx = np.flatnonzero(N < G)
+    mine = np.stack([idx, N[idx]], 1).astype(np.int64)
+    lists = allgather_pairs(mine)
+    cmax = max(len(x) for x in lists)
+    if 8 * cmax * nranks >= 2 * (nranks - 1) / nranks * 4 * N.size:
+        return None, 0
+    out = N.copy()
+    for x in lists:
+        if len(x):
+            np.minimum.at(out, x[:, 0], x[:, 1])
+    return out, 8 * cmax * (nranks - 1)
+
+
 def run(n, offsets, cols, row_begin=0, row_end=None, allreduce_min=lambda a: a,
-        cap=4096, record=True):
-    """Returns (labels, iterations, gf_changed, f_changed, snapshots)."""
+        cap=4096, record=True, allgather_pairs=None, nranks=1, stats=None, threshold=0.1):
+    """Returns (labels, iterations, gf_changed, f_changed, snapshots). With
+    ``allgather_pairs``, sparse iterations use the delta exchange; ``stats``
+    (a dict) then receives the exchange counts and bytes."""
     row_end = n if row_end is None else row_end
     rows, ocols = oriented_entries(n, offsets, cols, row_begin, row_end)
     f1 = allreduce_min(first_parents(n, offsets, cols, row_begin, row_end))
@@ -99,7 +123,19 @@ def run(n, offsets, cols, row_begin=0, row_end=None, allreduce_min=lambda a: a,
         it += 1
         N = G.copy()                     # f_k initialised to gf_{k-1} (shortcut folded)
         hook(rows, ocols, F, G, N)
-        N = allreduce_min(N)
+        sparse = gfc[-1] < threshold * n
+        merged = None
+        if allgather_pairs is not None and sparse:
+            merged, sent = delta_exchange(N, G, allgather_pairs, nranks)
+        if merged is not None:
+            N = merged
+            if stats is not None:
+                stats["delta"] = stats.get("delta", 0) + 1
+                stats["bytes"] = stats.get("bytes", 0) + sent
+        else:
+            N = allreduce_min(N)
+            if stats is not None:
+                stats["dense"] = stats.get("dense", 0) + 1
         G2 = N[N]
         gfc.append(int(np.count_nonzero(G2 != G)))
         fc.append(int(np.count_nonzero(N != F)))

@@ -44,6 +44,19 @@ def _worker(rank, world, port, q):
             dist.all_reduce(t, op=dist.ReduceOp.MIN)
             return t.numpy()
 
+        def allgather_pairs(pairs):
+            # the library's protocol: one allgather of the counts, then one of
+            # the (index, value) lists padded to the largest
+            cnt = torch.tensor([len(pairs)], dtype=torch.int64)
+            counts = [torch.zeros(1, dtype=torch.int64) for _ in range(world)]
+            dist.all_gather(counts, cnt)
+            cmax = max(int(c.item()) for c in counts)
+            buf = torch.zeros((max(cmax, 1), 2), dtype=torch.int64)
+            buf[:len(pairs)] = torch.from_numpy(pairs)
+            outs = [torch.zeros_like(buf) for _ in range(world)]
+            dist.all_gather(outs, buf)
+            return [o[:int(c.item())].numpy() for o, c in zip(outs, counts)]
+
         results = []
         cases = [(c.name, c.n, c.edges) for c in load_suite()[::9]]
         n, e = gen.rmat(11, 16, seed=9)
@@ -53,6 +66,11 @@ def _worker(rank, world, port, q):
             lo, hi = bench.row_partition(g.row_offsets, world, rank)
             f, it, gfc, fc, snaps = emulate.run(n, g.row_offsets, g.col_indices, lo, hi, allreduce_min)
             results.append((name, it, gfc, fc, np.stack(snaps) if snaps else None))
+            # the same with the sparse-iteration delta exchange
+            st = {}
+            f, it, gfc, fc, snaps = emulate.run(n, g.row_offsets, g.col_indices, lo, hi, allreduce_min,
+                                                allgather_pairs=allgather_pairs, nranks=world, stats=st)
+            results.append((name + "#delta", it, gfc, fc, np.stack(snaps) if snaps else None, st))
         if rank == 0:
             q.put(results)
     finally:
@@ -78,7 +96,12 @@ def test_two_rank_gloo_schedule_matches_single_device():
         p.join(timeout=60)
         assert p.exitcode == 0
     golden = {c.name: c for c in load_suite()}
-    for name, it, gfc, fc, snaps in results:
+    deltas = 0
+    for rec in results:
+        name, it, gfc, fc, snaps = rec[:5]
+        if name.endswith("#delta"):
+            deltas += rec[5].get("delta", 0)
+            name = name[:-len("#delta")]
         if name in golden:
             c = golden[name]
             assert it == c.iterations and gfc == c.gf_changed and fc == c.f_changed, name
@@ -89,6 +112,7 @@ def test_two_rank_gloo_schedule_matches_single_device():
             o = oracle.fastsv_csr(n, g.row_offsets, g.col_indices, snapshots=True)
             assert it == o.iterations and gfc == o.gf_changed.tolist(), name
             assert np.array_equal(snaps, o.snapshots), name
+    assert deltas > 0, "no sparse iteration took the delta exchange"
 
 
 def test_row_partition_covers_rows_and_balances_entries():
