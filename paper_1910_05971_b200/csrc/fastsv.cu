@@ -1215,7 +1215,7 @@ static int upload_impl(fsv_ctx* c, int64_t n, const int64_t* h_off_arr, const Co
   }
   c->H = H;
   c->HT = HT;
-  CUDA_TRY(c->hub_id.alloc(std::max(HT, 4)));
+  CUDA_TRY(c->hub_id.alloc((size_t)((std::max(HT, 4) + (1 << 19) - 1) >> 19 << 19)));   // 2 MB multiple
   if (n) k_positions<<<grid_for(c, n, 256), 256, 0, st>>>(ids_sorted.p, n, HT, pos.p, c->hub_id.p);
   umark(1);
 
@@ -1362,10 +1362,17 @@ static int upload_impl(fsv_ctx* c, int64_t n, const int64_t* h_off_arr, const Co
   if (const char* e = getenv("FSV_VPAD")) vpad = atoll(e) / 4 * 4;
   CUDA_TRY(c->xb.alloc(nv + vpad)); CUDA_TRY(c->gb.alloc(nv + vpad));
   c->X = c->xb.p + vpad; c->Y = c->f1.p; c->G = c->gb.p + vpad;
-  CUDA_TRY(c->G_hub.alloc(std::max(HT, 4))); {
+  // The hot hub arrays get whole 2 MB-aligned allocations (cudaMalloc aligns
+  // an allocation of >= 2 MB to 2 MB), like the vertex arrays: the dense
+  // hook's time depends on their placement relative to the vertex arrays at
+  // sub-2 MB offsets (profiles/r02/placement.txt), and a small
+  // allocation would land wherever the allocator's pool puts it.
+  constexpr long long kAlign2M = (2LL << 20) / (long long)sizeof(int);
+  auto round2m = [&](long long ints) { return (std::max<long long>(ints, 4) + kAlign2M - 1) / kAlign2M * kAlign2M; };
+  CUDA_TRY(c->G_hub.alloc((size_t)round2m(HT))); {
     long long hpad = 0;   // dev: FSV_HPAD shifts the hub accumulator (placement checks)
     if (const char* e = getenv("FSV_HPAD")) hpad = atoll(e);
-    CUDA_TRY(c->hub_acc.alloc(std::max<long long>(acc_len(HT), 4) + hpad));
+    CUDA_TRY(c->hub_acc.alloc((size_t)round2m(acc_len(HT) + hpad)));
     c->hacc = c->hub_acc.p + hpad;
   }
   CUDA_TRY(c->done.alloc(1)); CUDA_TRY(c->ticket.alloc(1));

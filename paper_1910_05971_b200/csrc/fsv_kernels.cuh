@@ -366,6 +366,11 @@ __device__ __forceinline__ void emit_row(int u, int gu, int val, const int* __re
 #ifndef FSV_ROW_FILTER
 #define FSV_ROW_FILTER 0
 #endif
+// Dev speed-of-light probes (wrong results, timing only): bit 0 drops the
+// dense hook's emissions, bit 1 its global gathers.
+#ifndef FSV_SOL
+#define FSV_SOL 0
+#endif
 __device__ __forceinline__ void emit_row_t(int u, int val, int t, const int* __restrict__ F,
                                            const int* __restrict__ G, int* __restrict__ N) {
   red_min(N + u, val);
@@ -723,8 +728,12 @@ __global__ void __launch_bounds__(HOOK_THREADS, 1) k_hook(HookArgs a) {
       int val[EPL];
 #pragma unroll
       for (int j = 0; j < EPL; ++j)
+#if FSV_SOL & 2
+        val[j] = s_hub[HOT_ACC + (c[j] & 0x7fffu)];   // dev speed-of-light probe: no global gathers (wrong results)
+#else
         val[j] = TIER ? gather_gf_tier(c[j], s_base, G, a.G_hub, (uint32_t)a.H)
                       : gather_gf(c[j], s_base, G);
+#endif
       // last header of this lane
       int lu = -1, lgu = INF;
 #pragma unroll
@@ -768,7 +777,7 @@ __global__ void __launch_bounds__(HOOK_THREADS, 1) k_hook(HookArgs a) {
       // a run carried in from a scan step is emitted here by lane 0.
       if (!dense && !__any_sync(0xffffffffu, nrec > FSV_REC)) {
         if (lane == 0 && carry_run < carry_gu) emit_row(carry_u, carry_gu, carry_run, F, G, N);
-        if (nrec) {
+        if (nrec && !(FSV_SOL & 1)) {
           // second pass: pick out the (at most two) records of this lane
           uint32_t rx0 = 0u, rx1 = 0u;
           int ry0 = 0, ry1 = 0;
@@ -855,7 +864,7 @@ __global__ void __launch_bounds__(HOOK_THREADS, 1) k_hook(HookArgs a) {
         cgu = h ? val[j] : cgu;
         run = h ? INF : min(run, val[j]);
       }
-      if (act) {
+      if (act && !(FSV_SOL & 1)) {
         int t[EPL];
 #pragma unroll
         for (int j = 0; j < EPL; ++j) {

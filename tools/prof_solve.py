@@ -37,6 +37,10 @@ for u in range(a.uploads):
     torch.cuda.synchronize()
     print(f"upload {u}: {e0.elapsed_time(e1):.3f} ms", flush=True)
 for _ in range(a.reps):
-    r = s.solve(profile=a.profile)
+    try:
+        r = s.solve(profile=a.profile)
+    except Exception as e:      # dev probes with broken semantics may not converge
+        print("solve failed:", e)
+        break
     print(f"solve {r.solve_ms:.3f} ms iters {r.iterations} hook {r.hook_ms:.3f} ({r.hook_launches}) push {r.push_ms:.3f} "
           f"first {r.first_ms:.3f} shortcut {r.shortcut_ms:.3f}", flush=True)
