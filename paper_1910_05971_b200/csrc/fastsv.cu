@@ -2582,7 +2582,20 @@ extern "C" int fsv_solve(fsv_ctx* c, const fsv_config* cfg, fsv_stats* stats) {
 // (the giant component of a skewed graph would otherwise serialise one
 // counter), then the representatives (label[u] == u, ascending) compacted
 // with their sizes, and the labels widened to int64 (the reference's ID_DTYPE).
-__global__ void k_comp_sizes(const int* __restrict__ L, long long n, unsigned* __restrict__ cnt) {
+// Two levels of aggregation: lanes with the same label (match_any), then a
+// per-block shared-memory table of labels (open addressing, flushed once per
+// block), so the giant component of a skewed graph costs one global atomic
+// per block instead of one per warp (all on one L2 line: 131 K for RMAT-22,
+// 180 µs serialised). Labels that do not find a table slot go to global.
+constexpr int kSizeSlots = 1024;   // power of two
+__global__ void __launch_bounds__(256) k_comp_sizes(const int* __restrict__ L, long long n, unsigned* __restrict__ cnt) {
+  __shared__ int s_key[kSizeSlots];
+  __shared__ unsigned s_val[kSizeSlots];
+  for (int i = threadIdx.x; i < kSizeSlots; i += blockDim.x) {
+    s_key[i] = -1;
+    s_val[i] = 0u;
+  }
+  __syncthreads();
   const long long stride = (long long)gridDim.x * blockDim.x;
   for (long long base = (long long)blockIdx.x * blockDim.x; base < n; base += stride) {  // block-uniform
     const long long u = base + threadIdx.x;
@@ -2591,9 +2604,25 @@ __global__ void k_comp_sizes(const int* __restrict__ L, long long n, unsigned* _
     const unsigned active = __ballot_sync(0xffffffffu, on);
     if (on) {
       const unsigned peers = __match_any_sync(active, l);
-      if ((int)(threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(cnt + l, (unsigned)__popc(peers));
+      if ((int)(threadIdx.x & 31) == __ffs(peers) - 1) {
+        const unsigned k = (unsigned)__popc(peers);
+        unsigned h = ((unsigned)l * 2654435761u) >> 22;   // 10 bits
+        bool done = k == 1u;   // a label alone in its warp: straight to global
+        if (done) atomicAdd(cnt + l, 1u);
+        for (int probe = 0; probe < 8 && !done; ++probe, h = (h + 1) & (kSizeSlots - 1)) {
+          const int prev = atomicCAS(&s_key[h], -1, l);
+          if (prev == -1 || prev == l) {
+            atomicAdd(&s_val[h], k);
+            done = true;
+          }
+        }
+        if (!done) atomicAdd(cnt + l, k);
+      }
     }
   }
+  __syncthreads();
+  for (int i = threadIdx.x; i < kSizeSlots; i += blockDim.x)
+    if (s_key[i] >= 0) atomicAdd(cnt + s_key[i], s_val[i]);
 }
 
 struct IsRoot {
