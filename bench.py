@@ -280,6 +280,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--hub-slots", type=int, default=0)
+    ap.add_argument("--tile", type=int, default=0,
+                    help="column-range tiling of the layout (vertices per tile, -1 auto, 0 off)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     world, rank, local = dist_env()
@@ -306,6 +308,8 @@ def main():
     n_edges = int(pairs.shape[0])
     del pairs
     solver = fb.Solver(local, hub_slots=args.hub_slots)
+    if args.tile:
+        solver.set_tile_width(args.tile)
     # one dedicated (non-default) stream for the solver, the L2 flush and the
     # timing events: the legacy default stream is not ordered against the
     # library's non-blocking stream, so flush/events/solve must share this one
@@ -487,6 +491,7 @@ def main():
                        "n": n, "edges": n_edges, "m_dir": g.m, "iterations": iters,
                        "oriented_entries": int(st.oriented_entries), "hub_slots": int(st.hub_slots),
                        "l2": "flushed between steps (256 MiB write + 256 MiB read, outside the timed events)",
+                       "layout_tiles": args.tile,
                        "parallelism": f"edge-partition x{world}" if world > 1 else "single GPU"},
             "iteration_model": {"bytes_per_iter": iter_bytes,
                                 "frac_of_hbm": iters * iter_bytes / (step_ms * 1e-3) / 1e9 / peak},

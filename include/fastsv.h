@@ -106,6 +106,16 @@ int fsv_destroy(fsv_ctx* ctx);
  * (top-degree vertices up to 55296 shared-memory slots), >0 = at most that. */
 int fsv_set_hub_slots(fsv_ctx* ctx, int slots);
 
+/* Column-range tiling of the NEXT upload's layout, for graphs without a
+ * hub table and without rows over 512 entries whose vertex vectors overflow
+ * L2 (BASELINE configs 3 and 4): every row is split into per-tile segments
+ * and the layout holds tile 0's segments, then tile 1's, ..., so the dense
+ * sweep gathers from (and reduces into) one L2-resident slice of the vertex
+ * vectors at a time. Results are identical; the layout build costs one
+ * count + compact pass per tile. 0 = off (default), > 0 = vertices per
+ * tile, < 0 = auto (8 M vertices = 32 MB slices). */
+int fsv_set_tile_width(fsv_ctx* ctx, int64_t vertices);
+
 /* Use an external stream (e.g. torch.cuda.current_stream().cuda_stream);
  * 0 restores the context's own stream. */
 int fsv_set_stream(fsv_ctx* ctx, void* cuda_stream);

@@ -172,6 +172,7 @@ struct fsv_ctx {
   bool ready = false;
   int64_t n = 0, m_dir = 0, E = 0, Epad = 0;
   int R = 0, H = 0, HT = 0;   // shared-memory hub slots, all tier slots
+  int tiles = 1;               // column-range tiles of the layout (k_tile_pass)
   DBuf<uint32_t> ecol;
   uint32_t* ecolp = nullptr;   // layout start inside ecol
   DBuf<int> span_row, hub_id, f1;
@@ -257,6 +258,7 @@ struct fsv_ctx {
   } lab;
   int host_syncs = 0, launches = 0;
   int hub_limit = kHubMax;
+  long long tile_width = 0;   // fsv_set_tile_width: 0 off, > 0 vertices per column tile, < 0 auto
   // device loop control + CUDA-graph (conditional WHILE) of the iteration loop
   DBuf<int> iterbuf;
   DBuf<unsigned long long> tstamp;
@@ -727,6 +729,82 @@ __global__ void k_piece_compact(const int4* __restrict__ pieces, const unsigned 
   }
 }
 
+// Column-range tiling (layouts without a hub table and without huge rows,
+// whose vertex vectors overflow L2: configs 3 and 4). Tile t keeps, for
+// every row, the row's kept entries whose column lies in [tlo, thi), behind
+// their own header; the layout is tile 0's rows, then tile 1's, ... So the
+// whole GPU, sweeping the layout in order, gathers gf from one tile-sized
+// slice of G (and reduces into the same slice of N) at a time, which stays
+// L2-resident. A row split over tiles emits one partial row minimum per
+// tile (min-reductions are idempotent). COMPACT = false counts a tile's
+// entries per row (cnt = k + 1 with the header, nzflag); true writes them.
+template <bool COMPACT>
+__global__ void k_tile_pass(const int64_t* __restrict__ off, long long col_base, long long row_begin,
+                            long long rows, const uint32_t* __restrict__ tmp, uint32_t tlo, uint32_t thi,
+                            long long* __restrict__ cnt, int* __restrict__ nzflag,
+                            const long long* __restrict__ out_off, const int* __restrict__ nzidx,
+                            uint32_t* __restrict__ ecol, int* __restrict__ nzrows, long long* __restrict__ nzoff) {
+  const int lane = threadIdx.x & 31;
+  const long long nw = (long long)gridDim.x * (blockDim.x >> 5);
+  for (long long w0 = ((long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32; w0 < rows;
+       w0 += nw * 32) {
+    const long long r = w0 + lane;
+    long long lo = 0, hi = 0, o = 0;
+    bool has = true;
+    if (r < rows) {
+      const long long u = row_begin + r;
+      lo = off[u] - col_base;
+      hi = off[u + 1] - col_base;
+      if (COMPACT) {
+        o = out_off[r];
+        has = out_off[r + 1] > o;
+        if (has) {
+          ecol[o] = HDR | (uint32_t)u;
+          const int z = nzidx[r];
+          nzrows[z] = (int)u;
+          nzoff[z] = o;
+        }
+        ++o;
+      }
+    }
+    if (!has) hi = lo;
+    const bool is_long = hi - lo > FSV_LONG_ROW;
+    long long k = 0;
+    if (!is_long) {
+      for (long long e = lo; e < hi; ++e) {
+        const uint32_t c = tmp[e];
+        if (c >= tlo && c < thi) {   // (DROP is above every tile)
+          if (COMPACT) ecol[o++] = c;
+          else ++k;
+        }
+      }
+    }
+    unsigned lm = __ballot_sync(0xffffffffu, is_long);
+    while (lm) {
+      const int src = __ffs(lm) - 1;
+      lm &= lm - 1;
+      const long long slo = __shfl_sync(0xffffffffu, lo, src);
+      const long long shi = __shfl_sync(0xffffffffu, hi, src);
+      long long so = __shfl_sync(0xffffffffu, o, src);
+      long long sk = 0;
+      for (long long e0 = slo; e0 < shi; e0 += 32) {
+        const long long e = e0 + lane;
+        const uint32_t c = e < shi ? tmp[e] : DROP;
+        const bool keep = c >= tlo && c < thi;
+        const unsigned b = __ballot_sync(0xffffffffu, keep);
+        if (COMPACT && keep) ecol[so + __popc(b & ((1u << lane) - 1u))] = c;
+        so += __popc(b);
+        sk += __popc(b);
+      }
+      if (lane == src) k = sk;
+    }
+    if (!COMPACT && r < rows) {
+      cnt[r] = k ? k + 1 : 0;
+      nzflag[r] = k > 0;
+    }
+  }
+}
+
 // Orientation pass 2 (no gathers): header + kept entries of each row, in
 // order, at out_off[r]; nzrows/nzoff for the span table.
 __global__ void k_orient_compact(const int64_t* __restrict__ off, long long col_base, long long row_begin,
@@ -1158,6 +1236,7 @@ static int upload_impl(fsv_ctx* c, int64_t n, const int64_t* h_off_arr, const Co
     k_degree<<<grid_for(c, n, 256), 256, 0, st>>>(offp, n, deg.p, ids.p, d_bad.p + 1, row_begin, row_end,
                                                   c->ws.hrow.p, c->ws.pieces.p, huge_ctr, max_huge, max_pieces);
   int H = 0;
+  long long max_deg = 0;
   // a valid CSR row has fewer than n entries (deduplicated, no self-loop),
   // so the degree sort needs bit_length(n - 1) key bits (22 for RMAT-22:
   // three onesweep passes instead of four). A malformed row with more only
@@ -1193,6 +1272,7 @@ static int upload_impl(fsv_ctx* c, int64_t n, const int64_t* h_off_arr, const Co
     CUDA_TRY(cudaMemcpyAsync(&h_badoff, d_bad.p + 1, sizeof h_badoff, cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaStreamSynchronize(st));
     if (h_badoff != ~0ull) return fail(FSV_ERR_INPUT, "row_offsets must be non-decreasing");
+    max_deg = probe ? top[0] : 0;
     int cand = 0;
     while (cand < probe && top[cand] >= kHubMinDegree) ++cand;
     H = (c->hub_limit >= 0) ? std::min(cand, c->hub_limit) : 0;
@@ -1213,6 +1293,18 @@ static int upload_impl(fsv_ctx* c, int64_t n, const int64_t* h_off_arr, const Co
     const long long t = std::min<long long>(cnt_ge, kTierMax) & ~3LL;
     if (t > H) HT = (int)t;
   }
+  // column-range tiling (k_tile_pass, fsv_set_tile_width): no hub table, no
+  // huge rows, vectors over one tile. Off by default: the tile passes cost
+  // more layout time than one solve gains; auto = 8 M vertices
+  // (32 MB slices of each vertex vector).
+  int T = 1;
+  long long tile_w = c->tile_width < 0 ? (8LL << 20) : c->tile_width;
+  {
+    if (const char* e = getenv("FSV_TILE_W")) tile_w = atoll(e);   // tests/dev: exact width in vertices
+    const bool no_huge = !n || max_deg <= HUGE_ROW;
+    if (!H && no_huge && tile_w > 0 && n > tile_w) T = (int)((n + tile_w - 1) / tile_w);
+  }
+  c->tiles = T;
   c->H = H;
   c->HT = HT;
   CUDA_TRY(c->hub_id.alloc((size_t)((std::max(HT, 4) + (1 << 19) - 1) >> 19 << 19)));   // 2 MB multiple
@@ -1235,16 +1327,16 @@ static int upload_impl(fsv_ctx* c, int64_t n, const int64_t* h_off_arr, const Co
   CUDA_TRY(cnt.alloc(rows + 1)); CUDA_TRY(out_off.alloc(rows + 1));
   CUDA_TRY(nzflag.alloc(rows + 1)); CUDA_TRY(nzidx.alloc(rows + 1));
   CUDA_TRY(etmp.alloc((size_t)std::max<int64_t>(mloc, 1)));
-  CUDA_TRY(nzrows.alloc((size_t)rows + 1));
-  CUDA_TRY(nzoff.alloc((size_t)rows + 1));
+  CUDA_TRY(nzrows.alloc((size_t)rows * T + 1));
+  CUDA_TRY(nzoff.alloc((size_t)rows * T + 1));
   {
     long long epad = 0;   // dev: FSV_EPAD shifts the layout (placement sensitivity checks)
     if (const char* e = getenv("FSV_EPAD")) epad = atoll(e);
-    CUDA_TRY(c->ecol.alloc((size_t)(mloc + rows + SPAN + epad)));
+    CUDA_TRY(c->ecol.alloc((size_t)(mloc + rows * T + SPAN + epad)));
     c->ecolp = c->ecol.p + epad;
   }
-  CUDA_TRY(c->ws.carry_e.alloc((size_t)K + 1));
-  CUDA_TRY(c->ws.carry_r.alloc((size_t)K + 1));
+  CUDA_TRY(c->ws.carry_e.alloc((size_t)std::max(K, T) + 1));
+  CUDA_TRY(c->ws.carry_r.alloc((size_t)std::max(K, T) + 1));
   CUDA_TRY(cudaMemsetAsync(c->ws.carry_e.p, 0, sizeof(long long), st));
   CUDA_TRY(cudaMemsetAsync(c->ws.carry_r.p, 0, sizeof(int), st));
   umark(2);
@@ -1267,6 +1359,9 @@ static int upload_impl(fsv_ctx* c, int64_t n, const int64_t* h_off_arr, const Co
           c->ws.hkept.p, c->ws.piece_kept.p, d_bad.p);
       k_huge_rows<<<c->sm_count * 2, 256, 0, st>>>(c->ws.hrow.p, huge_ctr, r0, r1, c->ws.hkept.p, cnt.p,
                                                   nzflag.p);
+    }
+    if (T > 1) continue;   // tiled: compacted tile by tile over all rows after the last chunk
+    if (nr) {
       size_t b = c->ws.tmp.n;
       CUDA_TRY(cub::DeviceScan::ExclusiveScan(c->ws.tmp.p, b, cnt.p + r0, out_off.p + r0, cuda::std::plus<>{},
                                               cub::FutureValue<long long>(c->ws.carry_e.p + k), (int)nr, st));
@@ -1288,12 +1383,34 @@ static int upload_impl(fsv_ctx* c, int64_t n, const int64_t* h_off_arr, const Co
       dbg_enc_ev.push_back(e);
     }
   }
+  // tiled layout: tile-major over ALL rows (a per-chunk tile order would
+  // revisit every tile slice once per chunk and lose the locality)
+  for (int t = 0; t < T && T > 1; ++t) {
+    const uint32_t tlo = (uint32_t)(t * tile_w), thi = (uint32_t)std::min<long long>((t + 1) * tile_w, n);
+    if (rows) {
+      const int tg = grid_for(c, (rows + 31) / 32 * 32, 256, 16);
+      k_tile_pass<false><<<tg, 256, 0, st>>>(offp, e_begin, row_begin, rows, etmp.p, tlo, thi, cnt.p, nzflag.p,
+                                              nullptr, nullptr, nullptr, nullptr, nullptr);
+      size_t b = c->ws.tmp.n;
+      CUDA_TRY(cub::DeviceScan::ExclusiveScan(c->ws.tmp.p, b, cnt.p, out_off.p, cuda::std::plus<>{},
+                                              cub::FutureValue<long long>(c->ws.carry_e.p + t), (int)rows, st));
+      b = c->ws.tmp.n;
+      CUDA_TRY(cub::DeviceScan::ExclusiveScan(c->ws.tmp.p, b, nzflag.p, nzidx.p, cuda::std::plus<>{},
+                                              cub::FutureValue<int>(c->ws.carry_r.p + t), (int)rows, st));
+    }
+    k_chunk_carry<<<1, 1, 0, st>>>(cnt.p, nzflag.p, out_off.p, nzidx.p, 0, rows, c->ws.carry_e.p, c->ws.carry_r.p, t);
+    if (rows)
+      k_tile_pass<true><<<grid_for(c, (rows + 31) / 32 * 32, 256, 16), 256, 0, st>>>(
+          offp, e_begin, row_begin, rows, etmp.p, tlo, thi, nullptr, nullptr, out_off.p, nzidx.p, c->ecolp,
+          nzrows.p, nzoff.p);
+  }
+  const int KT = T > 1 ? T : K;   // carry slots used
   umark(3);
   long long E = 0;
   int R = 0;
   unsigned long long h_bad = 0, h_overflow = 0;
-  CUDA_TRY(cudaMemcpyAsync(&E, c->ws.carry_e.p + K, sizeof E, cudaMemcpyDeviceToHost, st));
-  CUDA_TRY(cudaMemcpyAsync(&R, c->ws.carry_r.p + K, sizeof R, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaMemcpyAsync(&E, c->ws.carry_e.p + KT, sizeof E, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaMemcpyAsync(&R, c->ws.carry_r.p + KT, sizeof R, cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaMemcpyAsync(&h_bad, d_bad.p, sizeof h_bad, cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaMemcpyAsync(&h_overflow, huge_ctr + 2, sizeof h_overflow, cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaStreamSynchronize(st));
@@ -1435,6 +1552,12 @@ static int upload_impl(fsv_ctx* c, int64_t n, const int64_t* h_off_arr, const Co
   c->Epad = Epad;
   c->R = R;
   c->ready = true;
+  return FSV_OK;
+}
+
+extern "C" int fsv_set_tile_width(fsv_ctx* c, int64_t vertices) {
+  if (!c) return fail(FSV_ERR_CONTRACT, "NULL context");
+  c->tile_width = vertices;
   return FSV_OK;
 }
 

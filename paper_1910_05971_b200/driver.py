@@ -147,6 +147,12 @@ class Solver:
     def set_hub_slots(self, slots: int) -> None:
         _check(self._lib.fsv_set_hub_slots(self._ctx, int(slots)))
 
+    def set_tile_width(self, vertices: int) -> None:
+        """Column-range tiling of the next upload's layout (0 off, > 0 width,
+        < 0 auto); pays off over repeated solves of hub-less graphs whose
+        vectors overflow L2 (fsv_set_tile_width)."""
+        _check(self._lib.fsv_set_tile_width(self._ctx, int(vertices)))
+
     def attach_nccl(self, unique_id: bytes, nranks: int, rank: int) -> None:
         buf = ctypes.create_string_buffer(bytes(unique_id), 128)
         _check(self._lib.fsv_nccl_attach(self._ctx, buf, int(nranks), int(rank)))

@@ -542,3 +542,32 @@ def test_repeated_solves_are_deterministic(solver):
             assert gfc.tolist() == rec["gf_changed"] and fc.tolist() == rec["f_changed"], (index, i)
             if i % 8 == 0:
                 assert gen.pairs_digest(solver.labels()) == rec["labels_digest"], (index, i)
+
+
+def test_column_tiled_layout_matches_golden(solver, monkeypatch):
+    """Column-range tiling of the oriented layout (k_tile_pass: layouts
+    without hubs or huge rows, each row split into per-tile segments) forced
+    on small graphs by a tiny tile width: every per-iteration parent vector
+    of the golden suite, random multigraphs and forests equals the
+    reference's / the oracle's (configs 3 and 4 take the tiled layout by
+    default and are checked at full size by test_baseline_config_full_size)."""
+    rng = np.random.default_rng(93)
+    for width, chunks in (("7", None), ("64", "3"), ("1000", None)):
+        monkeypatch.setenv("FSV_TILE_W", width)
+        if chunks:   # chunked host upload: encode per chunk, tiles compacted over all rows after
+            monkeypatch.setenv("FSV_UPLOAD_CHUNKS", chunks)
+        else:
+            monkeypatch.delenv("FSV_UPLOAD_CHUNKS", raising=False)
+        for c in load_suite()[::4]:
+            g = fb.build_csr(c.n, c.edges)
+            labels, iters, gfc, fc, ms, snaps = solve(solver, g, True, -1)
+            assert iters == c.iterations and gfc.tolist() == c.gf_changed, (width, c.name)
+            assert np.array_equal(snaps, c.snapshots), (width, c.name)
+        for _ in range(20):
+            n, pairs = random_multigraph(rng, max_n=300, density=1.5)
+            check_against_oracle(solver, n, pairs, hub_slots=-1)
+        n, e = gen.forest(400, 1, 64, 2, seed=int(rng.integers(1 << 30)))
+        check_against_oracle(solver, n, e, hub_slots=-1)
+    monkeypatch.delenv("FSV_TILE_W")
+    monkeypatch.delenv("FSV_UPLOAD_CHUNKS", raising=False)
+    solver.set_hub_slots(0)
