@@ -740,7 +740,7 @@ __global__ void k_piece_compact(const int4* __restrict__ pieces, const unsigned 
 // entries per row (cnt = k + 1 with the header, nzflag); true writes them.
 template <bool COMPACT>
 __global__ void k_tile_pass(const int64_t* __restrict__ off, long long col_base, long long row_begin,
-                            long long rows, const uint32_t* __restrict__ tmp, uint32_t tlo, uint32_t thi,
+                            long long rows, const uint32_t* __restrict__ tmp, uint32_t tlo, uint32_t thi, bool first,
                             long long* __restrict__ cnt, int* __restrict__ nzflag,
                             const long long* __restrict__ out_off, const int* __restrict__ nzidx,
                             uint32_t* __restrict__ ecol, int* __restrict__ nzrows, long long* __restrict__ nzoff) {
@@ -767,13 +767,19 @@ __global__ void k_tile_pass(const int64_t* __restrict__ off, long long col_base,
         ++o;
       }
     }
-    if (!has) hi = lo;
+    // rows over HUGE_ROW keep only hub-coded entries (their columns come
+    // earlier in the degree order): they belong to the first tile, counted
+    // by k_huge_rows and written by k_piece_compact
+    const bool huge = hi - lo > HUGE_ROW;
+    if (!has || huge) hi = lo;
     const bool is_long = hi - lo > FSV_LONG_ROW;
     long long k = 0;
     if (!is_long) {
       for (long long e = lo; e < hi; ++e) {
         const uint32_t c = tmp[e];
-        if (c >= tlo && c < thi) {   // (DROP is above every tile)
+        // hub-coded columns (gathered from shared memory / the L2 tier, not
+        // from G) all go to the first tile; DROP is in no tile
+        if ((c & HUB) ? (first && c != DROP) : (c >= tlo && c < thi)) {
           if (COMPACT) ecol[o++] = c;
           else ++k;
         }
@@ -790,7 +796,7 @@ __global__ void k_tile_pass(const int64_t* __restrict__ off, long long col_base,
       for (long long e0 = slo; e0 < shi; e0 += 32) {
         const long long e = e0 + lane;
         const uint32_t c = e < shi ? tmp[e] : DROP;
-        const bool keep = c >= tlo && c < thi;
+        const bool keep = (c & HUB) ? (first && c != DROP) : (c >= tlo && c < thi);
         const unsigned b = __ballot_sync(0xffffffffu, keep);
         if (COMPACT && keep) ecol[so + __popc(b & ((1u << lane) - 1u))] = c;
         so += __popc(b);
@@ -798,7 +804,7 @@ __global__ void k_tile_pass(const int64_t* __restrict__ off, long long col_base,
       }
       if (lane == src) k = sk;
     }
-    if (!COMPACT && r < rows) {
+    if (!COMPACT && r < rows && !(huge && first)) {   // (k_huge_rows counted a huge row's first tile)
       cnt[r] = k ? k + 1 : 0;
       nzflag[r] = k > 0;
     }
@@ -1236,7 +1242,6 @@ static int upload_impl(fsv_ctx* c, int64_t n, const int64_t* h_off_arr, const Co
     k_degree<<<grid_for(c, n, 256), 256, 0, st>>>(offp, n, deg.p, ids.p, d_bad.p + 1, row_begin, row_end,
                                                   c->ws.hrow.p, c->ws.pieces.p, huge_ctr, max_huge, max_pieces);
   int H = 0;
-  long long max_deg = 0;
   // a valid CSR row has fewer than n entries (deduplicated, no self-loop),
   // so the degree sort needs bit_length(n - 1) key bits (22 for RMAT-22:
   // three onesweep passes instead of four). A malformed row with more only
@@ -1272,7 +1277,6 @@ static int upload_impl(fsv_ctx* c, int64_t n, const int64_t* h_off_arr, const Co
     CUDA_TRY(cudaMemcpyAsync(&h_badoff, d_bad.p + 1, sizeof h_badoff, cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaStreamSynchronize(st));
     if (h_badoff != ~0ull) return fail(FSV_ERR_INPUT, "row_offsets must be non-decreasing");
-    max_deg = probe ? top[0] : 0;
     int cand = 0;
     while (cand < probe && top[cand] >= kHubMinDegree) ++cand;
     H = (c->hub_limit >= 0) ? std::min(cand, c->hub_limit) : 0;
@@ -1301,8 +1305,7 @@ static int upload_impl(fsv_ctx* c, int64_t n, const int64_t* h_off_arr, const Co
   long long tile_w = c->tile_width < 0 ? (8LL << 20) : c->tile_width;
   {
     if (const char* e = getenv("FSV_TILE_W")) tile_w = atoll(e);   // tests/dev: exact width in vertices
-    const bool no_huge = !n || max_deg <= HUGE_ROW;
-    if (!H && no_huge && tile_w > 0 && n > tile_w) T = (int)((n + tile_w - 1) / tile_w);
+    if (tile_w > 0 && n > tile_w) T = (int)((n + tile_w - 1) / tile_w);
   }
   c->tiles = T;
   c->H = H;
@@ -1389,8 +1392,8 @@ static int upload_impl(fsv_ctx* c, int64_t n, const int64_t* h_off_arr, const Co
     const uint32_t tlo = (uint32_t)(t * tile_w), thi = (uint32_t)std::min<long long>((t + 1) * tile_w, n);
     if (rows) {
       const int tg = grid_for(c, (rows + 31) / 32 * 32, 256, 16);
-      k_tile_pass<false><<<tg, 256, 0, st>>>(offp, e_begin, row_begin, rows, etmp.p, tlo, thi, cnt.p, nzflag.p,
-                                              nullptr, nullptr, nullptr, nullptr, nullptr);
+      k_tile_pass<false><<<tg, 256, 0, st>>>(offp, e_begin, row_begin, rows, etmp.p, tlo, thi, t == 0, cnt.p,
+                                              nzflag.p, nullptr, nullptr, nullptr, nullptr, nullptr);
       size_t b = c->ws.tmp.n;
       CUDA_TRY(cub::DeviceScan::ExclusiveScan(c->ws.tmp.p, b, cnt.p, out_off.p, cuda::std::plus<>{},
                                               cub::FutureValue<long long>(c->ws.carry_e.p + t), (int)rows, st));
@@ -1399,10 +1402,15 @@ static int upload_impl(fsv_ctx* c, int64_t n, const int64_t* h_off_arr, const Co
                                               cub::FutureValue<int>(c->ws.carry_r.p + t), (int)rows, st));
     }
     k_chunk_carry<<<1, 1, 0, st>>>(cnt.p, nzflag.p, out_off.p, nzidx.p, 0, rows, c->ws.carry_e.p, c->ws.carry_r.p, t);
-    if (rows)
+    if (rows) {
       k_tile_pass<true><<<grid_for(c, (rows + 31) / 32 * 32, 256, 16), 256, 0, st>>>(
-          offp, e_begin, row_begin, rows, etmp.p, tlo, thi, nullptr, nullptr, out_off.p, nzidx.p, c->ecolp,
+          offp, e_begin, row_begin, rows, etmp.p, tlo, thi, t == 0, nullptr, nullptr, out_off.p, nzidx.p, c->ecolp,
           nzrows.p, nzoff.p);
+      if (t == 0)
+        k_piece_compact<<<c->sm_count * 16, 256, 0, st>>>(c->ws.pieces.p, huge_ctr + 1, row_begin, row_end, offp,
+                                                          e_begin, etmp.p, c->ws.hrow.p, out_off.p,
+                                                          c->ws.piece_kept.p, c->ecolp);
+    }
   }
   const int KT = T > 1 ? T : K;   // carry slots used
   umark(3);

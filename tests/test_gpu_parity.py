@@ -568,6 +568,19 @@ def test_column_tiled_layout_matches_golden(solver, monkeypatch):
             check_against_oracle(solver, n, pairs, hub_slots=-1)
         n, e = gen.forest(400, 1, 64, 2, seed=int(rng.integers(1 << 30)))
         check_against_oracle(solver, n, e, hub_slots=-1)
+        # with a hub table (hub-coded columns go to the first tile) and rows
+        # long enough for the huge-row pieces
+        for _ in range(4):
+            n = int(rng.integers(2000, 6000))
+            k = int(rng.integers(4 * n, 20 * n))
+            u = (rng.pareto(1.1, k) * 2).astype(np.int64) % n
+            v = rng.integers(0, n, k)
+            check_against_oracle(solver, n, np.stack([u, v], 1).astype(np.int32), hub_slots=256)
+        n, e = gen.rmat(14, 16, seed=int(rng.integers(1 << 30)))
+        check_against_oracle(solver, n, e, hub_slots=0)
+        monkeypatch.setenv("FSV_TIER_MIN_N", "0")   # and the L2 rank tier
+        check_against_oracle(solver, n, e, hub_slots=0)
+        monkeypatch.delenv("FSV_TIER_MIN_N")
     monkeypatch.delenv("FSV_TILE_W")
     monkeypatch.delenv("FSV_UPLOAD_CHUNKS", raising=False)
     solver.set_hub_slots(0)
