@@ -135,6 +135,9 @@ struct DBuf {
     n = 0;
     cap = 0;
   }
+  DBuf() = default;
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
   ~DBuf() { free(); }
 };
 
@@ -198,7 +201,12 @@ struct fsv_ctx {
     DBuf<int> carry_r;
     DBuf<unsigned char> tmp;
     DBuf<int64_t> cols64;
-    DBuf<uint32_t> etmp;
+    DBuf<uint32_t> etmp, etmp2;
+    // column-range tiling: runs per row, their bases, sort keys/ids, lengths,
+    // rows, sources, segment sizes/offsets
+    DBuf<int> t_runs, t_ids, t_len, t_row;
+    DBuf<long long> t_base, t_src, t_seg;
+    DBuf<uint32_t> t_key;
     DBuf<int4> pieces;
     DBuf<long long> hrow;
     DBuf<unsigned long long> hkept;
@@ -729,84 +737,93 @@ __global__ void k_piece_compact(const int4* __restrict__ pieces, const unsigned 
   }
 }
 
-// Column-range tiling (layouts without a hub table and without huge rows,
-// whose vertex vectors overflow L2: configs 3 and 4). Tile t keeps, for
-// every row, the row's kept entries whose column lies in [tlo, thi), behind
-// their own header; the layout is tile 0's rows, then tile 1's, ... So the
-// whole GPU, sweeping the layout in order, gathers gf from one tile-sized
-// slice of G (and reduces into the same slice of N) at a time, which stays
-// L2-resident. A row split over tiles emits one partial row minimum per
-// tile (min-reductions are idempotent). COMPACT = false counts a tile's
-// entries per row (cnt = k + 1 with the header, nzflag); true writes them.
-template <bool COMPACT>
-__global__ void k_tile_pass(const int64_t* __restrict__ off, long long col_base, long long row_begin,
-                            long long rows, const uint32_t* __restrict__ tmp, uint32_t tlo, uint32_t thi, bool first,
-                            long long* __restrict__ cnt, int* __restrict__ nzflag,
-                            const long long* __restrict__ out_off, const int* __restrict__ nzidx,
-                            uint32_t* __restrict__ ecol, int* __restrict__ nzrows, long long* __restrict__ nzoff) {
+// Column-range tiling of a built layout (fsv_set_tile_width). Every row
+// segment (header + kept codes, ecol) is cut into runs of consecutive codes
+// in the same column tile (hub-coded columns, gathered from shared memory or
+// the L2 tier rather than from G, count as tile 0); the runs are stably
+// sorted by tile and written back, each behind its own copy of the row's
+// header: all rows' tile-0 runs, then tile 1's, ... The dense sweep then
+// gathers gf from, and reduces into, one W-vertex slice of the vertex
+// vectors at a time, which stays L2-resident. A row split over runs emits
+// one partial row minimum per run (min-reductions are idempotent).
+__device__ __forceinline__ uint32_t code_tile(uint32_t c, long long w) {
+  return (c & HUB) ? 0u : (uint32_t)((long long)c / w);
+}
+
+// Runs per row segment i = [nzoff[i] + 1, nzoff[i + 1]) (the last ends at E).
+template <bool EMIT>
+__global__ void k_tile_runs(const uint32_t* __restrict__ ecol, const long long* __restrict__ nzoff,
+                            const int* __restrict__ nzrows, long long R, long long E, long long w,
+                            int* __restrict__ runs, const long long* __restrict__ run_base,
+                            uint32_t* __restrict__ key, long long* __restrict__ src, int* __restrict__ len,
+                            int* __restrict__ row) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < R; i += (long long)gridDim.x * blockDim.x) {
+    const long long lo = nzoff[i] + 1, hi = (i + 1 < R) ? nzoff[i + 1] : E;
+    long long k = EMIT ? run_base[i] : 0;
+    int cnt = 0;
+    uint32_t cur = 0xffffffffu;
+    long long start = lo;
+    for (long long e = lo; e < hi; ++e) {
+      const uint32_t t = code_tile(ecol[e], w);
+      if (t != cur) {
+        if (EMIT && cnt) { key[k] = cur; src[k] = start; len[k] = (int)(e - start); row[k] = nzrows[i]; ++k; }
+        cur = t;
+        start = e;
+        ++cnt;
+      }
+    }
+    if (EMIT) {
+      if (cnt) { key[k] = cur; src[k] = start; len[k] = (int)(hi - start); row[k] = nzrows[i]; }
+    } else {
+      runs[i] = cnt;
+    }
+  }
+}
+
+__global__ void k_iota(int* __restrict__ a, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    a[i] = (int)i;
+}
+
+__global__ void k_tile_lens(const int* __restrict__ ids, const int* __restrict__ len, long long M,
+                            long long* __restrict__ seg) {
+  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < M; k += (long long)gridDim.x * blockDim.x)
+    seg[k] = len[ids[k]] + 1;
+}
+
+// Sorted run k: header at out[k], its codes behind it; the span table's
+// segment arrays (nzrows, nzoff) follow the new order. A thread per run
+// (runs are short: at most a row), its dependent loads independent of the
+// other threads'; runs over 32 codes are copied by the whole warp.
+__global__ void k_tile_scatter(const uint32_t* __restrict__ ecol, const int* __restrict__ ids,
+                               const long long* __restrict__ src, const int* __restrict__ len,
+                               const int* __restrict__ row, const long long* __restrict__ out, long long M,
+                               uint32_t* __restrict__ ecol2, int* __restrict__ nzrows, long long* __restrict__ nzoff) {
   const int lane = threadIdx.x & 31;
-  const long long nw = (long long)gridDim.x * (blockDim.x >> 5);
-  for (long long w0 = ((long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32; w0 < rows;
-       w0 += nw * 32) {
-    const long long r = w0 + lane;
-    long long lo = 0, hi = 0, o = 0;
-    bool has = true;
-    if (r < rows) {
-      const long long u = row_begin + r;
-      lo = off[u] - col_base;
-      hi = off[u + 1] - col_base;
-      if (COMPACT) {
-        o = out_off[r];
-        has = out_off[r + 1] > o;
-        if (has) {
-          ecol[o] = HDR | (uint32_t)u;
-          const int z = nzidx[r];
-          nzrows[z] = (int)u;
-          nzoff[z] = o;
-        }
-        ++o;
-      }
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long base = (long long)blockIdx.x * blockDim.x; base < M; base += stride) {   // block-uniform
+    const long long k = base + threadIdx.x;
+    long long o = 0, s0 = 0;
+    int l = 0;
+    if (k < M) {
+      const int id = ids[k];
+      o = out[k];
+      s0 = src[id];
+      l = len[id];
+      const int u = row[id];
+      ecol2[o] = HDR | (uint32_t)u;
+      nzrows[k] = u;
+      nzoff[k] = o;
+      if (l <= 32)
+        for (int j = 0; j < l; ++j) ecol2[o + 1 + j] = ecol[s0 + j];
     }
-    // rows over HUGE_ROW keep only hub-coded entries (their columns come
-    // earlier in the degree order): they belong to the first tile, counted
-    // by k_huge_rows and written by k_piece_compact
-    const bool huge = hi - lo > HUGE_ROW;
-    if (!has || huge) hi = lo;
-    const bool is_long = hi - lo > FSV_LONG_ROW;
-    long long k = 0;
-    if (!is_long) {
-      for (long long e = lo; e < hi; ++e) {
-        const uint32_t c = tmp[e];
-        // hub-coded columns (gathered from shared memory / the L2 tier, not
-        // from G) all go to the first tile; DROP is in no tile
-        if ((c & HUB) ? (first && c != DROP) : (c >= tlo && c < thi)) {
-          if (COMPACT) ecol[o++] = c;
-          else ++k;
-        }
-      }
-    }
-    unsigned lm = __ballot_sync(0xffffffffu, is_long);
+    unsigned lm = __ballot_sync(0xffffffffu, l > 32);
     while (lm) {
-      const int src = __ffs(lm) - 1;
+      const int q = __ffs(lm) - 1;
       lm &= lm - 1;
-      const long long slo = __shfl_sync(0xffffffffu, lo, src);
-      const long long shi = __shfl_sync(0xffffffffu, hi, src);
-      long long so = __shfl_sync(0xffffffffu, o, src);
-      long long sk = 0;
-      for (long long e0 = slo; e0 < shi; e0 += 32) {
-        const long long e = e0 + lane;
-        const uint32_t c = e < shi ? tmp[e] : DROP;
-        const bool keep = (c & HUB) ? (first && c != DROP) : (c >= tlo && c < thi);
-        const unsigned b = __ballot_sync(0xffffffffu, keep);
-        if (COMPACT && keep) ecol[so + __popc(b & ((1u << lane) - 1u))] = c;
-        so += __popc(b);
-        sk += __popc(b);
-      }
-      if (lane == src) k = sk;
-    }
-    if (!COMPACT && r < rows && !(huge && first)) {   // (k_huge_rows counted a huge row's first tile)
-      cnt[r] = k ? k + 1 : 0;
-      nzflag[r] = k > 0;
+      const long long qo = __shfl_sync(0xffffffffu, o, q), qs = __shfl_sync(0xffffffffu, s0, q);
+      const int ql = __shfl_sync(0xffffffffu, l, q);
+      for (int j = lane; j < ql; j += 32) ecol2[qo + 1 + j] = ecol[qs + j];
     }
   }
 }
@@ -1330,16 +1347,16 @@ static int upload_impl(fsv_ctx* c, int64_t n, const int64_t* h_off_arr, const Co
   CUDA_TRY(cnt.alloc(rows + 1)); CUDA_TRY(out_off.alloc(rows + 1));
   CUDA_TRY(nzflag.alloc(rows + 1)); CUDA_TRY(nzidx.alloc(rows + 1));
   CUDA_TRY(etmp.alloc((size_t)std::max<int64_t>(mloc, 1)));
-  CUDA_TRY(nzrows.alloc((size_t)rows * T + 1));
-  CUDA_TRY(nzoff.alloc((size_t)rows * T + 1));
+  CUDA_TRY(nzrows.alloc((size_t)rows + 1));
+  CUDA_TRY(nzoff.alloc((size_t)rows + 1));
   {
     long long epad = 0;   // dev: FSV_EPAD shifts the layout (placement sensitivity checks)
     if (const char* e = getenv("FSV_EPAD")) epad = atoll(e);
-    CUDA_TRY(c->ecol.alloc((size_t)(mloc + rows * T + SPAN + epad)));
+    CUDA_TRY(c->ecol.alloc((size_t)(mloc + rows + SPAN + epad)));
     c->ecolp = c->ecol.p + epad;
   }
-  CUDA_TRY(c->ws.carry_e.alloc((size_t)std::max(K, T) + 1));
-  CUDA_TRY(c->ws.carry_r.alloc((size_t)std::max(K, T) + 1));
+  CUDA_TRY(c->ws.carry_e.alloc((size_t)K + 1));
+  CUDA_TRY(c->ws.carry_r.alloc((size_t)K + 1));
   CUDA_TRY(cudaMemsetAsync(c->ws.carry_e.p, 0, sizeof(long long), st));
   CUDA_TRY(cudaMemsetAsync(c->ws.carry_r.p, 0, sizeof(int), st));
   umark(2);
@@ -1363,7 +1380,6 @@ static int upload_impl(fsv_ctx* c, int64_t n, const int64_t* h_off_arr, const Co
       k_huge_rows<<<c->sm_count * 2, 256, 0, st>>>(c->ws.hrow.p, huge_ctr, r0, r1, c->ws.hkept.p, cnt.p,
                                                   nzflag.p);
     }
-    if (T > 1) continue;   // tiled: compacted tile by tile over all rows after the last chunk
     if (nr) {
       size_t b = c->ws.tmp.n;
       CUDA_TRY(cub::DeviceScan::ExclusiveScan(c->ws.tmp.p, b, cnt.p + r0, out_off.p + r0, cuda::std::plus<>{},
@@ -1386,33 +1402,7 @@ static int upload_impl(fsv_ctx* c, int64_t n, const int64_t* h_off_arr, const Co
       dbg_enc_ev.push_back(e);
     }
   }
-  // tiled layout: tile-major over ALL rows (a per-chunk tile order would
-  // revisit every tile slice once per chunk and lose the locality)
-  for (int t = 0; t < T && T > 1; ++t) {
-    const uint32_t tlo = (uint32_t)(t * tile_w), thi = (uint32_t)std::min<long long>((t + 1) * tile_w, n);
-    if (rows) {
-      const int tg = grid_for(c, (rows + 31) / 32 * 32, 256, 16);
-      k_tile_pass<false><<<tg, 256, 0, st>>>(offp, e_begin, row_begin, rows, etmp.p, tlo, thi, t == 0, cnt.p,
-                                              nzflag.p, nullptr, nullptr, nullptr, nullptr, nullptr);
-      size_t b = c->ws.tmp.n;
-      CUDA_TRY(cub::DeviceScan::ExclusiveScan(c->ws.tmp.p, b, cnt.p, out_off.p, cuda::std::plus<>{},
-                                              cub::FutureValue<long long>(c->ws.carry_e.p + t), (int)rows, st));
-      b = c->ws.tmp.n;
-      CUDA_TRY(cub::DeviceScan::ExclusiveScan(c->ws.tmp.p, b, nzflag.p, nzidx.p, cuda::std::plus<>{},
-                                              cub::FutureValue<int>(c->ws.carry_r.p + t), (int)rows, st));
-    }
-    k_chunk_carry<<<1, 1, 0, st>>>(cnt.p, nzflag.p, out_off.p, nzidx.p, 0, rows, c->ws.carry_e.p, c->ws.carry_r.p, t);
-    if (rows) {
-      k_tile_pass<true><<<grid_for(c, (rows + 31) / 32 * 32, 256, 16), 256, 0, st>>>(
-          offp, e_begin, row_begin, rows, etmp.p, tlo, thi, t == 0, nullptr, nullptr, out_off.p, nzidx.p, c->ecolp,
-          nzrows.p, nzoff.p);
-      if (t == 0)
-        k_piece_compact<<<c->sm_count * 16, 256, 0, st>>>(c->ws.pieces.p, huge_ctr + 1, row_begin, row_end, offp,
-                                                          e_begin, etmp.p, c->ws.hrow.p, out_off.p,
-                                                          c->ws.piece_kept.p, c->ecolp);
-    }
-  }
-  const int KT = T > 1 ? T : K;   // carry slots used
+  const int KT = K;   // carry slots used
   umark(3);
   long long E = 0;
   int R = 0;
@@ -1444,6 +1434,71 @@ static int upload_impl(fsv_ctx* c, int64_t n, const int64_t* h_off_arr, const Co
       v = (long long)cv;
     }
     return fail(FSV_ERR_INPUT, "edge (%lld, %lld) out of range for n=%lld", u, v, (long long)n);
+  }
+  if (T > 1 && R > 0) {
+    // tiled layout from the built one (k_tile_runs, stable sort by tile,
+    // k_tile_scatter); grow-only workspaces (stream-ordered allocations of
+    // this size are returned to the driver at every synchronisation)
+    auto& tws = c->ws;
+    CUDA_TRY(tws.t_runs.alloc((size_t)R));
+    CUDA_TRY(tws.t_base.alloc((size_t)R + 1));
+    int* runs = tws.t_runs.p;
+    long long* run_base = tws.t_base.p;
+    const int rg = grid_for(c, R, 256, 16);
+    k_tile_runs<false><<<rg, 256, 0, st>>>(c->ecolp, nzoff.p, nzrows.p, R, E, tile_w, runs, nullptr, nullptr,
+                                           nullptr, nullptr, nullptr);
+    size_t sb = 0;
+    cub::DeviceScan::ExclusiveScan(nullptr, sb, runs, run_base, cuda::std::plus<>{}, 0LL, (int)R, st);
+    CUDA_TRY(tws.tmp.alloc(std::max(sb, tws.tmp.n)));
+    sb = tws.tmp.n;
+    CUDA_TRY(cub::DeviceScan::ExclusiveScan(tws.tmp.p, sb, runs, run_base, cuda::std::plus<>{}, 0LL, (int)R, st));
+    long long M = 0;
+    int last_runs = 0;
+    CUDA_TRY(cudaMemcpyAsync(&M, run_base + R - 1, sizeof M, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaMemcpyAsync(&last_runs, runs + R - 1, sizeof last_runs, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    M += last_runs;
+    CUDA_TRY(tws.t_key.alloc((size_t)M * 2));
+    CUDA_TRY(tws.t_ids.alloc((size_t)M * 2));
+    CUDA_TRY(tws.t_len.alloc((size_t)M));
+    CUDA_TRY(tws.t_row.alloc((size_t)M));
+    CUDA_TRY(tws.t_src.alloc((size_t)M));
+    CUDA_TRY(tws.t_seg.alloc((size_t)M * 2));
+    uint32_t *key = tws.t_key.p, *key2 = tws.t_key.p + M;
+    int *ids = tws.t_ids.p, *ids2 = tws.t_ids.p + M, *len = tws.t_len.p, *row = tws.t_row.p;
+    long long *src = tws.t_src.p, *seg = tws.t_seg.p, *out = tws.t_seg.p + M;
+    k_tile_runs<true><<<rg, 256, 0, st>>>(c->ecolp, nzoff.p, nzrows.p, R, E, tile_w, nullptr, run_base, key, src,
+                                          len, row);
+    k_iota<<<grid_for(c, M, 256), 256, 0, st>>>(ids, M);
+    int kbits = 1;
+    while ((1LL << kbits) < T) ++kbits;
+    sb = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, sb, key, key2, ids, ids2, (int)M, 0, kbits, st);
+    size_t sb2 = 0;
+    cub::DeviceScan::ExclusiveScan(nullptr, sb2, seg, out, cuda::std::plus<>{}, 0LL, (int)M, st);
+    CUDA_TRY(cudaStreamSynchronize(st));   // (the workspace may grow)
+    CUDA_TRY(tws.tmp.alloc(std::max(std::max(sb, sb2), tws.tmp.n)));
+    sb = tws.tmp.n;
+    CUDA_TRY(cub::DeviceRadixSort::SortPairs(tws.tmp.p, sb, key, key2, ids, ids2, (int)M, 0, kbits, st));
+    k_tile_lens<<<grid_for(c, M, 256), 256, 0, st>>>(ids2, len, M, seg);
+    sb = tws.tmp.n;
+    CUDA_TRY(cub::DeviceScan::ExclusiveScan(tws.tmp.p, sb, seg, out, cuda::std::plus<>{}, 0LL, (int)M, st));
+    const long long E2 = E + (M - R);
+    long long epad = 0;
+    if (const char* e = getenv("FSV_EPAD")) epad = atoll(e);
+    CUDA_TRY(cudaStreamSynchronize(st));   // the run lists are read: the segment arrays may grow now
+    CUDA_TRY(tws.etmp2.alloc((size_t)(E2 + SPAN + epad)));   // the tiled layout, swapped in below
+    CUDA_TRY(nzrows.alloc((size_t)M + 1));
+    CUDA_TRY(nzoff.alloc((size_t)M + 1));
+    k_tile_scatter<<<grid_for(c, M, 256, 16), 256, 0, st>>>(c->ecolp, ids2, src, len, row, out, M,
+                                                                tws.etmp2.p + epad, nzrows.p, nzoff.p);
+    CUDA_TRY(cudaGetLastError());
+    std::swap(c->ecol.p, tws.etmp2.p);   // (DBuf owns its pointer: swap the members, never copy)
+    std::swap(c->ecol.n, tws.etmp2.n);
+    std::swap(c->ecol.cap, tws.etmp2.cap);
+    c->ecolp = c->ecol.p + epad;
+    E = E2;
+    R = (int)M;
   }
   const long long Epad = (E + SPAN - 1) / SPAN * SPAN;
   umark(4);
@@ -1817,7 +1872,7 @@ struct MergeArgs {
 };
 
 __global__ void k_group_min_merge(MergeArgs a) {
-  if (a.done && *(volatile const int*)a.done) return;
+  if (a.done && __ldcg(a.done)) return;
   const long long stride = (long long)gridDim.x * blockDim.x;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < a.n; i += stride) {
     int v = a.buf[0][i];

@@ -221,12 +221,12 @@ __device__ __forceinline__ unsigned long long global_ns() {
 }
 
 __device__ __forceinline__ int loop_iter(const LoopCtl& lc, int iter) {
-  return lc.graph == 1 ? *(volatile const int*)lc.iterp : iter;
+  return lc.graph == 1 ? __ldcg(lc.iterp) : iter;   // written by the previous kernel
 }
 
 // Early exit after convergence: in graph mode the loop condition must drop.
 __device__ __forceinline__ bool converged_exit(const int* done, const LoopCtl& lc) {
-  if (*(volatile const int*)done) {
+  if (__ldcg(done)) {
     if (lc.graph == 1 && blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(lc.cond, 0u);
     return true;
   }
@@ -575,7 +575,7 @@ __device__ __forceinline__ void push_local(const PushArgs& a, long long* w_start
 // Phase B: one warp per long-row chunk, contiguous columns.
 __device__ __forceinline__ void push_big(const PushArgs& a) {
   const int lane = threadIdx.x & 31;
-  const unsigned long long total = *(volatile unsigned long long*)a.nchunks;
+  const unsigned long long total = __ldcg(a.nchunks);   // written before the grid barrier (L2)
   const long long nw = (long long)gridDim.x * (blockDim.x >> 5);
   constexpr int PER = PUSH_BCHUNK / 32;
   for (long long q = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -634,7 +634,7 @@ __device__ __forceinline__ int gather_gf_tier(uint32_t c, uint32_t s_base, const
 template <bool HUBS, bool TIER, int NSTEP>
 __global__ void __launch_bounds__(HOOK_THREADS, 1) k_hook(HookArgs a) {
   extern __shared__ int s_hub[];
-  if (*(volatile const int*)a.done) return;
+  if (__ldcg(a.done)) return;
   if (a.lc.graph == 1) {
     const int it = loop_iter(a.lc, a.iter);
     unsigned long long* slot = a.lc.cnt_base + (size_t)(it - 1) * NCOUNT;
@@ -964,9 +964,9 @@ __global__ void k_hubfix(int* __restrict__ hub_acc, const int* __restrict__ hub_
                          const int* __restrict__ G_hub, int H, const int* __restrict__ F,
                          const int* __restrict__ G, int* __restrict__ N, const int* done, const int* mode,
                          int iter, const int* iterp, int* X, int* Y) {
-  if (*(volatile const int*)done) return;
+  if (__ldcg(done)) return;
   if (iterp) {   // graph mode: iteration and buffers from the device (loop_bufs)
-    iter = *(volatile const int*)iterp;
+    iter = __ldcg(iterp);
     F = (iter & 1) ? X : Y;
     N = (iter & 1) ? Y : X;
   }
