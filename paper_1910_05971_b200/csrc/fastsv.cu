@@ -2475,14 +2475,19 @@ static int solve_body(fsv_ctx* const* cs, int count, const fsv_config* cfg, int3
     cs[r]->labels_src = cs[r]->G;
   }
 #ifdef FSV_CHECKS
-  if (count == 1) {  // checked build: the buffers the solve kernels may load from / reduce into
+  {  // checked build: the buffers the solve kernels may load from / reduce into (every rank's)
     ChkRanges r{};
-    auto add_ld = [&](const int* p, size_t len) { if (p && r.nl < 12) { r.lo[r.nl] = p; r.hi[r.nl++] = p + len; } };
-    auto add_red = [&](const int* p, size_t len) { if (p && r.nr < 4) { r.rlo[r.nr] = p; r.rhi[r.nr++] = p + len; } };
-    add_red(c->xb.p, c->xb.n); add_red(c->f1.p, c->f1.n); add_red(c->hacc, (size_t)acc_len(c->HT));
-    add_ld(c->xb.p, c->xb.n); add_ld(c->f1.p, c->f1.n); add_ld(c->gb.p, c->gb.n);
-    add_ld(c->G_hub.p, c->G_hub.n); add_ld(c->hub_id.p, c->hub_id.n); add_ld(c->colsp, (size_t)c->csr_local);
-    add_ld(c->span_row.p, c->span_row.n);
+    auto add_ld = [&](const int* p, size_t len) { if (p && r.nl < kChkLd) { r.lo[r.nl] = p; r.hi[r.nl++] = p + len; } };
+    auto add_red = [&](const int* p, size_t len) {
+      if (p && r.nr < kChkRed) { r.rlo[r.nr] = p; r.rhi[r.nr++] = p + len; }
+    };
+    for (int q = 0; q < count; ++q) {
+      const fsv_ctx* x = cs[q];
+      add_red(x->xb.p, x->xb.n); add_red(x->f1.p, x->f1.n); add_red(x->hacc, (size_t)acc_len(x->HT));
+      add_ld(x->xb.p, x->xb.n); add_ld(x->f1.p, x->f1.n); add_ld(x->gb.p, x->gb.n);
+      add_ld(x->G_hub.p, x->G_hub.n); add_ld(x->hub_id.p, x->hub_id.n); add_ld(x->colsp, (size_t)x->csr_local);
+      add_ld(x->span_row.p, x->span_row.n);
+    }
     CUDA_TRY(cudaMemcpyToSymbolAsync(g_chk, &r, sizeof r, 0, cudaMemcpyHostToDevice, st));
   }
 #endif

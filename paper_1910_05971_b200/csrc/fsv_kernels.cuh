@@ -111,12 +111,13 @@ __device__ __forceinline__ uint4 ld_stream(const uint4* p, uint64_t pol) {
 // and every min-reduction of the FastSV solve kernels must hit one of the
 // buffers the host registered for this solve, else the kernel traps. Ranges
 // are empty (checks off) outside fastsv solves.
+constexpr int kChkRed = 32, kChkLd = 96;   // room for an emulated rank group of 8 contexts
 struct ChkRanges {
-  const int* rlo[4];
-  const int* rhi[4];
+  const int* rlo[kChkRed];
+  const int* rhi[kChkRed];
   int nr;
-  const int* lo[12];
-  const int* hi[12];
+  const int* lo[kChkLd];
+  const int* hi[kChkLd];
   int nl;
 };
 __device__ ChkRanges g_chk;

@@ -454,7 +454,8 @@ def test_bounds_checked_build_runs_clean():
     r = subprocess.run([sys.executable, str(root / "tools" / "sanitize_run.py")], env=env,
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
-    assert "mismatches: 0" in r.stdout, r.stdout[-2000:]
+    assert "(single context) done, mismatches: 0" in r.stdout, r.stdout[-2000:]
+    assert "groups) done, mismatches: 0" in r.stdout, r.stdout[-2000:]
 
 
 def test_graph_reuse_across_uploads_of_the_same_shape(solver):

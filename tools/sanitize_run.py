@@ -30,4 +30,45 @@ for policy in (0, 1, 2):
 lo, hi = 0, n // 2
 s.upload(g, lo, hi, g.col_indices[g.row_offsets[lo]:g.row_offsets[hi]])
 s.run()
-print("sanitize run done, mismatches:", bad)
+print("sanitize run (single context) done, mismatches:", bad)
+# device-CSR upload (borrowed arrays), tiled layouts, emulated rank groups
+# with the delta exchange, and the device Labeling, all under the checks
+import os
+import torch
+from paper_1910_05971_b200.driver import group_run
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+import bench
+n, e = gen.rmat(13, 16, seed=5)
+g = fb.build_csr(n, e)
+ref_lab = None
+s.set_hub_slots(0)
+s.upload(g)
+ref_lab, ref_it = s.run()[:2]
+d_off = torch.from_numpy(np.ascontiguousarray(g.row_offsets).copy()).cuda()
+d_cols = torch.from_numpy(np.ascontiguousarray(g.col_indices).copy()).cuda()
+s.upload_device(n, d_off.data_ptr(), d_cols.data_ptr())
+lab, it = s.run()[:2]
+bad += (it != ref_it) or not np.array_equal(lab, ref_lab)
+lbl = s.labeling()
+bad += not np.array_equal(lbl.labels, ref_lab.astype(np.int64))
+for w in ("97", "1000"):
+    os.environ["FSV_TILE_W"] = w
+    for hubs in (-1, 0):
+        s.set_hub_slots(hubs)
+        s.upload(g)
+        lab, it = s.run()[:2]
+        bad += (it != ref_it) or not np.array_equal(lab, ref_lab)
+del os.environ["FSV_TILE_W"]
+for ranks in (2, 3):
+    solvers = []
+    for r in range(ranks):
+        lo, hi = bench.row_partition(g.row_offsets, ranks, r)
+        x = fb.Solver(0)
+        x.upload(g, lo, hi, g.col_indices[g.row_offsets[lo]:g.row_offsets[hi]])
+        solvers.append(x)
+    for policy in (0, 2):
+        lab, it = group_run(solvers, policy=policy)[:2]
+        bad += (it != ref_it) or not np.array_equal(lab, ref_lab)
+    for x in solvers:
+        x.close()
+print("sanitize run (device upload, tiles, groups) done, mismatches:", bad)
