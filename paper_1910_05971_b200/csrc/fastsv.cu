@@ -371,6 +371,9 @@ static int staged_d2h(fsv_ctx* c, void* dst, const void* src, size_t bytes, cuda
   auto issue = [&](size_t i) -> int {
     const size_t o = i * kStageBytes, b = std::min(kStageBytes, bytes - o);
     const int k = (int)(i % kStageBufs);
+    // a staged upload may still be reading this buffer on another stream
+    if (c->stage_used[k]) CUDA_TRY(cudaEventSynchronize(c->stage_ev[k]));
+    c->stage_used[k] = false;
     CUDA_TRY(cudaMemcpyAsync(c->stage_buf[k], (const char*)src + o, b, cudaMemcpyDeviceToHost, s));
     CUDA_TRY(cudaEventRecord(c->stage_ev[k], s));
     return FSV_OK;
