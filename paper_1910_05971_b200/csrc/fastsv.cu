@@ -178,12 +178,6 @@ struct fsv_ctx {
   int tiles = 1;               // column-range tiles of the layout (k_tile_pass)
   DBuf<uint32_t> ecol;
   uint32_t* ecolp = nullptr;   // layout start inside ecol
-  // lane-owned-rows copy of the layout for k_hook_sell (hub-table layouts)
-  bool sell = false;
-  int sell_mode = -1;          // fsv_set_sell / FSV_SELL: -1 auto, 0 off, 1 on whenever there is a hub table
-  int sell_ctas = 0, sell_wa = 0;   // CTAs planned for; stream-A warps per CTA
-  DBuf<uint2> sell_a, sell_b;
-  DBuf<long long> sell_abase, sell_bbase;
   DBuf<int> span_row, hub_id, f1;
   // full symmetric CSR of this rank's rows, for sparse (push) iterations
   DBuf<int64_t> csr_off;
@@ -213,10 +207,6 @@ struct fsv_ctx {
     DBuf<int> t_runs, t_ids, t_len, t_row;
     DBuf<long long> t_base, t_src, t_seg;
     DBuf<uint32_t> t_key;
-    // lane-owned-rows build: pieces per row segment, piece lists, slice plan
-    DBuf<int> s_cnt, s_seg, s_len, s_ids;
-    DBuf<long long> s_start, s_off;
-    DBuf<uint32_t> s_key;
     DBuf<int4> pieces;
     DBuf<long long> hrow;
     DBuf<unsigned long long> hkept;
@@ -227,8 +217,6 @@ struct fsv_ctx {
   // solve state
   DBuf<int> xb, gb, G_hub, hub_acc, done;   // xb and f1: parent buffers, gb: gf
   int* hacc = nullptr;   // hub accumulator start inside hub_acc
-  int acc_reps = 1;      // copies of its first ACC_REP_SLOTS slots (HookArgs::acc_reps)
-  long long acc_rep_len = 0, acc_total = 0;   // ints per copy, ints of all copies
   int* X = nullptr;
   int* Y = nullptr;
   int* G = nullptr;
@@ -444,8 +432,7 @@ extern "C" int fsv_create(int device, fsv_ctx** out) {
   const int hook_smem = std::max((kHubMax + HOT_ACC) * (int)sizeof(int), PUSH_SCRATCH_BYTES);
   cudaError_t e = cudaSuccess;
   for (const void* fn : {(const void*)k_hook<true, false, STEPS>, (const void*)k_hook<true, true, STEPS>,
-                         (const void*)k_hook<true, false, 1>, (const void*)k_hook<true, true, 1>,
-                         (const void*)k_hook_sell<false>, (const void*)k_hook_sell<true>})
+                         (const void*)k_hook<true, false, 1>, (const void*)k_hook<true, true, 1>})
     if (e == cudaSuccess) e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, hook_smem);
   if (e != cudaSuccess) {
     delete c;
@@ -844,138 +831,6 @@ __global__ void k_tile_scatter(const uint32_t* __restrict__ ecol, const int* __r
   }
 }
 
-// ---- lane-owned rows (k_hook_sell) from the built layout ---------------------
-// Row segment i = header at nzoff[i], codes in (nzoff[i], nzoff[i+1]) (k_pad
-// sets nzoff[R] = E). A code belongs to stream A when it is a shared-memory
-// hub slot (HUB, slot < H), else to stream B.
-__device__ __forceinline__ bool sell_is_a(uint32_t c, int H) { return (c & HUB) && (int)(c & IDMASK) < H; }
-
-// pieces per segment: na[i], nb[i] (entry R of each array = 0 for the scan)
-__global__ void k_sell_count(const uint32_t* __restrict__ ecol, const long long* __restrict__ nzoff, long long R,
-                             int H, int* __restrict__ na, int* __restrict__ nb) {
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i <= R; i += (long long)gridDim.x * blockDim.x) {
-    int ca = 0, cb = 0;
-    if (i < R) {
-      const long long lo = nzoff[i] + 1, hi = nzoff[i + 1];
-      for (long long e = lo; e < hi; ++e) {
-        if (sell_is_a(ecol[e], H)) ++ca; else ++cb;
-      }
-    }
-    na[i] = (ca + SELL_CAP_A - 1) / SELL_CAP_A;
-    nb[i] = (cb + SELL_CAP_B - 1) / SELL_CAP_B;
-  }
-}
-
-// piece lists: segment, first entry (layout index) and entry count of every
-// piece; sort key = data blocks of the piece
-__global__ void k_sell_pieces(const uint32_t* __restrict__ ecol, const long long* __restrict__ nzoff, long long R,
-                              int H, const int* __restrict__ pa, const int* __restrict__ pb,
-                              int* __restrict__ a_seg, long long* __restrict__ a_start, int* __restrict__ a_len,
-                              uint32_t* __restrict__ a_key, int* __restrict__ a_ids,
-                              int* __restrict__ b_seg, long long* __restrict__ b_start, int* __restrict__ b_len,
-                              uint32_t* __restrict__ b_key, int* __restrict__ b_ids) {
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < R; i += (long long)gridDim.x * blockDim.x) {
-    const long long lo = nzoff[i] + 1, hi = nzoff[i + 1];
-    int ka = pa[i], kb = pb[i], ca = 0, cb = 0;
-    for (long long e = lo; e < hi; ++e) {
-      if (sell_is_a(ecol[e], H)) {
-        if (ca == 0) { a_seg[ka] = (int)i; a_start[ka] = e; }
-        if (++ca == SELL_CAP_A) { a_len[ka] = ca; a_key[ka] = SELL_CAP_A / 4; a_ids[ka] = ka; ++ka; ca = 0; }
-      } else {
-        if (cb == 0) { b_seg[kb] = (int)i; b_start[kb] = e; }
-        if (++cb == SELL_CAP_B) { b_len[kb] = cb; b_key[kb] = SELL_CAP_B / 2; b_ids[kb] = kb; ++kb; cb = 0; }
-      }
-    }
-    if (ca) { a_len[ka] = ca; a_key[ka] = (uint32_t)(ca + 3) / 4; a_ids[ka] = ka; }
-    if (cb) { b_len[kb] = cb; b_key[kb] = (uint32_t)(cb + 1) / 2; b_ids[kb] = kb; }
-  }
-}
-
-// Slices (32 length-sorted pieces) are dealt to the W hook warps in snake
-// order; thread w lays its slices end to end: off[s] = first block of slice s
-// inside warp w's run, wblocks[w] = the run's blocks rounded up to groups.
-__global__ void k_sell_plan(const uint32_t* __restrict__ key_sorted, long long P, int W,
-                            long long* __restrict__ off, long long* __restrict__ wblocks) {
-  const int w = blockIdx.x * blockDim.x + threadIdx.x;
-  if (w > W) return;
-  long long run = 0;
-  if (w < W) {
-    const long long nsl = (P + 31) / 32;
-    for (long long r = 0; r * W < nsl; ++r) {
-      const long long s = r * W + ((r & 1) ? W - 1 - w : w);
-      if (s >= nsl) continue;
-      off[s] = run;
-      run += 1 + (long long)key_sorted[s * 32];
-    }
-    run = (run + SELL_GROUP - 1) / SELL_GROUP * SELL_GROUP;
-  }
-  wblocks[w] = run;   // entry W = 0 for the scan
-}
-
-// One warp per slice: header block, then the data blocks; lane l copies the
-// matching codes of its piece (A: four 16-bit slots per word, B: two codes),
-// repeating its last code up to the slice length. Warps past the last slice
-// of each hook warp's run fill the run's padding with empty headers.
-template <bool A>
-__global__ void k_sell_scatter(const uint32_t* __restrict__ ecol, const long long* __restrict__ nzoff,
-                               const int* __restrict__ nzrows, int H, const int* __restrict__ seg,
-                               const long long* __restrict__ start, const int* __restrict__ len,
-                               const uint32_t* __restrict__ key_sorted, const int* __restrict__ ids_sorted,
-                               long long P, int W, const long long* __restrict__ off,
-                               const long long* __restrict__ wbase, uint2* __restrict__ out) {
-  const int lane = threadIdx.x & 31;
-  const long long nw = (long long)gridDim.x * (blockDim.x >> 5);
-  const long long nsl = (P + 31) / 32;
-  constexpr int PER = A ? 4 : 2;
-  for (long long s = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); s < nsl; s += nw) {
-    const long long r = s / W;
-    const int j = (int)(s % W);
-    const int w = (r & 1) ? W - 1 - j : j;
-    uint2* dst = out + (wbase[w] + off[s]) * 32 + lane;
-    const int L = (int)key_sorted[s * 32];
-    const int id = ids_sorted[min(s * 32 + lane, P - 1)];
-    const int sg = seg[id];
-    long long e = start[id];
-    int left = len[id];
-    dst[0] = make_uint2((uint32_t)nzrows[sg], (uint32_t)L);
-    uint32_t last = 0;
-    for (int b = 0; b < L; ++b) {
-      uint32_t c[PER];
-#pragma unroll
-      for (int k = 0; k < PER; ++k) {
-        if (left > 0) {
-          uint32_t x = ecol[e++];
-          while (sell_is_a(x, H) != A) x = ecol[e++];   // `left` more matching codes exist in the segment
-          last = A ? (x & IDMASK) : x;
-          --left;
-        }
-        c[k] = last;
-      }
-      dst[(b + 1) * 32] = A ? make_uint2(c[0] | (c[1 % PER] << 16), c[2 % PER] | (c[3 % PER] << 16))
-                            : make_uint2(c[0], c[1 % PER]);
-    }
-  }
-}
-
-// empty headers {dummy vertex n, 0 data blocks} in the padding of every run
-__global__ void k_sell_padfill(const uint32_t* __restrict__ key_sorted, long long P, int W,
-                               const long long* __restrict__ off, const long long* __restrict__ wbase, int n,
-                               uint2* __restrict__ out) {
-  const int lane = threadIdx.x & 31;
-  const long long nw = (long long)gridDim.x * (blockDim.x >> 5);
-  const long long nsl = (P + 31) / 32;
-  for (long long w = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); w < W; w += nw) {
-    // the run's last slice: the largest round r with a slice for this warp
-    long long used = 0;
-    const long long rounds = (nsl + W - 1) / W;
-    for (long long r = rounds - 1; r >= 0; --r) {
-      const long long s = r * W + ((r & 1) ? W - 1 - w : w);
-      if (s < nsl) { used = off[s] + 1 + (long long)key_sorted[s * 32]; break; }
-    }
-    for (long long b = wbase[w] + used; b < wbase[w + 1]; ++b) out[b * 32 + lane] = make_uint2((uint32_t)n, 0u);
-  }
-}
-
 // Orientation pass 2 (no gathers): header + kept entries of each row, in
 // order, at out_off[r]; nzrows/nzoff for the span table.
 __global__ void k_orient_compact(const int64_t* __restrict__ off, long long col_base, long long row_begin,
@@ -1227,93 +1082,6 @@ static int grid_for(fsv_ctx* c, long long work, int threads, int per_sm = 8) {
   long long g = (work + threads - 1) / threads;
   g = std::min<long long>(g, (long long)c->sm_count * per_sm);
   return (int)std::max<long long>(g, 1);
-}
-
-// Lane-owned-rows copy of the finished layout (streams A and B of
-// k_hook_sell) for the W hook warps of this device. R row segments, E entries.
-static int build_sell(fsv_ctx* c, cudaStream_t st, long long E, int R, long long n) {
-  // warp roles per CTA: wa warps sweep stream A, the others stream B
-  int wa = 20;
-  if (const char* e = getenv("FSV_SELL_WA")) wa = atoi(e);   // dev: tuning
-  wa = std::max(1, std::min(HOOK_THREADS / 32 - 1, wa));
-  const int WA = c->sm_count * wa, WB = c->sm_count * (HOOK_THREADS / 32 - wa);
-  const int W = std::max(WA, WB);
-  auto& ws = c->ws;
-  const long long R1 = (long long)R + 1;
-  CUDA_TRY(ws.s_cnt.alloc((size_t)R1 * 4));
-  int *na = ws.s_cnt.p, *nb = na + R1, *pa = nb + R1, *pb = pa + R1;
-  const long long* nzoff = ws.nzoff.p;
-  const int rg = grid_for(c, R1, 256, 16);
-  k_sell_count<<<rg, 256, 0, st>>>(c->ecolp, nzoff, R, c->H, na, nb);
-  size_t sb = 0;
-  cub::DeviceScan::ExclusiveSum(nullptr, sb, na, pa, (int)R1, st);
-  if (sb > ws.tmp.n) { CUDA_TRY(cudaStreamSynchronize(st)); CUDA_TRY(ws.tmp.alloc(sb)); }
-  sb = ws.tmp.n;
-  CUDA_TRY(cub::DeviceScan::ExclusiveSum(ws.tmp.p, sb, na, pa, (int)R1, st));
-  sb = ws.tmp.n;
-  CUDA_TRY(cub::DeviceScan::ExclusiveSum(ws.tmp.p, sb, nb, pb, (int)R1, st));
-  int PA = 0, PB = 0;
-  CUDA_TRY(cudaMemcpyAsync(&PA, pa + R, sizeof(int), cudaMemcpyDeviceToHost, st));
-  CUDA_TRY(cudaMemcpyAsync(&PB, pb + R, sizeof(int), cudaMemcpyDeviceToHost, st));
-  CUDA_TRY(cudaStreamSynchronize(st));
-  const long long P = (long long)PA + PB;
-  const long long nslA = ((long long)PA + 31) / 32, nslB = ((long long)PB + 31) / 32;
-  CUDA_TRY(ws.s_seg.alloc((size_t)std::max<long long>(P, 1)));
-  CUDA_TRY(ws.s_len.alloc((size_t)std::max<long long>(P, 1)));
-  CUDA_TRY(ws.s_start.alloc((size_t)std::max<long long>(P, 1)));
-  CUDA_TRY(ws.s_key.alloc((size_t)std::max<long long>(2 * P, 1)));
-  CUDA_TRY(ws.s_ids.alloc((size_t)std::max<long long>(2 * P, 1)));
-  CUDA_TRY(ws.s_off.alloc((size_t)(nslA + nslB + 2 * ((long long)W + 1))));
-  CUDA_TRY(c->sell_abase.alloc((size_t)WA + 1));
-  CUDA_TRY(c->sell_bbase.alloc((size_t)WB + 1));
-  int *segA = ws.s_seg.p, *segB = segA + PA, *lenA = ws.s_len.p, *lenB = lenA + PA;
-  long long *startA = ws.s_start.p, *startB = startA + PA;
-  uint32_t *keyA = ws.s_key.p, *keyB = keyA + PA, *keyAs = keyA + P, *keyBs = keyAs + PA;
-  int *idsA = ws.s_ids.p, *idsB = idsA + PA, *idsAs = idsA + P, *idsBs = idsAs + PA;
-  long long *offA = ws.s_off.p, *offB = offA + nslA, *wblkA = offB + nslB, *wblkB = wblkA + W + 1;
-  if (R)
-    k_sell_pieces<<<rg, 256, 0, st>>>(c->ecolp, nzoff, R, c->H, pa, pb, segA, startA, lenA, keyA, idsA, segB,
-                                      startB, lenB, keyB, idsB);
-  {
-    size_t s1 = 0, s2 = 0, s3 = 0;
-    cub::DeviceRadixSort::SortPairsDescending(nullptr, s1, keyA, keyAs, idsA, idsAs, PA, 0, 6, st);
-    cub::DeviceRadixSort::SortPairsDescending(nullptr, s2, keyB, keyBs, idsB, idsBs, PB, 0, 6, st);
-    cub::DeviceScan::ExclusiveSum(nullptr, s3, wblkA, c->sell_abase.p, W + 1, st);
-    const size_t need = std::max(s1, std::max(s2, s3));
-    if (need > ws.tmp.n) { CUDA_TRY(cudaStreamSynchronize(st)); CUDA_TRY(ws.tmp.alloc(need)); }
-  }
-  if (PA) { sb = ws.tmp.n; CUDA_TRY(cub::DeviceRadixSort::SortPairsDescending(ws.tmp.p, sb, keyA, keyAs, idsA, idsAs, PA, 0, 6, st)); }
-  if (PB) { sb = ws.tmp.n; CUDA_TRY(cub::DeviceRadixSort::SortPairsDescending(ws.tmp.p, sb, keyB, keyBs, idsB, idsBs, PB, 0, 6, st)); }
-  const int pg = (W + 1 + 255) / 256;
-  k_sell_plan<<<pg, 256, 0, st>>>(keyAs, PA, WA, offA, wblkA);
-  k_sell_plan<<<pg, 256, 0, st>>>(keyBs, PB, WB, offB, wblkB);
-  sb = ws.tmp.n;
-  CUDA_TRY(cub::DeviceScan::ExclusiveSum(ws.tmp.p, sb, wblkA, c->sell_abase.p, WA + 1, st));
-  sb = ws.tmp.n;
-  CUDA_TRY(cub::DeviceScan::ExclusiveSum(ws.tmp.p, sb, wblkB, c->sell_bbase.p, WB + 1, st));
-  long long TA = 0, TB = 0;
-  CUDA_TRY(cudaMemcpyAsync(&TA, c->sell_abase.p + WA, sizeof TA, cudaMemcpyDeviceToHost, st));
-  CUDA_TRY(cudaMemcpyAsync(&TB, c->sell_bbase.p + WB, sizeof TB, cudaMemcpyDeviceToHost, st));
-  CUDA_TRY(cudaStreamSynchronize(st));
-  // (+ one group of slack: the sweep's first group load is unconditional)
-  CUDA_TRY(c->sell_a.alloc((size_t)(TA + SELL_GROUP) * 32));
-  CUDA_TRY(c->sell_b.alloc((size_t)(TB + SELL_GROUP) * 32));
-  const int sgrid = c->sm_count * 16;
-  if (PA)
-    k_sell_scatter<true><<<sgrid, 256, 0, st>>>(c->ecolp, nzoff, ws.nzrows.p, c->H, segA, startA, lenA, keyAs,
-                                                idsAs, PA, WA, offA, c->sell_abase.p, c->sell_a.p);
-  if (PB)
-    k_sell_scatter<false><<<sgrid, 256, 0, st>>>(c->ecolp, nzoff, ws.nzrows.p, c->H, segB, startB, lenB, keyBs,
-                                                 idsBs, PB, WB, offB, c->sell_bbase.p, c->sell_b.p);
-  k_sell_padfill<<<c->sm_count * 2, 256, 0, st>>>(keyAs, PA, WA, offA, c->sell_abase.p, (int)n, c->sell_a.p);
-  k_sell_padfill<<<c->sm_count * 2, 256, 0, st>>>(keyBs, PB, WB, offB, c->sell_bbase.p, (int)n, c->sell_b.p);
-  CUDA_TRY(cudaGetLastError());
-  c->sell_ctas = c->sm_count;
-  c->sell_wa = wa;
-  if (getenv("FSV_UPLOAD_DEBUG"))
-    fprintf(stderr, "[upload] sliced layout: A %d pieces %lld blocks (%d warps), B %d pieces %lld blocks (%d warps)\n",
-            PA, TA, WA, PB, TB, WB);
-  return FSV_OK;
 }
 
 template <typename ColT>
@@ -1748,18 +1516,6 @@ static int upload_impl(fsv_ctx* c, int64_t n, const int64_t* h_off_arr, const Co
   if (ntask)
     k_span_row<<<grid_for(c, ntask, 256), 256, 0, st>>>(nzoff.p, nzrows.p, R + 1, ntask,
                                                          small ? STEP : SPAN, c->span_row.p);
-  // hub-table layouts also get the lane-owned-rows copy the dense hook of
-  // k_hook_sell sweeps (auto: not for small layouts, whose warps would idle)
-  c->sell = false;
-  {
-    int mode = c->sell_mode;
-    if (const char* e = getenv("FSV_SELL")) mode = atoi(e);
-    if (H > 0 && T == 1 && R > 0 && mode > 0) {   // experimental: opt-in (FSV_SELL=1) until it beats k_hook
-      int rc = build_sell(c, st, E, R, n);
-      if (rc) return rc;
-      c->sell = true;
-    }
-  }
   umark(5);
 
   // f_1 is computed by every solve (k_f1 in solve_impl), not cached here
@@ -1799,13 +1555,7 @@ static int upload_impl(fsv_ctx* c, int64_t n, const int64_t* h_off_arr, const Co
   CUDA_TRY(c->G_hub.alloc((size_t)round2m(HT))); {
     long long hpad = 0;   // dev: FSV_HPAD shifts the hub accumulator (placement checks)
     if (const char* e = getenv("FSV_HPAD")) hpad = atoll(e);
-    // copies of the shared-memory hubs' slots behind the array (k_hook_sell)
-    c->acc_reps = 8;
-    if (const char* e = getenv("FSV_ACC_REPS")) c->acc_reps = std::max(1, std::min(64, atoi(e)));   // dev
-    c->acc_rep_len = round2m(acc_len(HT));
-    c->acc_total = c->acc_rep_len + (long long)(c->acc_reps - 1) * round2m(acc_len(std::min(HT, ACC_REP_SLOTS)));
-    if (c->acc_reps > 1 && acc_len(std::min(HT, ACC_REP_SLOTS)) > c->acc_rep_len) c->acc_reps = 1;
-    CUDA_TRY(c->hub_acc.alloc((size_t)(c->acc_total + round2m(hpad))));
+    CUDA_TRY(c->hub_acc.alloc((size_t)round2m(acc_len(HT) + hpad)));
     c->hacc = c->hub_acc.p + hpad;
   }
   CUDA_TRY(c->done.alloc(1)); CUDA_TRY(c->ticket.alloc(1));
@@ -2157,7 +1907,6 @@ static int launch_hook(fsv_ctx* c, int k, bool graph) {
     a.ecol = c->ecolp; a.nspans = nspans; a.span_row = c->span_row.p;
     a.F = F; a.G = c->G; a.N = N; a.G_hub = c->G_hub.p; a.H = c->H; a.HT = c->HT;
     a.hub_acc = c->hacc; a.hub_id = c->hub_id.p;
-    a.acc_reps = (c->sell && FSV_FUSE_HUBFIX) ? c->acc_reps : 1; a.acc_rep_len = c->acc_rep_len;
     a.done = c->done.p; a.mode = c->mode.p; a.iter = k;
     PushArgs& p = a.push;
     p.list = c->dlist.p; p.count = c->dcount.p; p.rcap = c->rcap;
@@ -2171,24 +1920,13 @@ static int launch_hook(fsv_ctx* c, int k, bool graph) {
     a.fix_barrier = reinterpret_cast<unsigned*>(slot + C_FIXBAR);
     a.task_ctr = reinterpret_cast<unsigned*>(slot + C_SPANS);
     a.lc = lc;
-    a.sell.a = c->sell_a.p; a.sell.a_base = c->sell_abase.p;
-    a.sell.b = c->sell_b.p; a.sell.b_base = c->sell_bbase.p;
-    a.sell.ctas = c->sell ? c->sell_ctas : 0;
-    a.sell.wa = c->sell_wa;
-    a.sell.probe = 0;
-#ifdef FSV_SELL_PROBE
-    if (const char* e = getenv("FSV_SELL_PROBE")) a.sell.probe = atoi(e);
-#endif
-    a.sell.pref_thr = c->n / 8;
-    if (const char* e = getenv("FSV_SELL_PREF")) a.sell.pref_thr = atoll(e);   // dev: -1 always, large never
     // persistent, one CTA per SM; cooperative launch guarantees co-residency
     // for the grid barrier of the sparse (push) path
     pmark(c, k, 0);
     void* kargs[] = {&a};
     const size_t dyn = std::max<size_t>(c->H ? (size_t)(HOT_ACC + c->H) * sizeof(int) : 0,
                                         PUSH_SCRATCH_BYTES);
-    const void* fn = c->sell ? (c->HT > c->H ? (const void*)k_hook_sell<true> : (const void*)k_hook_sell<false>)
-                     : small ? (c->HT > c->H ? (const void*)k_hook<true, true, 1>
+    const void* fn = small ? (c->HT > c->H ? (const void*)k_hook<true, true, 1>
                               : c->H       ? (const void*)k_hook<true, false, 1>
                                            : (const void*)k_hook<false, false, 1>)
                            : (c->HT > c->H ? (const void*)k_hook<true, true, STEPS>
@@ -2427,8 +2165,7 @@ static std::vector<long long> graph_key(const fsv_ctx* c) {
           P(c->hacc), P(c->hub_id.p), P(c->done.p), P(c->mode.p), P(c->dlist.p), P(c->dcount.p), c->rcap,
           c->dgrid, P(c->offp), P(c->colsp), c->col_base, c->row_begin, c->row_end, P(c->cnt.p),
           P(c->chunks.p), P(c->iterbuf.p), P(c->tstamp.p), P(c->ticket.p), P(c->partials.p), c->n,
-          c->sm_count, P(c->comm), (long long)c->sell, c->sell_wa, P(c->sell_a.p), P(c->sell_b.p), P(c->sell_abase.p),
-          P(c->sell_bbase.p)};
+          c->sm_count, P(c->comm)};
 }
 
 // Builds (or reuses) the CUDA graph of the iteration loop: one conditional
@@ -2749,7 +2486,7 @@ static int solve_body(fsv_ctx* const* cs, int count, const fsv_config* cfg, int3
     };
     for (int q = 0; q < count; ++q) {
       const fsv_ctx* x = cs[q];
-      add_red(x->xb.p, x->xb.n); add_red(x->f1.p, x->f1.n); add_red(x->hacc, (size_t)x->acc_total);
+      add_red(x->xb.p, x->xb.n); add_red(x->f1.p, x->f1.n); add_red(x->hacc, (size_t)acc_len(x->HT));
       add_ld(x->xb.p, x->xb.n); add_ld(x->f1.p, x->f1.n); add_ld(x->gb.p, x->gb.n);
       add_ld(x->G_hub.p, x->G_hub.n); add_ld(x->hub_id.p, x->hub_id.n); add_ld(x->colsp, (size_t)x->csr_local);
       add_ld(x->span_row.p, x->span_row.n);
@@ -2778,7 +2515,7 @@ static int solve_body(fsv_ctx* const* cs, int count, const fsv_config* cfg, int3
   for (int r = 0; r < count; ++r) {
     fsv_ctx* x = cs[r];
     k_solve_init<<<grid_for(x, std::max<long long>(x->HT, (long long)cap * NCOUNT), 256), 256, 0, st>>>(
-        x->X, x->Y, x->G, x->n, x->hacc, x->HT ? x->acc_total : 0, x->cnt.p, (long long)cap * NCOUNT, x->done.p,
+        x->X, x->Y, x->G, x->n, x->hacc, x->HT, x->cnt.p, (long long)cap * NCOUNT, x->done.p,
         x->ticket.p, x->mode.p, x->policy == 2 ? 1 : 0, x->tstamp.p, x->rep.p);
   }
   pmark(c, 1, 6);

@@ -152,17 +152,6 @@ __device__ __forceinline__ int ldg(const int* p) {
   return __ldg(p);
 }
 
-// Random gathers of vertex values that never hit L1 (the hub table leaves it
-// ~28 KB): L2-only loads run ~13% faster than the read-only path there
-// (tools/gather_smem_probe.cu: 139 vs 123 G gathers/s).
-#ifndef FSV_GATHER_CG
-#define FSV_GATHER_CG 1
-#endif
-__device__ __forceinline__ int ldgather(const int* p) {
-  FSV_CHK_LD(p);
-  return FSV_GATHER_CG ? __ldcg(p) : __ldg(p);
-}
-
 __device__ __forceinline__ void red_min(int* p, int v) {
   FSV_CHK_RED(p);
   asm volatile("red.relaxed.gpu.global.min.s32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
@@ -180,10 +169,6 @@ __device__ __forceinline__ void red_min_shared(uint32_t saddr, int v) {
 #define FSV_ACC_STRIDE 1
 #endif
 constexpr int ACC_SPREAD = 65536;
-// Slots below ACC_REP_SLOTS (every shared-memory hub) have acc_reps copies of
-// their accumulator: reductions aimed at one slot from all SMs serialise on
-// the L2 sector that holds it, and the copies divide that queue.
-constexpr int ACC_REP_SLOTS = 65536;
 __host__ __device__ __forceinline__ long long acc_at(long long s) {
   return FSV_ACC_STRIDE == 1 ? s
          : (s < ACC_SPREAD ? s * FSV_ACC_STRIDE : (long long)ACC_SPREAD * FSV_ACC_STRIDE + (s - ACC_SPREAD));
@@ -281,20 +266,6 @@ struct PushArgs {
   unsigned* barrier;            // grid barrier counter of this iteration
 };
 
-// Lane-owned-rows ("sliced") copy of the oriented layout, used by k_hook_sell
-// on hub-table layouts (see the section before that kernel): two streams of
-// 256-byte blocks per hook warp, planned for `warps` warps.
-struct SellArgs {
-  const uint2* a;            // stream A: shared-memory hub columns, 16-bit slots
-  const long long* a_base;   // [ctas * wa + 1] first block of each A warp's run
-  const uint2* b;            // stream B: every other column, 32-bit codes
-  const long long* b_base;   // [ctas * (warps per CTA - wa) + 1]
-  int ctas;                  // CTAs the streams were planned for (0: no sliced copy)
-  int wa;                    // warps of each CTA that sweep stream A; the others sweep B
-  int probe;                 // dev probes (FSV_SELL_PROBE builds)
-  long long pref_thr;        // rows load their parent with their gf when more gf values than this changed
-};                           // in the previous iteration (most rows then emit), else only when they emit
-
 struct HookArgs {
   const uint32_t* ecol;   // oriented entries (headers + edges), padded to SPAN
   long long nspans;       // warp tasks of NSTEP consecutive STEP-entry steps
@@ -306,9 +277,6 @@ struct HookArgs {
   int H;                  // shared-memory slots (multiple of 4)
   int HT;                 // all tier slots: [0,H) shared memory, [H,HT) the L2 rank tier
   int* hub_acc;           // column-side minima aimed at tier slots
-  int acc_reps;           // copies of the first ACC_REP_SLOTS accumulator slots (k_hook_sell: CTA b
-  long long acc_rep_len;  // reduces into copy b % acc_reps, copy r at hub_acc + r * acc_rep_len; r = 0 is
-                          // the array itself); the hub fix-up takes the minimum over the copies
   const int* hub_id;      // slot -> vertex (fused hub fix-up)
   unsigned* fix_barrier;  // grid barrier before the fused hub fix-up
   unsigned* task_ctr;     // dynamic tail of the dense task loop (FSV_DYN_TAIL)
@@ -317,7 +285,6 @@ struct HookArgs {
   int iter;
   PushArgs push;
   LoopCtl lc;
-  SellArgs sell;
 };
 
 // Changed-gf ("delta") list written by the vertex pass: warp w owns
@@ -663,9 +630,12 @@ __device__ __forceinline__ int gather_gf_tier(uint32_t c, uint32_t s_base, const
 // differs and no carried minimum is pending, the whole step is a no-op apart
 // from carry bookkeeping — the common case once components have converged.
 
-// Graph mode: iteration number, buffers and per-iteration counter slots come
-// from device memory (the loop body is captured once).
-__device__ __forceinline__ void hook_loop_args(HookArgs& a) {
+// HUBS = false (no hub slots, H == 0) compiles the hub table, hub mask and
+// accumulators out; TIER (implies HUBS) adds the L2 rank tier gathers.
+template <bool HUBS, bool TIER, int NSTEP>
+__global__ void __launch_bounds__(HOOK_THREADS, 1) k_hook(HookArgs a) {
+  extern __shared__ int s_hub[];
+  if (__ldcg(a.done)) return;
   if (a.lc.graph == 1) {
     const int it = loop_iter(a.lc, a.iter);
     unsigned long long* slot = a.lc.cnt_base + (size_t)(it - 1) * NCOUNT;
@@ -680,81 +650,32 @@ __device__ __forceinline__ void hook_loop_args(HookArgs& a) {
     a.fix_barrier = reinterpret_cast<unsigned*>(slot + C_FIXBAR);
     a.task_ctr = reinterpret_cast<unsigned*>(slot + C_SPANS);
   }
-}
-
-// Sparse iteration: push from the vertices whose gf changed; the push
-// scratch aliases the (unused) hub table in dynamic shared memory.
-__device__ __forceinline__ void hook_push(const HookArgs& a, int* s_hub) {
-  long long* s_start = reinterpret_cast<long long*>(s_hub);
-  long long* s_excl = s_start + HOOK_THREADS;
-  int* s_val = reinterpret_cast<int*>(s_excl + HOOK_THREADS);
-  int* s_list = s_val + HOOK_THREADS;            // 128 expanded vertices per warp
-  const int wib = threadIdx.x >> 5;
-  DBG_T(0);
-  push_local(a.push, s_start + wib * 32, s_excl + wib * 32, s_val + wib * 32, s_list + wib * 128);
-  // grid barrier: every CTA is resident (one persistent CTA per SM)
-  __syncthreads();
-  DBG_T(1);
-  if (threadIdx.x == 0) {
-    __threadfence();
-    atomicAdd(a.push.barrier, 1u);
-    while (*(volatile unsigned*)a.push.barrier < gridDim.x) __nanosleep(64);
-    __threadfence();
-  }
-  __syncthreads();
-  DBG_T(2);
-  push_big(a.push);
-#ifdef FSV_DEBUG_TIMING
-  __syncthreads();
-  DBG_T(3);
-#endif
-}
-
-// End of a dense hook on a hub-table layout: flush the CTA's hot
-// accumulators, then (fused hub fix-up) a grid barrier and the accumulated
-// column-side minima go to N (k_hubfix's work).
-__device__ __forceinline__ void hook_hub_finish(const HookArgs& a, int* s_hub) {
-  int* __restrict__ hub_acc = a.hub_acc;
-  int* __restrict__ my_acc = hub_acc + (long long)(blockIdx.x % a.acc_reps) * a.acc_rep_len;
-  __syncthreads();
-  for (int i = threadIdx.x; i < HOT_ACC; i += blockDim.x) {
-    const int v = s_hub[i];
-    if (v != INF) red_min(my_acc + acc_at(i), v);
-  }
-#if FSV_FUSE_HUBFIX
-  // every CTA is resident (cooperative launch, one persistent CTA per SM)
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    atomicAdd(a.fix_barrier, 1u);
-    while (*(volatile unsigned*)a.fix_barrier < gridDim.x) __nanosleep(32);
-    __threadfence();
-  }
-  __syncthreads();
-  for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < a.HT; s += gridDim.x * blockDim.x) {
-    int acc = __ldcg(hub_acc + acc_at(s));
-    if (acc != INF) hub_acc[acc_at(s)] = INF;
-    if (s < ACC_REP_SLOTS)
-      for (int r = 1; r < a.acc_reps; ++r) {
-        int* p = hub_acc + (long long)r * a.acc_rep_len + acc_at(s);
-        const int x = __ldcg(p);
-        if (x != INF) { *p = INF; acc = min(acc, x); }
-      }
-    if (acc == INF) continue;
-    emit_row(ldg(a.hub_id + s), ldg(a.G_hub + s), acc, a.F, a.G, a.N);
-  }
-#endif
-}
-
-// HUBS = false (no hub slots, H == 0) compiles the hub table, hub mask and
-// accumulators out; TIER (implies HUBS) adds the L2 rank tier gathers.
-template <bool HUBS, bool TIER, int NSTEP>
-__global__ void __launch_bounds__(HOOK_THREADS, 1) k_hook(HookArgs a) {
-  extern __shared__ int s_hub[];
-  if (__ldcg(a.done)) return;
-  hook_loop_args(a);
   if (a.mode[a.iter] == 1) {
-    hook_push(a, s_hub);
+    // sparse iteration: push from the vertices whose gf changed; the push
+    // scratch aliases the (unused) hub table in dynamic shared memory
+    long long* s_start = reinterpret_cast<long long*>(s_hub);
+    long long* s_excl = s_start + HOOK_THREADS;
+    int* s_val = reinterpret_cast<int*>(s_excl + HOOK_THREADS);
+    int* s_list = s_val + HOOK_THREADS;            // 128 expanded vertices per warp
+    const int wib = threadIdx.x >> 5;
+    DBG_T(0);
+    push_local(a.push, s_start + wib * 32, s_excl + wib * 32, s_val + wib * 32, s_list + wib * 128);
+    // grid barrier: every CTA is resident (one persistent CTA per SM)
+    __syncthreads();
+    DBG_T(1);
+    if (threadIdx.x == 0) {
+      __threadfence();
+      atomicAdd(a.push.barrier, 1u);
+      while (*(volatile unsigned*)a.push.barrier < gridDim.x) __nanosleep(64);
+      __threadfence();
+    }
+    __syncthreads();
+    DBG_T(2);
+    push_big(a.push);
+#ifdef FSV_DEBUG_TIMING
+    __syncthreads();
+    DBG_T(3);
+#endif
     return;
   }
   // s_hub[0, HOT_ACC): this CTA's accumulator of the hottest hub slots;
@@ -1009,232 +930,31 @@ __global__ void __launch_bounds__(HOOK_THREADS, 1) k_hook(HookArgs a) {
       s += nwarps;
     }
   }
-  if (HUBS) hook_hub_finish(a, s_hub);
-}
-
-// ---- dense hook over lane-owned rows (hub-table layouts) ---------------------
-//
-// k_hook's warp step spends most of its instructions on finding row
-// boundaries inside a lane's entries and on the segmented scan that joins a
-// row's lanes. This layout removes both: the oriented rows are cut into
-// pieces of at most SELL_CAP entries, the pieces are sorted by length, and 32
-// consecutive pieces form a slice in which lane l owns piece l (a sliced
-// ELLPACK). A lane's row vertex, its gf and its running minimum are plain
-// registers; a row's end is the slice's end, the same for all lanes. A piece
-// emits its own partial row minimum (min-reductions are idempotent), shorter
-// pieces of a slice repeat their last entry, and the lanes past the last
-// piece of a stream repeat the last piece (duplicates are harmless too).
-//
-// Entries are split by where their gf is gathered from:
-//   stream A  columns with a shared-memory hub slot (< H): 16-bit slots, four
-//             per 8-byte lane word; column side goes to the hub accumulator
-//   stream B  every other column (vertex ids, or HUB|slot of the L2 rank
-//             tier): two 32-bit codes per lane word
-// A stream is a sequence of 256-byte blocks (one 8-byte word per lane): a
-// header block {row vertex, data blocks that follow} opens a slice. Each hook
-// warp owns one contiguous run of blocks per stream (slices are dealt to the
-// warps in snake order over the length-sorted list, so the runs are balanced
-// at build time) and walks it SELL_GROUP blocks at a time with the next group
-// in flight; a run is padded to whole groups with empty headers of the dummy
-// vertex n (gf = INF, never emits).
-// Dev probes (-DFSV_SELL_PROBE, runtime mask in SellArgs::probe from the
-// FSV_SELL_PROBE environment variable; wrong results, timing only):
-// 1 no column-side emissions, 2 no row-side emissions, 4 no header gathers,
-// 8 no table gathers, 16 stream-B warps idle, 32 stream-A warps idle.
-#ifdef FSV_SELL_PROBE
-#define SELL_PROBE(bit) ((probe & (bit)) != 0)
-#else
-#define SELL_PROBE(bit) false
+  if (HUBS) {
+    __syncthreads();
+    for (int i = threadIdx.x; i < HOT_ACC; i += blockDim.x) {
+      const int v = s_hub[i];
+      if (v != INF) red_min(hub_acc + acc_at(i), v);
+    }
+#if FSV_FUSE_HUBFIX
+    // hub fix-up in the same launch: grid barrier (every CTA is resident),
+    // then the accumulated column-side minima go to N (k_hubfix's work)
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      atomicAdd(a.fix_barrier, 1u);
+      while (*(volatile unsigned*)a.fix_barrier < gridDim.x) __nanosleep(32);
+      __threadfence();
+    }
+    __syncthreads();
+    for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < a.HT; s += gridDim.x * blockDim.x) {
+      const int acc = __ldcg(hub_acc + acc_at(s));
+      if (acc == INF) continue;
+      hub_acc[acc_at(s)] = INF;
+      emit_row(ldg(a.hub_id + s), ldg(a.G_hub + s), acc, F, G, N);
+    }
 #endif
-constexpr int SELL_GROUP = 4;          // blocks per pipeline group
-constexpr int SELL_CAP_A = 128;        // entries per piece, stream A (32 blocks of 4)
-constexpr int SELL_CAP_B = 64;         // entries per piece, stream B (32 blocks of 2)
-
-__device__ __forceinline__ uint2 ld_stream8(const uint2* p, uint64_t pol) {
-  uint2 r;
-  asm volatile("ld.global.nc.L2::cache_hint.v2.u32 {%0,%1}, [%2], %3;"
-               : "=r"(r.x), "=r"(r.y) : "l"(p), "l"(pol));
-  return r;
-}
-
-__device__ __forceinline__ int lds_gf(uint32_t saddr) {
-  int v;
-  asm("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(saddr));
-  return v;
-}
-
-// gf of a stream-B column: a vertex from G, a tier slot from the compact G_hub
-template <bool TIER>
-__device__ __forceinline__ int gather_b(uint32_t c, const int* __restrict__ G, const int* __restrict__ G_hub) {
-  if (TIER) {
-    const int* gp = (c & HUB) ? G_hub + (c & IDMASK) : G + c;
-    return ldgather(gp);
   }
-  return ldgather(G + c);
-}
-
-// One stream of this warp: `sp` = the warp's first block + lane, ngroups
-// groups of SELL_GROUP blocks.
-template <bool A, bool TIER, bool PREF>
-__device__ __forceinline__ void sell_sweep(const uint2* __restrict__ sp, int ngroups, uint32_t s_acc,
-                                           uint32_t s_base, const int* __restrict__ F,
-                                           const int* __restrict__ G, int* __restrict__ N,
-                                           const int* __restrict__ G_hub, int* __restrict__ hub_acc,
-                                           uint64_t pol, int probe) {
-  if (ngroups <= 0) return;
-  constexpr int PER = A ? 4 : 2;       // entries per lane word
-  uint2 q[SELL_GROUP], nx[SELL_GROUP];
-#pragma unroll
-  for (int d = 0; d < SELL_GROUP; ++d) q[d] = ld_stream8(sp + d * 32, pol);
-  int rem = 0;                          // data blocks left in the open slice (warp-uniform)
-  int u = 0, gu = INF, tu = 0, run = INF;
-#pragma unroll 1
-  for (int g = 0; g < ngroups; ++g) {
-    sp += SELL_GROUP * 32;
-    if (g + 1 < ngroups) {
-#pragma unroll
-      for (int d = 0; d < SELL_GROUP; ++d) nx[d] = ld_stream8(sp + d * 32, pol);
-    }
-    // which blocks of the group are headers: known from the slice lengths alone
-    bool hd[SELL_GROUP];
-#pragma unroll
-    for (int d = 0; d < SELL_GROUP; ++d) {
-      hd[d] = rem == 0;
-      rem = hd[d] ? (int)q[d].y : rem - 1;
-    }
-    // every gather of the group in flight together: a header's gf and parent,
-    // a data block's column gf values
-    int v[SELL_GROUP][PER];
-#pragma unroll
-    for (int d = 0; d < SELL_GROUP; ++d) {
-      if (hd[d]) {
-        if (SELL_PROBE(4)) {   // dev probe: no header gathers (wrong results)
-          v[d][0] = (int)(q[d].x | 0x100000u);
-          if (PREF) v[d][1] = (int)q[d].x;
-        } else {
-          v[d][0] = ldgather(G + q[d].x);
-          if (PREF) v[d][1] = ldgather(F + q[d].x);
-        }
-      } else if (A) {
-        if (SELL_PROBE(8)) {   // dev probe: no table gathers (wrong results)
-          v[d][0] = (int)(q[d].x & 0xffffu); v[d][1] = (int)(q[d].x >> 16);
-          v[d][2 % PER] = (int)(q[d].y & 0xffffu); v[d][3 % PER] = (int)(q[d].y >> 16);
-        } else {
-          v[d][0] = lds_gf(s_base + ((q[d].x & 0xffffu) << 2));
-          v[d][1] = lds_gf(s_base + ((q[d].x >> 16) << 2));
-          v[d][2 % PER] = lds_gf(s_base + ((q[d].y & 0xffffu) << 2));
-          v[d][3 % PER] = lds_gf(s_base + ((q[d].y >> 16) << 2));
-        }
-      } else {
-        v[d][0] = gather_b<TIER>(q[d].x, G, G_hub);
-        v[d][1] = gather_b<TIER>(q[d].y, G, G_hub);
-      }
-    }
-#pragma unroll
-    for (int d = 0; d < SELL_GROUP; ++d) {
-      if (hd[d]) {
-        // the slice that ends here: each lane's piece minimum -> its row vertex
-        if (run < gu && !SELL_PROBE(2)) {
-          red_min(N + u, run);
-          if (!PREF) tu = ldg(F + u);
-          if (tu != u) red_min(N + tu, run);
-        }
-        u = (int)q[d].x;
-        gu = v[d][0];
-        if (PREF) tu = v[d][1];
-        run = INF;
-      } else if (A) {
-        const int lo = min(min(v[d][0], v[d][1]), min(v[d][2 % PER], v[d][3 % PER]));
-        const int hi = max(max(v[d][0], v[d][1]), max(v[d][2 % PER], v[d][3 % PER]));
-        run = min(run, lo);
-        if (gu < hi && !SELL_PROBE(1)) {
-          // column side: gf of the row -> the hub's accumulator slot
-          const uint32_t sl[4] = {q[d].x & 0xffffu, q[d].x >> 16, q[d].y & 0xffffu, q[d].y >> 16};
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            if (gu < v[d][j % PER]) {
-              if (sl[j] < (uint32_t)HOT_ACC) red_min_shared(s_acc + (sl[j] << 2), gu);
-              else red_min(hub_acc + acc_at(sl[j]), gu);
-            }
-          }
-        }
-      } else {
-        run = min(run, min(v[d][0], v[d][1]));
-        if (gu < max(v[d][0], v[d][1]) && !SELL_PROBE(1)) {
-          const uint32_t cc[2] = {q[d].x, q[d].y};
-          int t[2] = {-1, -1};
-#pragma unroll
-          for (int j = 0; j < 2; ++j) {
-            if (gu < v[d][j]) {
-              if (TIER && (cc[j] & HUB)) {
-                red_min(hub_acc + acc_at(cc[j] & IDMASK), gu);
-              } else {
-                red_min(N + cc[j], gu);
-                t[j] = ldg(F + cc[j]);
-              }
-            }
-          }
-#pragma unroll
-          for (int j = 0; j < 2; ++j)
-            if (t[j] >= 0 && t[j] != (int)cc[j]) red_min(N + t[j], gu);
-        }
-      }
-    }
-#pragma unroll
-    for (int d = 0; d < SELL_GROUP; ++d) q[d] = nx[d];
-  }
-  if (run < gu && !SELL_PROBE(2)) {
-    red_min(N + u, run);
-    if (!PREF) tu = ldg(F + u);
-    if (tu != u) red_min(N + tu, run);
-  }
-}
-
-template <bool TIER>
-__global__ void __launch_bounds__(HOOK_THREADS, 1) k_hook_sell(HookArgs a) {
-  extern __shared__ int s_hub[];
-  if (__ldcg(a.done)) return;
-  hook_loop_args(a);
-  if (a.mode[a.iter] == 1) {
-    hook_push(a, s_hub);
-    return;
-  }
-  for (int i = threadIdx.x; i < (a.H >> 2); i += blockDim.x)
-    reinterpret_cast<int4*>(s_hub + HOT_ACC)[i] = reinterpret_cast<const int4*>(a.G_hub)[i];
-  for (int i = threadIdx.x; i < HOT_ACC; i += blockDim.x) s_hub[i] = INF;
-  __syncthreads();
-  const uint32_t s_acc = (uint32_t)__cvta_generic_to_shared(s_hub);
-  const uint32_t s_base = s_acc + 4u * HOT_ACC;
-  const int lane = threadIdx.x & 31;
-  const uint64_t pol = policy_evict_first();
-  // warp roles: the first wa warps of a CTA sweep stream A (shared-memory
-  // gathers), the others stream B (L2/DRAM gathers), so the two kinds of
-  // latency overlap on every SM
-  const int wib = threadIdx.x >> 5, wa = a.sell.wa, wb = (blockDim.x >> 5) - wa;
-  const int probe = a.sell.probe;
-  (void)probe;
-  // shared-memory hub slots reduce into this CTA's copy of the accumulator
-  int* my_acc = a.hub_acc + (long long)(blockIdx.x % a.acc_reps) * a.acc_rep_len;
-  const bool pref = (long long)__ldcg(a.lc.cnt_base + (size_t)(a.iter - 2) * NCOUNT + C_GF) > a.sell.pref_thr;
-  if ((int)blockIdx.x < a.sell.ctas) {
-    if (wib < wa && SELL_PROBE(32)) {
-    } else if (wib < wa) {
-      const long long* ab = a.sell.a_base + (long long)blockIdx.x * wa + wib;
-      const long long a0 = ab[0], a1 = ab[1];
-      const uint2* sp = a.sell.a + a0 * 32 + lane;
-      const int ng = (int)((a1 - a0) / SELL_GROUP);
-      if (pref) sell_sweep<true, TIER, true>(sp, ng, s_acc, s_base, a.F, a.G, a.N, a.G_hub, my_acc, pol, probe);
-      else sell_sweep<true, TIER, false>(sp, ng, s_acc, s_base, a.F, a.G, a.N, a.G_hub, my_acc, pol, probe);
-    } else if (!SELL_PROBE(16)) {
-      const long long* bb = a.sell.b_base + (long long)blockIdx.x * wb + (wib - wa);
-      const long long b0 = bb[0], b1 = bb[1];
-      const uint2* sp = a.sell.b + b0 * 32 + lane;
-      const int ng = (int)((b1 - b0) / SELL_GROUP);
-      if (pref) sell_sweep<false, TIER, true>(sp, ng, s_acc, s_base, a.F, a.G, a.N, a.G_hub, a.hub_acc, pol, probe);
-      else sell_sweep<false, TIER, false>(sp, ng, s_acc, s_base, a.F, a.G, a.N, a.G_hub, a.hub_acc, pol, probe);
-    }
-  }
-  hook_hub_finish(a, s_hub);
 }
 
 // ---- hub accumulator -> N ---------------------------------------------------
@@ -1554,12 +1274,12 @@ __global__ void __launch_bounds__(SC_THREADS) k_first(FirstArgs a) {
 }
 
 // ---- solve-start initialisation ----------------------------------------------
-__global__ void k_solve_init(int* X, int* Y, int* G, long long n, int* hub_acc, long long H,
+__global__ void k_solve_init(int* X, int* Y, int* G, long long n, int* hub_acc, int H,
                              unsigned long long* cnt, long long ncnt, int* done, unsigned* ticket,
                              int* mode, int first_mode, unsigned long long* tstamp, SolveReport* rep) {
   const long long t0 = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const long long stride = (long long)gridDim.x * blockDim.x;
-  for (long long s = t0; s < H; s += stride) hub_acc[s] = INF;   // H = ints of the accumulator and its copies
+  for (long long s = t0; s < H; s += stride) hub_acc[acc_at(s)] = INF;
   for (long long k = t0; k < ncnt; k += stride) cnt[k] = 0ull;
   if (t0 == 0) {
     X[n] = (int)n; Y[n] = (int)n; G[n] = INF;  // dummy vertex n of the padding row
