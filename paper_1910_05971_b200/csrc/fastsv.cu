@@ -1938,7 +1938,7 @@ static int launch_hook(fsv_ctx* c, int k, bool graph) {
   }
   if (c->HT && !FSV_FUSE_HUBFIX) {
     pmark(c, k, 2);
-    k_hubfix<<<grid_for(c, c->HT, 256), 256, 0, st>>>(c->hacc, c->hub_id.p, c->G_hub.p, c->HT, F, c->G, N,
+    k_hubfix<<<grid_for(c, c->HT, 256), 256, 0, st>>>(c->hacc, c->hub_id.p, c->G_hub.p, c->HT, N,
                                                        c->done.p, c->mode.p, k,
                                                        graph ? c->iterbuf.p : nullptr, c->X, c->Y);
     pmark(c, k, 3);
@@ -1982,8 +1982,12 @@ static int launch_vertex(fsv_ctx* c, int k, int max_iter, bool graph) {
   s.dl = delta_out(c);
   s.iter = k; s.max_iter = max_iter;
   s.lc = lc;
+  s.mode = c->mode.p;
   pmark(c, k, 6);
-  k_shortcut<<<vertex_grid(c), SC_THREADS, 0, c->stream>>>(s);
+  // cooperative: the stochastic hooks of a dense iteration need grid barriers
+  void* kargs[] = {&s};
+  CUDA_TRY(cudaLaunchCooperativeKernel((const void*)k_shortcut, dim3(vertex_grid(c)), dim3(SC_THREADS), kargs, 0,
+                                       c->stream));
   pmark(c, k, 7);
   ++c->launches;
   return FSV_OK;

@@ -25,8 +25,16 @@
 //
 // Writes into N are min-atomics filtered by the read-only gf_k: N[x] <= gf_k[x]
 // always and gf_k[F[x]] <= gf_k[x], so val >= gf_k[x] makes both hooks
-// no-ops. The stochastic target of a column-side emission is not filtered a
-// second time (a no-op min is harmless; the gather costs more than it saves).
+// no-ops.
+//
+// Stochastic hooks of a dense iteration are deferred to the vertex pass: the
+// dense sweep only applies the aggressive hooks (N[x] <-min val), which leaves
+// N[u] = min(gf_k[u], mngf[u]); k_shortcut then applies f[f_k[u]] <-min
+// mngf[u] once per lowered vertex (N[u] < gf_k[u] implies N[u] = mngf[u];
+// for the others mngf[u] >= gf_k[u] >= gf_k[f_k[u]] >= N[f_k[u]] is a no-op)
+// from coalesced streams, instead of a parent gather and a second reduction
+// per contributing entry inside the sweep. A sparse (push) iteration applies
+// both hooks inline.
 #pragma once
 #include <cstdint>
 #include <cstdio>
@@ -87,7 +95,8 @@ constexpr int NCOUNT = 16;               // counter slots per iteration
 enum { C_GF = 0, C_F = 1, C_NONSTAR = 2, C_ROOTS = 3, C_VIOL = 4,   // vertex-pass counters
        C_FLOPS = 5, C_CHUNKS = 6, C_BARRIER = 8,       // push bookkeeping
        C_FIXBAR = 9,                                   // hub fix-up barrier of the dense hook
-       C_SPANS = 10 };                                 // dynamic task counter of the dense hook
+       C_SPANS = 10,                                   // dynamic task counter of the dense hook
+       C_SCBAR = 11, C_SCBAR2 = 12 };                  // grid barriers of the vertex pass (deferred hooks)
 
 // ---- memory helpers -------------------------------------------------------
 
@@ -305,7 +314,8 @@ struct DeltaOut {
 struct ShortcutArgs {
   int* F;                 // in: f_k; out: gf_{k+1} (next N init)
   int* G;                 // in: gf_k; out: gf_{k+1}
-  const int* N;           // f_{k+1}
+  int* N;                 // f_{k+1} (the stochastic hooks of a dense iteration are applied to it here)
+  const int* mode;        // mode[iter]: 0 after a dense sweep (aggressive hooks only), 1 after a push
   long long n;
   const int* hub_id;
   int* G_hub;
@@ -322,20 +332,13 @@ struct ShortcutArgs {
 
 // ---- emission of one hook contribution -------------------------------------
 
-// Row side: run minimum `val` of row vertex u (gu = gf_k[u]).
-__device__ __forceinline__ void emit_row(int u, int gu, int val, const int* __restrict__ F,
-                                         const int* __restrict__ G, int* __restrict__ N) {
-  if (val < gu) {
-    red_min(N + u, val);                 // aggressive: f[u] <-min mngf[u]
-    int t = ldg(F + u);
-    if (t != u && val < ldg(G + t)) red_min(N + t, val);  // stochastic: f[f[u]] <-min mngf[u]
-  }
+// Aggressive hook of the dense sweep: value `val` (a row's run minimum, or a
+// row's gf on the column side) aimed at vertex u whose gf is gu. The
+// stochastic hook is deferred to the vertex pass (k_shortcut).
+__device__ __forceinline__ void emit_agg(int u, int gu, int val, int* __restrict__ N) {
+  if (val < gu) red_min(N + u, val);
 }
 
-// Row emission inside k_hook, with the parent t = F[u] already loaded (or
-// loaded here when t < 0). The stochastic target is filtered by gf[t] only
-// with FSV_ROW_FILTER: the filter is a second dependent gather on the
-// critical path of a step, a no-op min is harmless.
 // k_hook applies the hub accumulator itself after a grid barrier instead of
 // a separate k_hubfix launch.
 #ifndef FSV_FUSE_HUBFIX
@@ -361,39 +364,11 @@ __device__ __forceinline__ void emit_row(int u, int gu, int val, const int* __re
 #ifndef FSV_DENSE_LANES
 #define FSV_DENSE_LANES 16
 #endif
-#ifndef FSV_PREF
-#define FSV_PREF 0
-#endif
-#ifndef FSV_ROW_FILTER
-#define FSV_ROW_FILTER 0
-#endif
 // Dev speed-of-light probes (wrong results, timing only): bit 0 drops the
 // dense hook's emissions, bit 1 its global gathers.
 #ifndef FSV_SOL
 #define FSV_SOL 0
 #endif
-__device__ __forceinline__ void emit_row_t(int u, int val, int t, const int* __restrict__ F,
-                                           const int* __restrict__ G, int* __restrict__ N) {
-  red_min(N + u, val);
-  if (t < 0) t = ldg(F + u);
-  if (t != u && (!FSV_ROW_FILTER || val < ldg(G + t))) red_min(N + t, val);
-}
-
-// Column side of edge entry c of a row whose gf is gu: v <- gu (kept for
-// the hub-accumulator fix-up path and for clarity; k_hook batches these).
-__device__ __forceinline__ void emit_col(uint32_t c, int gu, const int* __restrict__ F,
-                                         const int* __restrict__ G, int* __restrict__ N,
-                                         int* __restrict__ hub_acc) {
-  const int x = (int)(c & IDMASK);
-  if (c & HUB) {
-    red_min(hub_acc + acc_at(x), gu);
-  } else {
-    red_min(N + x, gu);
-    int t = ldg(F + x);
-    if (t != x && gu < ldg(G + t)) red_min(N + t, gu);
-  }
-}
-
 // One gathered gf value per entry: hub edges from the shared-memory table
 // (32-bit shared address, no generic conversion), everything else from
 // global through the read-only path. Both loads are predicated, no branch.
@@ -691,7 +666,6 @@ __global__ void __launch_bounds__(HOOK_THREADS, 1) k_hook(HookArgs a) {
   const uint32_t s_acc = (uint32_t)__cvta_generic_to_shared(s_hub);
   const uint32_t s_base = s_acc + 4u * HOT_ACC;
 
-  const int* __restrict__ F = a.F;
   const int* __restrict__ G = a.G;
   int* __restrict__ N = a.N;
   int* __restrict__ hub_acc = a.hub_acc;
@@ -777,7 +751,7 @@ __global__ void __launch_bounds__(HOOK_THREADS, 1) k_hook(HookArgs a) {
       // the smallest of them is the row minimum). No scan, no pending run:
       // a run carried in from a scan step is emitted here by lane 0.
       if (!dense && !__any_sync(0xffffffffu, nrec > FSV_REC)) {
-        if (lane == 0 && carry_run < carry_gu) emit_row(carry_u, carry_gu, carry_run, F, G, N);
+        if (lane == 0) emit_agg(carry_u, carry_gu, carry_run, N);
         if (nrec && !(FSV_SOL & 1)) {
           // second pass: pick out the (at most two) records of this lane
           uint32_t rx0 = 0u, rx1 = 0u;
@@ -801,23 +775,18 @@ __global__ void __launch_bounds__(HOOK_THREADS, 1) k_hook(HookArgs a) {
           const bool h0 = HUBS && (rx0 & HUB), h1 = HUBS && nrec > 1 && (rx1 & HUB);
           const bool g1 = nrec > 1 && !h1;
           const int x0 = (int)(rx0 & IDMASK), x1 = (int)(rx1 & IDMASK);
-          int t0 = -1, t1 = -1;
           if (h0) {
             if (x0 < HOT_ACC) red_min_shared(s_acc + 4u * (uint32_t)x0, ry0);
             else red_min(hub_acc + acc_at(x0), ry0);
           } else {
             red_min(N + x0, ry0);
-            t0 = ldg(F + x0);
           }
           if (h1) {
             if (x1 < HOT_ACC) red_min_shared(s_acc + 4u * (uint32_t)x1, ry1);
             else red_min(hub_acc + acc_at(x1), ry1);
           } else if (g1) {
             red_min(N + x1, ry1);
-            t1 = ldg(F + x1);
           }
-          if (t0 >= 0 && t0 != x0) red_min(N + t0, ry0);
-          if (t1 >= 0 && t1 != x1) red_min(N + t1, ry1);
         }
         carry_run = INF;
         if (hb) {
@@ -836,15 +805,8 @@ __global__ void __launch_bounds__(HOOK_THREADS, 1) k_hook(HookArgs a) {
       //             threshold = its gf
       //   edge j:   column side, target = v (or hub slot), value = row gf,
       //             threshold = gf[v]
-      // then every active slot does N[target] <-min value and the stochastic
-      // N[F[target]] <-min value, with all loads of the lane in flight together.
-#if FSV_PREF
-      // parent of the row entering the lane, needed if that row closes here
-      // (issued now so its latency overlaps the slot loop and the scan)
-      const int tin = (lu >= 0 && in_u >= 0) ? ldg(F + in_u) : -1;
-#else
-      const int tin = -1;
-#endif
+      // then every active slot does N[target] <-min value (the stochastic
+      // N[F[target]] <-min value is deferred to the vertex pass).
       int cu = in_u, cgu = in_gu, run = INF, pre = INF;
       bool seen = false;
       unsigned act = 0, hubm = 0;
@@ -866,27 +828,17 @@ __global__ void __launch_bounds__(HOOK_THREADS, 1) k_hook(HookArgs a) {
         run = h ? INF : min(run, val[j]);
       }
       if (act && !(FSV_SOL & 1)) {
-        int t[EPL];
 #pragma unroll
         for (int j = 0; j < EPL; ++j) {
-          t[j] = -1;
           if ((act >> j) & 1u) {
             if (HUBS && ((hubm >> j) & 1u)) {
               if (w[j] < HOT_ACC) red_min_shared(s_acc + 4u * (uint32_t)w[j], y[j]);
               else red_min(hub_acc + acc_at(w[j]), y[j]);
             } else {
               red_min(N + w[j], y[j]);
-              t[j] = ldg(F + w[j]);
             }
           }
         }
-        // the stochastic hook of these emissions is not filtered by gf[t]:
-        // they already passed the aggressive filter, and the extra gather
-        // cost more than the no-op reductions it saves (config 2 hook
-        // 241 -> 230 us; configs 3-4 unchanged)
-#pragma unroll
-        for (int j = 0; j < EPL; ++j)
-          if (t[j] >= 0 && t[j] != w[j]) red_min(N + t[j], y[j]);
       }
 #if FSV_DENSE_LANES > 0
       if (HUBS) dense = __popc(__ballot_sync(0xffffffffu, act != 0)) >= FSV_DENSE_LANES;
@@ -905,7 +857,7 @@ __global__ void __launch_bounds__(HOOK_THREADS, 1) k_hook(HookArgs a) {
       const int cin = (lane == 0) ? carry_run : (ef ? ev : min(ev, carry_run));
       if (seen) {
         const int v = min(cin, pre);
-        if (v < in_gu) emit_row_t(in_u, v, tin, F, G, N);  // row entering the lane closes here
+        if (v < in_gu) red_min(N + in_u, v);  // row entering the lane closes here
       }
       const int lv = __shfl_sync(0xffffffffu, sv, 31);
       const int lf = __shfl_sync(0xffffffffu, sf, 31);
@@ -917,7 +869,7 @@ __global__ void __launch_bounds__(HOOK_THREADS, 1) k_hook(HookArgs a) {
       }
     }
     // the run still open at the span end: partial minimum of row carry_u
-    if (lane == 0 && carry_run < carry_gu) emit_row(carry_u, carry_gu, carry_run, F, G, N);
+    if (lane == 0) emit_agg(carry_u, carry_gu, carry_run, N);
     if constexpr (DYN) {
       if (++k < fixed) {
         s += nwarps;
@@ -951,7 +903,7 @@ __global__ void __launch_bounds__(HOOK_THREADS, 1) k_hook(HookArgs a) {
       const int acc = __ldcg(hub_acc + acc_at(s));
       if (acc == INF) continue;
       hub_acc[acc_at(s)] = INF;
-      emit_row(ldg(a.hub_id + s), ldg(a.G_hub + s), acc, F, G, N);
+      emit_agg(ldg(a.hub_id + s), ldg(a.G_hub + s), acc, N);
     }
 #endif
   }
@@ -962,13 +914,11 @@ __global__ void __launch_bounds__(HOOK_THREADS, 1) k_hook(HookArgs a) {
 // gf of slot s is G_hub[s] (compact, refreshed by the vertex pass), not a
 // random gather of G[hub_id[s]].
 __global__ void k_hubfix(int* __restrict__ hub_acc, const int* __restrict__ hub_id,
-                         const int* __restrict__ G_hub, int H, const int* __restrict__ F,
-                         const int* __restrict__ G, int* __restrict__ N, const int* done, const int* mode,
-                         int iter, const int* iterp, int* X, int* Y) {
+                         const int* __restrict__ G_hub, int H, int* __restrict__ N, const int* done,
+                         const int* mode, int iter, const int* iterp, int* X, int* Y) {
   if (__ldcg(done)) return;
   if (iterp) {   // graph mode: iteration and buffers from the device (loop_bufs)
     iter = __ldcg(iterp);
-    F = (iter & 1) ? X : Y;
     N = (iter & 1) ? Y : X;
   }
   if (mode[iter] != 0) return;
@@ -977,7 +927,7 @@ __global__ void k_hubfix(int* __restrict__ hub_acc, const int* __restrict__ hub_
     if (acc == INF) continue;
     hub_acc[acc_at(s)] = INF;
     const int h = ldg(hub_id + s);
-    emit_row(h, ldg(G_hub + s), acc, F, G, N);
+    emit_agg(h, ldg(G_hub + s), acc, N);
   }
 }
 
@@ -1172,10 +1122,78 @@ __global__ void __launch_bounds__(SC_THREADS, FSV_SC_MINB) k_shortcut(ShortcutAr
   const long long t0 = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & 31;
   const long long n4 = a.n >> 2;
-  const int* __restrict__ N = a.N;
   int4* F4 = reinterpret_cast<int4*>(a.F);
   int4* G4 = reinterpret_cast<int4*>(a.G);
   const int4* N4 = reinterpret_cast<const int4*>(a.N);
+  if (a.mode[a.iter] == 0) {
+    // Stochastic hooks of a dense iteration. The sweep only applied the
+    // aggressive hooks, so N[u] = min(gf[u], mngf[u]) here; a vertex it
+    // lowered (N[u] < gf[u], hence N[u] = mngf[u]) now hooks its parent:
+    // f[f_k[u]] <-min mngf[u] (kernels.py:110-118). BSP: every mngf[u] must
+    // be read before any N is lowered here, so pass A parks the lowered
+    // vertices' values in G (sign bit set; G[u] is only read by its own
+    // thread until the final pass rewrites it: a lowered vertex's gf always
+    // changes), a grid barrier follows (all blocks are resident: cooperative
+    // launch), pass B issues the reductions, and a second barrier precedes
+    // the grandparent gathers below.
+    unsigned touched = 0;   // bit j: the thread's j-th group holds a lowered vertex (j >= 31 share bit 31)
+    int j = 0;
+    for (long long i = t0; i < n4; i += stride, ++j) {
+      int4 nu;   // (L2 load: the final pass must not find a stale copy in L1)
+      asm volatile("ld.global.cg.v4.s32 {%0,%1,%2,%3}, [%4];"
+                   : "=r"(nu.x), "=r"(nu.y), "=r"(nu.z), "=r"(nu.w) : "l"(N4 + i));
+      int4 go = G4[i];
+      const bool lx = nu.x < go.x, ly = nu.y < go.y, lz = nu.z < go.z, lw = nu.w < go.w;
+      if (lx | ly | lz | lw) {
+        if (lx) go.x = nu.x | (int)0x80000000;
+        if (ly) go.y = nu.y | (int)0x80000000;
+        if (lz) go.z = nu.z | (int)0x80000000;
+        if (lw) go.w = nu.w | (int)0x80000000;
+        G4[i] = go;
+        touched |= 1u << min(j, 31);
+      }
+    }
+    int tail_val = -1;   // the scalar tail (n % 4 vertices): its values stay in a register
+    if (t0 < (a.n & 3)) {
+      const long long u = (n4 << 2) + t0;
+      const int nu = __ldcg(a.N + u);
+      if (nu < a.G[u]) tail_val = nu;
+    }
+    unsigned* bar = reinterpret_cast<unsigned*>(a.cnt + C_SCBAR);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      atomicAdd(bar, 1u);
+      while (*(volatile unsigned*)bar < gridDim.x) __nanosleep(32);
+      __threadfence();
+    }
+    __syncthreads();
+    j = 0;
+    for (long long i = t0; i < n4; i += stride, ++j) {
+      if (!((touched >> min(j, 31)) & 1u)) continue;
+      const int4 go = G4[i], fo = F4[i];
+      const int u = (int)(i << 2);
+      if (go.x < 0 && fo.x != u) red_min(a.N + fo.x, go.x & 0x7fffffff);
+      if (go.y < 0 && fo.y != u + 1) red_min(a.N + fo.y, go.y & 0x7fffffff);
+      if (go.z < 0 && fo.z != u + 2) red_min(a.N + fo.z, go.z & 0x7fffffff);
+      if (go.w < 0 && fo.w != u + 3) red_min(a.N + fo.w, go.w & 0x7fffffff);
+    }
+    if (tail_val >= 0) {
+      const long long u = (n4 << 2) + t0;
+      const int fo = a.F[u];
+      if (fo != (int)u) red_min(a.N + fo, tail_val);
+    }
+    bar = reinterpret_cast<unsigned*>(a.cnt + C_SCBAR2);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      atomicAdd(bar, 1u);
+      while (*(volatile unsigned*)bar < gridDim.x) __nanosleep(32);
+      __threadfence();
+    }
+    __syncthreads();
+  }
+  const int* __restrict__ N = a.N;
   // warp gw handles groups [wb, wb+32) of every stride: its delta region is private
   const long long gwarp = t0 >> 5;
   int* region = a.dl.list + gwarp * a.dl.rcap;

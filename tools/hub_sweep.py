@@ -7,7 +7,7 @@ from paper_1910_05971_b200 import generators as gen
 cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 2
 n, pairs = gen.baseline_graph(cfg)
 g = fb.build_csr(n, pairs)
-for H in (32768, 40960, 49152, 53248, 57344, 32768, 49152, 57344):
+for H in (24576, 32768, 40960, 47104, 49152, 51200, 53248, 57344):
     s = fb.Solver(0, hub_slots=H)
     s.upload(g)
     ts = [s.solve().solve_ms for _ in range(5)]
