@@ -103,7 +103,9 @@ int fsv_create(int device, fsv_ctx** out);
 int fsv_destroy(fsv_ctx* ctx);
 
 /* Hub table size used by the NEXT upload: <0 = no hubs, 0 = auto
- * (top-degree vertices up to 55296 shared-memory slots), >0 = at most that. */
+ * (top-degree vertices up to 47104 shared-memory slots: 192 KB with the hot
+ * accumulators, which keeps enough L1 for the global gathers), >0 = at most
+ * that, up to 55296. */
 int fsv_set_hub_slots(fsv_ctx* ctx, int slots);
 
 /* Column-range tiling of the NEXT upload's layout, for graphs without a

@@ -143,6 +143,13 @@ struct DBuf {
 
 // hub table + hot accumulators within the 227 KB opt-in shared memory
 static constexpr int kHubMax = (SMEM_OPTIN_INTS - HOT_ACC) / 1024 * 1024;
+// Default table: 192 KB of shared memory with the hot accumulators. Above
+// that the carve-out leaves ~28 KB of L1 and the random global gathers of the
+// sweep and the push run at half rate (tools/gather_smem_probe.cu: 139 vs
+// 250 G gathers/s); the 8 K least connected hubs are worth less than that
+// (config 2: 0.533 -> 0.523 ms, push 42 -> 31 us).
+static constexpr int kHubAuto = 192 * 1024 / (int)sizeof(int) - HOT_ACC;
+static_assert(kHubAuto <= kHubMax && kHubAuto % 4 == 0, "default hub table size");
 static constexpr int kHubMinDegree = 32;  // below this a hub slot buys nothing
 static constexpr long long kTierMinN = 1LL << 23;   // rank tier only when the vectors overflow L2
 #ifndef FSV_TIER_MIN_DEG
@@ -265,7 +272,7 @@ struct fsv_ctx {
     long long count = 0;
   } lab;
   int host_syncs = 0, launches = 0;
-  int hub_limit = kHubMax;
+  int hub_limit = kHubAuto;
   long long tile_width = 0;   // fsv_set_tile_width: 0 off, > 0 vertices per column tile, < 0 auto
   // device loop control + CUDA-graph (conditional WHILE) of the iteration loop
   DBuf<int> iterbuf;
@@ -1629,7 +1636,7 @@ extern "C" int fsv_set_tile_width(fsv_ctx* c, int64_t vertices) {
 
 extern "C" int fsv_set_hub_slots(fsv_ctx* c, int slots) {
   if (!c) return fail(FSV_ERR_CONTRACT, "NULL context");
-  c->hub_limit = slots < 0 ? -1 : (slots == 0 ? kHubMax : std::min(slots, kHubMax));
+  c->hub_limit = slots < 0 ? -1 : (slots == 0 ? kHubAuto : std::min(slots, kHubMax));
   return FSV_OK;
 }
 

@@ -1131,15 +1131,34 @@ __global__ void __launch_bounds__(SC_THREADS, FSV_SC_MINB) k_shortcut(ShortcutAr
     // lowered (N[u] < gf[u], hence N[u] = mngf[u]) now hooks its parent:
     // f[f_k[u]] <-min mngf[u] (kernels.py:110-118). BSP: every mngf[u] must
     // be read before any N is lowered here, so pass A parks the lowered
-    // vertices' values in G (sign bit set; G[u] is only read by its own
-    // thread until the final pass rewrites it: a lowered vertex's gf always
-    // changes), a grid barrier follows (all blocks are resident: cooperative
-    // launch), pass B issues the reductions, and a second barrier precedes
-    // the grandparent gathers below.
-    unsigned touched = 0;   // bit j: the thread's j-th group holds a lowered vertex (j >= 31 share bit 31)
+    // vertices' values (in registers, or in G with the sign bit set: G[u] is
+    // only read by its own thread until the final pass rewrites it, since a
+    // lowered vertex's gf always changes), a grid barrier follows (all blocks
+    // are resident: cooperative launch), pass B issues the reductions, and a
+    // second barrier precedes the grandparent gathers below.
+    // The first PARK groups of a thread stay in registers (every group when
+    // n <= 4 * PARK * threads, e.g. RMAT-22); only the rest go through G.
+    constexpr int PARK = 8;
+    int4 pk[PARK];
+#pragma unroll
+    for (int j = 0; j < PARK; ++j) {
+      const long long i = t0 + j * stride;
+      pk[j] = make_int4(-1, -1, -1, -1);
+      if (i < n4) {
+        int4 nu;   // (L2 load: the final pass must not find a stale copy in L1)
+        asm volatile("ld.global.cg.v4.s32 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(nu.x), "=r"(nu.y), "=r"(nu.z), "=r"(nu.w) : "l"(N4 + i));
+        const int4 go = G4[i];
+        pk[j].x = nu.x < go.x ? nu.x : -1;
+        pk[j].y = nu.y < go.y ? nu.y : -1;
+        pk[j].z = nu.z < go.z ? nu.z : -1;
+        pk[j].w = nu.w < go.w ? nu.w : -1;
+      }
+    }
+    unsigned touched = 0;   // bit j: the thread's (PARK + j)-th group holds a lowered vertex (j >= 31 share bit 31)
     int j = 0;
-    for (long long i = t0; i < n4; i += stride, ++j) {
-      int4 nu;   // (L2 load: the final pass must not find a stale copy in L1)
+    for (long long i = t0 + PARK * stride; i < n4; i += stride, ++j) {
+      int4 nu;
       asm volatile("ld.global.cg.v4.s32 {%0,%1,%2,%3}, [%4];"
                    : "=r"(nu.x), "=r"(nu.y), "=r"(nu.z), "=r"(nu.w) : "l"(N4 + i));
       int4 go = G4[i];
@@ -1168,8 +1187,20 @@ __global__ void __launch_bounds__(SC_THREADS, FSV_SC_MINB) k_shortcut(ShortcutAr
       __threadfence();
     }
     __syncthreads();
+#pragma unroll
+    for (int j2 = 0; j2 < PARK; ++j2) {
+      const int4 v = pk[j2];
+      if ((v.x & v.y & v.z & v.w) < 0) continue;   // all -1: nothing lowered in this group
+      const long long i = t0 + j2 * stride;
+      const int4 fo = F4[i];
+      const int u = (int)(i << 2);
+      if (v.x >= 0 && fo.x != u) red_min(a.N + fo.x, v.x);
+      if (v.y >= 0 && fo.y != u + 1) red_min(a.N + fo.y, v.y);
+      if (v.z >= 0 && fo.z != u + 2) red_min(a.N + fo.z, v.z);
+      if (v.w >= 0 && fo.w != u + 3) red_min(a.N + fo.w, v.w);
+    }
     j = 0;
-    for (long long i = t0; i < n4; i += stride, ++j) {
+    for (long long i = t0 + PARK * stride; i < n4; i += stride, ++j) {
       if (!((touched >> min(j, 31)) & 1u)) continue;
       const int4 go = G4[i], fo = F4[i];
       const int u = (int)(i << 2);

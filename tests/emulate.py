@@ -9,11 +9,15 @@ logic and the collective semantics can be tested on CPU:
   iteration 1  f1[u] = min(u, smallest neighbour) from each rank's own rows,
              assembled with an allreduce-min (k_f1 + ncclAllReduce)
   iteration k>=2 on every rank, over its own oriented entries (k_hook):
-             row side    run-min of gf over the row  -> N[u], N[F[u]]
-             column side gf[row]                     -> N[v], N[F[v]]
-             each filtered by "value < gf_k[target]"; then allreduce-min of N
-             (ncclAllReduce ncclMin) and the replicated vertex pass
-             gf' = N[N] (k_shortcut) with the gf-stability stop rule.
+             row side    run-min of gf over the row  -> N[u]
+             column side gf[row]                     -> N[v]
+             each filtered by "value < gf_k[target]" (aggressive hooks); then
+             allreduce-min of N (ncclAllReduce ncclMin) and the replicated
+             vertex pass (k_shortcut): the deferred stochastic hooks
+             N[F[u]] <-min N[u] for every u the sweep lowered (N[u] < gf_k[u],
+             all values read before any is lowered), then gf' = N[N] with the
+             gf-stability stop rule. A sparse iteration (the library's push)
+             applies both hooks per contribution instead (N[u] and N[F[u]]).
 
 ``allreduce_min`` is injected so the same code runs single-process (identity)
 or across gloo ranks (torch.distributed.all_reduce with ReduceOp.MIN).
@@ -64,8 +68,10 @@ def _scatter_min(target, idx, vals):
         np.minimum.at(target, idx, vals)
 
 
-def hook(rows, cols, F, G, N):
-    """One rank's phase H over its oriented entries (N modified in place)."""
+def hook(rows, cols, F, G, N, stochastic=True):
+    """One rank's phase H over its oriented entries (N modified in place).
+    stochastic=False: aggressive hooks only (the dense sweep; the vertex pass
+    then runs deferred_stochastic)."""
     if rows.size == 0:
         return
     gv = G[cols]
@@ -77,16 +83,29 @@ def hook(rows, cols, F, G, N):
     ok = rmin < G[ru]
     u, val = ru[ok], rmin[ok]
     _scatter_min(N, u, val)
-    t = F[u]
-    ok2 = (t != u) & (val < G[t])
-    _scatter_min(N, t[ok2], val[ok2])
+    if stochastic:
+        t = F[u]
+        ok2 = (t != u) & (val < G[t])
+        _scatter_min(N, t[ok2], val[ok2])
     # column side: v <- gf[row]
     ok = gu < gv
     v, val = cols[ok], gu[ok]
     _scatter_min(N, v, val)
-    t = F[v]
-    ok2 = (t != v) & (val < G[t])
-    _scatter_min(N, t[ok2], val[ok2])
+    if stochastic:
+        t = F[v]
+        ok2 = (t != v) & (val < G[t])
+        _scatter_min(N, t[ok2], val[ok2])
+
+
+def deferred_stochastic(F, G, N):
+    """The vertex pass's first step after a dense sweep (k_shortcut): every
+    vertex the aggressive hooks lowered hooks its parent with its new value,
+    all values read before any reduction lands."""
+    u = np.flatnonzero(N < G)
+    val = N[u].copy()
+    t = F[u]
+    ok = t != u
+    _scatter_min(N, t[ok], val[ok])
 
 
 def delta_exchange(N, G, allgather_pairs, nranks):
@@ -122,8 +141,8 @@ def run(n, offsets, cols, row_begin=0, row_end=None, allreduce_min=lambda a: a,
     while gfc[-1] != 0 and it < cap:
         it += 1
         N = G.copy()                     # f_k initialised to gf_{k-1} (shortcut folded)
-        hook(rows, ocols, F, G, N)
         sparse = gfc[-1] < threshold * n
+        hook(rows, ocols, F, G, N, stochastic=sparse)
         merged = None
         if allgather_pairs is not None and sparse:
             merged, sent = delta_exchange(N, G, allgather_pairs, nranks)
@@ -136,6 +155,8 @@ def run(n, offsets, cols, row_begin=0, row_end=None, allreduce_min=lambda a: a,
             N = allreduce_min(N)
             if stats is not None:
                 stats["dense"] = stats.get("dense", 0) + 1
+        if not sparse:
+            deferred_stochastic(F, G, N)
         G2 = N[N]
         gfc.append(int(np.count_nonzero(G2 != G)))
         fc.append(int(np.count_nonzero(N != F)))
