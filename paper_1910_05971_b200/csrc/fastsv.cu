@@ -150,6 +150,11 @@ static constexpr int kHubMax = (SMEM_OPTIN_INTS - HOT_ACC) / 1024 * 1024;
 // (config 2: 0.533 -> 0.523 ms, push 42 -> 31 us).
 static constexpr int kHubAuto = 192 * 1024 / (int)sizeof(int) - HOT_ACC;
 static_assert(kHubAuto <= kHubMax && kHubAuto % 4 == 0, "default hub table size");
+// With the L2 rank tier (vectors over L2) the default table is smaller still:
+// the freed L1 (~124 KB) caches the most connected tier slots of the compact
+// G_hub, which the tier gathers in degree-rank order (config 5: 23.4 ms at
+// 47104 slots, 19.8 ms at 24576, 20.0 ms at 16384).
+static constexpr int kHubAutoTier = 24576;
 static constexpr int kHubMinDegree = 32;  // below this a hub slot buys nothing
 static constexpr long long kTierMinN = 1LL << 23;   // rank tier only when the vectors overflow L2
 #ifndef FSV_TIER_MIN_DEG
@@ -273,6 +278,7 @@ struct fsv_ctx {
   } lab;
   int host_syncs = 0, launches = 0;
   int hub_limit = kHubAuto;
+  bool hub_auto = true;        // default table size (smaller when the rank tier is used)
   long long tile_width = 0;   // fsv_set_tile_width: 0 off, > 0 vertices per column tile, < 0 auto
   // device loop control + CUDA-graph (conditional WHILE) of the iteration loop
   DBuf<int> iterbuf;
@@ -1322,7 +1328,10 @@ static int upload_impl(fsv_ctx* c, int64_t n, const int64_t* h_off_arr, const Co
     CUDA_TRY(cudaMemcpyAsync(&cnt_ge, d_bad.p + 1, sizeof cnt_ge, cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaStreamSynchronize(st));
     const long long t = std::min<long long>(cnt_ge, kTierMax) & ~3LL;
-    if (t > H) HT = (int)t;
+    if (t > H) {
+      HT = (int)t;
+      if (c->hub_auto) H = std::min(H, kHubAutoTier);
+    }
   }
   // column-range tiling (k_tile_pass, fsv_set_tile_width): no hub table, no
   // huge rows, vectors over one tile. Off by default: the tile passes cost
@@ -1637,6 +1646,7 @@ extern "C" int fsv_set_tile_width(fsv_ctx* c, int64_t vertices) {
 extern "C" int fsv_set_hub_slots(fsv_ctx* c, int slots) {
   if (!c) return fail(FSV_ERR_CONTRACT, "NULL context");
   c->hub_limit = slots < 0 ? -1 : (slots == 0 ? kHubAuto : std::min(slots, kHubMax));
+  c->hub_auto = slots == 0;
   return FSV_OK;
 }
 

@@ -108,6 +108,37 @@ __device__ __forceinline__ uint64_t policy_evict_first() {
 
 // Streamed once per iteration: evict first from L2 so the parent vectors
 // stay L2-resident. L1 may allocate: a lane's two 16-byte halves share sectors.
+// A lane's 8 entries of a step as one 256-bit load (sm_100): one request per
+// sector, and no L1 allocation (FSV_STREAM_NA) so the ~60 KB of L1 next to
+// the hub table stay with the gathers.
+#ifndef FSV_STREAM_V8
+#define FSV_STREAM_V8 1
+#endif
+#ifndef FSV_STREAM_NA
+#define FSV_STREAM_NA 1
+#endif
+struct Entries8 {
+  uint32_t c[8];
+};
+__device__ __forceinline__ Entries8 ld_stream8(const uint4* p, uint64_t pol) {
+  Entries8 r;
+#if FSV_STREAM_V8
+#if FSV_STREAM_NA
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8], %9;"
+#else
+  asm volatile("ld.global.nc.L2::cache_hint.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8], %9;"
+#endif
+               : "=r"(r.c[0]), "=r"(r.c[1]), "=r"(r.c[2]), "=r"(r.c[3]), "=r"(r.c[4]), "=r"(r.c[5]),
+                 "=r"(r.c[6]), "=r"(r.c[7]) : "l"(p), "l"(pol));
+#else
+  asm volatile("ld.global.nc.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=r"(r.c[0]), "=r"(r.c[1]), "=r"(r.c[2]), "=r"(r.c[3]) : "l"(p), "l"(pol));
+  asm volatile("ld.global.nc.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=r"(r.c[4]), "=r"(r.c[5]), "=r"(r.c[6]), "=r"(r.c[7]) : "l"(p + 1), "l"(pol));
+#endif
+  return r;
+}
+
 __device__ __forceinline__ uint4 ld_stream(const uint4* p, uint64_t pol) {
   uint4 r;
   asm volatile("ld.global.nc.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
@@ -174,8 +205,13 @@ __device__ __forceinline__ void red_min_shared(uint32_t saddr, int v) {
 // ACC_SPREAD slots (the shared-memory hubs, whose accumulators take most of
 // the column-side reductions) one per STRIDE ints; tier slots beyond stay
 // packed.
+// Default 2: with packed slots (1) eight accumulators share a 32-byte sector,
+// the reductions aimed at them queue at the L2 slice that owns it, and the
+// dense hook's time depended on where the array sat in its 2 MB page (config
+// 2: 0.501-0.524 ms over FSV_HPAD/FSV_VPAD shifts); one slot per 8 bytes
+// gives 0.508-0.512 ms at every placement (4 and 8 the same, 32 slower).
 #ifndef FSV_ACC_STRIDE
-#define FSV_ACC_STRIDE 1
+#define FSV_ACC_STRIDE 2
 #endif
 constexpr int ACC_SPREAD = 65536;
 __host__ __device__ __forceinline__ long long acc_at(long long s) {
@@ -692,13 +728,12 @@ __global__ void __launch_bounds__(HOOK_THREADS, 1) k_hook(HookArgs a) {
     int carry_gu = carry_u >= 0 ? ldg(G + carry_u) : INF;
     int carry_run = INF;
     const uint4* p = reinterpret_cast<const uint4*>(a.ecol + (size_t)s * (NSTEP * STEP)) + 2 * lane;
-    uint4 n0 = ld_stream(p, pol), n1 = ld_stream(p + 1, pol);
+    Entries8 nx = ld_stream8(p, pol);
 #pragma unroll 1
     for (int st = 0; st < NSTEP; ++st) {
-      const uint32_t c[EPL] = {n0.x, n0.y, n0.z, n0.w, n1.x, n1.y, n1.z, n1.w};
+      const uint32_t c[EPL] = {nx.c[0], nx.c[1], nx.c[2], nx.c[3], nx.c[4], nx.c[5], nx.c[6], nx.c[7]};
       if (st + 1 < NSTEP) {
-        n0 = ld_stream(p + (st + 1) * 64, pol);
-        n1 = ld_stream(p + (st + 1) * 64 + 1, pol);
+        nx = ld_stream8(p + (st + 1) * 64, pol);
       }
       int val[EPL];
 #pragma unroll
