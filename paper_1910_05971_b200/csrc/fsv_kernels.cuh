@@ -218,6 +218,12 @@ __host__ __device__ __forceinline__ long long acc_at(long long s) {
   return FSV_ACC_STRIDE == 1 ? s
          : (s < ACC_SPREAD ? s * FSV_ACC_STRIDE : (long long)ACC_SPREAD * FSV_ACC_STRIDE + (s - ACC_SPREAD));
 }
+// Shared-memory hub slots (< H <= ACC_SPREAD) never reach the packed tail, so
+// the kernels without the rank tier index with one multiply.
+template <bool TIER>
+__device__ __forceinline__ long long acc_idx(int s) {
+  return TIER ? acc_at(s) : (long long)s * FSV_ACC_STRIDE;
+}
 __host__ __device__ __forceinline__ long long acc_len(long long slots) {
   return slots <= 0 ? 0 : acc_at(slots - 1) + 1;
 }
@@ -812,13 +818,13 @@ __global__ void __launch_bounds__(HOOK_THREADS, 1) k_hook(HookArgs a) {
           const int x0 = (int)(rx0 & IDMASK), x1 = (int)(rx1 & IDMASK);
           if (h0) {
             if (x0 < HOT_ACC) red_min_shared(s_acc + 4u * (uint32_t)x0, ry0);
-            else red_min(hub_acc + acc_at(x0), ry0);
+            else red_min(hub_acc + acc_idx<TIER>(x0), ry0);
           } else {
             red_min(N + x0, ry0);
           }
           if (h1) {
             if (x1 < HOT_ACC) red_min_shared(s_acc + 4u * (uint32_t)x1, ry1);
-            else red_min(hub_acc + acc_at(x1), ry1);
+            else red_min(hub_acc + acc_idx<TIER>(x1), ry1);
           } else if (g1) {
             red_min(N + x1, ry1);
           }
@@ -868,7 +874,7 @@ __global__ void __launch_bounds__(HOOK_THREADS, 1) k_hook(HookArgs a) {
           if ((act >> j) & 1u) {
             if (HUBS && ((hubm >> j) & 1u)) {
               if (w[j] < HOT_ACC) red_min_shared(s_acc + 4u * (uint32_t)w[j], y[j]);
-              else red_min(hub_acc + acc_at(w[j]), y[j]);
+              else red_min(hub_acc + acc_idx<TIER>(w[j]), y[j]);
             } else {
               red_min(N + w[j], y[j]);
             }
@@ -921,7 +927,7 @@ __global__ void __launch_bounds__(HOOK_THREADS, 1) k_hook(HookArgs a) {
     __syncthreads();
     for (int i = threadIdx.x; i < HOT_ACC; i += blockDim.x) {
       const int v = s_hub[i];
-      if (v != INF) red_min(hub_acc + acc_at(i), v);
+      if (v != INF) red_min(hub_acc + (long long)i * FSV_ACC_STRIDE, v);   // (HOT_ACC <= ACC_SPREAD)
     }
 #if FSV_FUSE_HUBFIX
     // hub fix-up in the same launch: grid barrier (every CTA is resident),
