@@ -53,3 +53,36 @@ def test_partitioned_schedule_single_process():
                 snaps.append(F.copy())
             assert len(snaps) == c.iterations, (c.name, P)
             assert np.array_equal(np.stack(snaps), c.snapshots), (c.name, P)
+
+
+def test_deferred_stochastic_hooks_equal_inline_hooks():
+    """The dense sweep's aggressive-only hooks followed by the vertex pass's
+    deferred stochastic hooks (one per lowered vertex, every value read before
+    any lands) give the same f_{k+1} as hooking both targets per contribution,
+    in every iteration of every golden graph, also when the sweep is split over
+    ranks and merged by an elementwise min first."""
+    for c in load_suite()[::3]:
+        g = fb.build_csr(c.n, c.edges)
+        for P in (1, 3):
+            parts = [(c.n * r // P, c.n * (r + 1) // P) for r in range(P)]
+            rows_cols = [emulate.oriented_entries(c.n, g.row_offsets, g.col_indices, lo, hi)
+                         for lo, hi in parts]
+            f1 = np.min([emulate.first_parents(c.n, g.row_offsets, g.col_indices, lo, hi)
+                         for lo, hi in parts], axis=0)
+            F, G = f1.copy(), f1[f1]
+            k = 1
+            while np.any(G != (np.arange(c.n) if k == 1 else Gprev)):
+                inline, deferred = [], []
+                for rows, cols in rows_cols:
+                    a, b = G.copy(), G.copy()
+                    emulate.hook(rows, cols, F, G, a, stochastic=True)
+                    emulate.hook(rows, cols, F, G, b, stochastic=False)
+                    inline.append(a)
+                    deferred.append(b)
+                Na, Nb = np.min(inline, axis=0), np.min(deferred, axis=0)
+                emulate.deferred_stochastic(F, G, Nb)
+                assert np.array_equal(Na, Nb), (c.name, P, k)
+                assert np.array_equal(Na, c.snapshots[k]), (c.name, P, k)
+                Gprev, F, G = G, Na, Na[Na]
+                k += 1
+            assert k == c.iterations, (c.name, P)

@@ -171,6 +171,33 @@ def test_baseline_config_full_size(solver, index):
         assert np.array_equal(labels, oracle.uf_labels(n, pairs))
 
 
+@pytest.mark.parametrize("hub_slots", [55296, 24576, 4096])
+def test_config2_hub_table_sizes(solver, hub_slots):
+    """The hub table size is a performance knob (default 47,104 slots: 192 KB of
+    shared memory; 55,296 is the largest table, 24,576 the rank-tier default):
+    the result does not depend on it."""
+    rec = load_configs()[2]
+    n, pairs = gen.baseline_graph(2)
+    g = fb.build_csr(n, pairs)
+    solver.set_hub_slots(hub_slots)
+    solver.upload(g)
+    assert solver.stats.hub_slots == hub_slots
+    labels, iters, gfc, fc, ms, _ = solver.run()
+    solver.set_hub_slots(0)
+    assert iters == rec["iterations"]
+    assert gfc.tolist() == rec["gf_changed"] and fc.tolist() == rec["f_changed"]
+    assert gen.pairs_digest(labels) == rec["labels_digest"]
+
+
+def test_default_hub_table_keeps_l1(solver):
+    """Default table: 47,104 slots (with the hot accumulators 192 KB, below the
+    carve-out step that halves the random-gather rate)."""
+    n, pairs = gen.baseline_graph(2)
+    solver.set_hub_slots(0)
+    solver.upload(fb.build_csr(n, pairs))
+    assert solver.stats.hub_slots == 47104
+
+
 POLICY = {"auto": (3, 0.1), "auto_t1": (3, 1.0), "auto_t05": (3, 0.5), "sparse_only": (2, 0.1),
           "dense_only": (1, 0.1)}
 
