@@ -118,6 +118,15 @@ int fsv_set_hub_slots(fsv_ctx* ctx, int slots);
  * tile, < 0 = auto (8 M vertices = 32 MB slices). */
 int fsv_set_tile_width(fsv_ctx* ctx, int64_t vertices);
 
+/* Minority sweep (default on). In a dense iteration from the third on, of a
+ * hub-table layout held by one rank: when the vertices whose grandparent
+ * differs from that of the most connected vertex have a small degree sum
+ * (at most 1/16 of the stored directed entries), only the edges incident to
+ * them are visited (a push in both directions along their CSR rows) instead
+ * of sweeping every stored entry; an entry whose endpoints carry the same
+ * grandparent contributes nothing. Results are identical; 0 turns it off. */
+int fsv_set_minority_sweep(fsv_ctx* ctx, int enable);
+
 /* Use an external stream (e.g. torch.cuda.current_stream().cuda_stream);
  * 0 restores the context's own stream. */
 int fsv_set_stream(fsv_ctx* ctx, void* cuda_stream);

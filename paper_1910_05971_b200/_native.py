@@ -46,6 +46,7 @@ FASTSV_SYMBOLS = {
     "fsv_destroy": (c_int, [c_void_p]),
     "fsv_set_hub_slots": (c_int, [c_void_p, c_int]),
     "fsv_set_tile_width": (c_int, [c_void_p, c_int64]),
+    "fsv_set_minority_sweep": (c_int, [c_void_p, c_int]),
     "fsv_set_stream": (c_int, [c_void_p, c_void_p]),
     "fsv_upload_csr": (c_int, [c_void_p, c_int64, c_void_p, c_void_p, c_int64, c_int64]),
     "fsv_upload_csr64": (c_int, [c_void_p, c_int64, c_void_p, c_void_p, c_int64, c_int64]),

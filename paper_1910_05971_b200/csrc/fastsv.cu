@@ -175,6 +175,13 @@ static constexpr long long kTierMax = (long long)FSV_TIER_MAX_M << 20;   // 8M: 
 #define FSV_GRAPH_BODY 2
 #endif
 static constexpr int kTraceCap = 4096;    // iteration cap of the counter array
+// The minority sweep replaces a dense sweep when the listed vertices' degree
+// sum is at most 1/kMinorityDiv of the stored directed entries (it gathers
+// from global memory what the dense sweep mostly gathers from shared memory).
+#ifndef FSV_MINORITY_DIV
+#define FSV_MINORITY_DIV 16
+#endif
+static constexpr long long kMinorityDiv = FSV_MINORITY_DIV;
 
 struct fsv_ctx {
   int device = 0;
@@ -259,6 +266,7 @@ struct fsv_ctx {
   int hook_launches = 0;
   int policy = 0;
   double threshold = 0.1;
+  int minority = 1;           // fsv_set_minority_sweep
   std::vector<int> h_mode;
   // results of the last solve
   int iterations = 0;
@@ -1643,6 +1651,13 @@ extern "C" int fsv_set_tile_width(fsv_ctx* c, int64_t vertices) {
   return FSV_OK;
 }
 
+extern "C" int fsv_set_minority_sweep(fsv_ctx* c, int enable) {
+  if (!c) return fail(FSV_ERR_CONTRACT, "NULL context");
+  c->minority = enable != 0;
+  c->graph_dirty = true;
+  return FSV_OK;
+}
+
 extern "C" int fsv_set_hub_slots(fsv_ctx* c, int slots) {
   if (!c) return fail(FSV_ERR_CONTRACT, "NULL context");
   c->hub_limit = slots < 0 ? -1 : (slots == 0 ? kHubAuto : std::min(slots, kHubMax));
@@ -1937,6 +1952,14 @@ static int launch_hook(fsv_ctx* c, int k, bool graph) {
     a.fix_barrier = reinterpret_cast<unsigned*>(slot + C_FIXBAR);
     a.task_ctr = reinterpret_cast<unsigned*>(slot + C_SPANS);
     a.lc = lc;
+    // minority sweep: only when this context holds every row (one rank) — ranks
+    // would have to agree on the branch, and each only sees its own rows
+    a.n = c->n;
+    a.mlist = c->dlist.p; a.mcount = c->dcount.p;
+    a.off32 = c->off32 ? c->csr_off32.p : nullptr;
+    a.minority_thr = (c->minority && c->H && c->row_begin == 0 && c->row_end == c->n && !(c->comm && c->nranks > 1) &&
+                      (uintptr_t)c->offp % 16 == 0)   // (vector loads of a borrowed offset array)
+                         ? c->csr_local / kMinorityDiv : -1;
     // persistent, one CTA per SM; cooperative launch guarantees co-residency
     // for the grid barrier of the sparse (push) path
     pmark(c, k, 0);
@@ -2186,7 +2209,7 @@ static std::vector<long long> graph_key(const fsv_ctx* c) {
           P(c->hacc), P(c->hub_id.p), P(c->done.p), P(c->mode.p), P(c->dlist.p), P(c->dcount.p), c->rcap,
           c->dgrid, P(c->offp), P(c->colsp), c->col_base, c->row_begin, c->row_end, P(c->cnt.p),
           P(c->chunks.p), P(c->iterbuf.p), P(c->tstamp.p), P(c->ticket.p), P(c->partials.p), c->n,
-          c->sm_count, P(c->comm)};
+          c->sm_count, P(c->comm), c->minority, P(c->off32 ? c->csr_off32.p : nullptr)};
 }
 
 // Builds (or reuses) the CUDA graph of the iteration loop: one conditional

@@ -73,7 +73,7 @@ constexpr int STEP = 32 * EPL;           // entries per warp step
 constexpr int STEPS = FSV_STEPS;         // steps per span
 constexpr int SPAN = STEP * STEPS;       // entries per warp task
 constexpr int HOOK_THREADS = FSV_HOOK_THREADS;
-constexpr int PUSH_SCRATCH_BYTES = HOOK_THREADS * 36;  // s_start, s_excl (8 B), s_val (4 B), s_list (16 B)
+constexpr int PUSH_SCRATCH_BYTES = HOOK_THREADS * 40;  // s_start, s_excl (8 B), s_val, s_src (4 B), s_list (16 B)
 // Column-side minima aimed at the HOT_ACC most connected hubs are combined in
 // shared memory per CTA and flushed once at the end: a top hub can be the
 // target of ~1e5 reductions per iteration, which would otherwise serialise
@@ -96,7 +96,8 @@ enum { C_GF = 0, C_F = 1, C_NONSTAR = 2, C_ROOTS = 3, C_VIOL = 4,   // vertex-pa
        C_FLOPS = 5, C_CHUNKS = 6, C_BARRIER = 8,       // push bookkeeping
        C_FIXBAR = 9,                                   // hub fix-up barrier of the dense hook
        C_SPANS = 10,                                   // dynamic task counter of the dense hook
-       C_SCBAR = 11, C_SCBAR2 = 12 };                  // grid barriers of the vertex pass (deferred hooks)
+       C_SCBAR = 11, C_SCBAR2 = 12,                    // grid barriers of the vertex pass (deferred hooks)
+       C_MDEG = 13, C_MBAR = 14 };                     // minority sweep: degree sum of the listed vertices, barrier
 
 // ---- memory helpers -------------------------------------------------------
 
@@ -292,9 +293,9 @@ __device__ __forceinline__ bool converged_exit(const int* done, const LoopCtl& l
 // global list. Phase B (after a grid barrier) pushes the chunks, one warp per
 // chunk, so a high-degree vertex is spread over the whole GPU.
 struct PushChunk {
-  long long pos;     // first column index of the chunk (rank-local)
-  int cnt;           // entries in the chunk (<= PUSH_BCHUNK)
+  long long pos_cnt; // first column index of the chunk (rank-local, < 2^48) | entries in the chunk << 48
   int val;           // gf[v] pushed to every neighbour
+  int src;           // v itself (the minority sweep pulls the neighbours' gf back into N[v])
 };
 
 struct PushArgs {
@@ -336,6 +337,12 @@ struct HookArgs {
   int iter;
   PushArgs push;
   LoopCtl lc;
+  // minority sweep (hub-table layouts, one rank): see hook_minority
+  long long n;            // vertices
+  int* mlist;             // the vertex pass's delta regions, free during a dense hook
+  int* mcount;
+  const int* off32;       // int32 copy of the CSR offsets when they fit, else null
+  long long minority_thr; // degree sum up to which the minority sweep replaces the dense sweep (< 0: off)
 };
 
 // Changed-gf ("delta") list written by the vertex pass: warp w owns
@@ -454,13 +461,24 @@ static_assert(PUSH_BCHUNK % 32 == 0 && PUSH_BIG <= 8192, "push chunk shapes");
 // a pushed vertex receives the same value, and their parents are often one
 // root, so unfiltered reductions would pile onto one address. All loads of
 // the lane are issued together.
-template <int PER>
-__device__ __forceinline__ void push_entries(const int (&u)[PER], const int (&val)[PER],
+// BIDIR (minority sweep of a dense iteration): the neighbour's gf is also
+// pulled back into the source vertex, N[src] <-min gf[u], and only the
+// aggressive hooks are applied (the vertex pass defers the stochastic ones).
+template <int PER, bool BIDIR>
+__device__ __forceinline__ void push_entries(const int (&u)[PER], const int (&val)[PER], const int (&src)[PER],
                                              const int* __restrict__ F, const int* __restrict__ G,
                                              int* __restrict__ N) {
   int gt[PER], t[PER];
 #pragma unroll
   for (int j = 0; j < PER; ++j) gt[j] = u[j] >= 0 ? ldg(G + u[j]) : INF;
+  if (BIDIR) {
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {
+      if (u[j] >= 0 && val[j] < gt[j]) red_min(N + u[j], val[j]);
+      if (u[j] >= 0 && gt[j] < val[j]) red_min(N + src[j], gt[j]);
+    }
+    return;
+  }
 #pragma unroll
   for (int j = 0; j < PER; ++j) {
     t[j] = -1;
@@ -480,8 +498,9 @@ __device__ __forceinline__ void push_entries(const int (&u)[PER], const int (&va
 }
 
 // Phase A. w_start/w_excl/w_val: this warp's shared scratch (32 entries each).
+template <bool BIDIR>
 __device__ __forceinline__ void push_local(const PushArgs& a, long long* w_start, long long* w_excl,
-                                           int* w_val, int* w_list) {
+                                           int* w_val, int* w_src, int* w_list) {
   const int lane = threadIdx.x & 31;
   const long long nw = (long long)gridDim.x * (blockDim.x >> 5);
   constexpr int PER = PUSH_CHUNK / 32;
@@ -517,9 +536,10 @@ __device__ __forceinline__ void push_local(const PushArgs& a, long long* w_start
 #endif
     for (int b = 0; b < cnt; b += 32) {
       long long deg = 0, start = 0;
-      int gv = INF;
+      int gv = INF, vs = 0;
       if (b + lane < cnt) {
         const int v = reg[b + lane];
+        vs = v;
         if (v >= a.row_begin && v < a.row_end) {
           const long long o0 = a.off[v];
           start = o0 - a.col_base;
@@ -536,15 +556,16 @@ __device__ __forceinline__ void push_local(const PushArgs& a, long long* w_start
         const long long bs = __shfl_sync(0xffffffffu, start, src);
         const long long bd = __shfl_sync(0xffffffffu, deg, src);
         const int bv = __shfl_sync(0xffffffffu, gv, src);
+        const int bsrc = __shfl_sync(0xffffffffu, vs, src);
         const long long nck = (bd + PUSH_BCHUNK - 1) / PUSH_BCHUNK;
         unsigned long long base = 0;
         if (lane == 0) base = atomicAdd(a.nchunks, (unsigned long long)nck);
         base = __shfl_sync(0xffffffffu, base, 0);
         for (long long q = lane; q < nck; q += 32) {
           PushChunk ck;
-          ck.pos = bs + q * PUSH_BCHUNK;
-          ck.cnt = (int)min((long long)PUSH_BCHUNK, bd - q * PUSH_BCHUNK);
+          ck.pos_cnt = (bs + q * PUSH_BCHUNK) | (min((long long)PUSH_BCHUNK, bd - q * PUSH_BCHUNK) << 48);
           ck.val = bv;
+          ck.src = bsrc;
           a.chunks[base + q] = ck;
         }
       }
@@ -561,22 +582,25 @@ __device__ __forceinline__ void push_local(const PushArgs& a, long long* w_start
       w_start[lane] = start;
       w_excl[lane] = incl - deg;
       w_val[lane] = gv;
+      w_src[lane] = vs;
       __syncwarp();
       int o = 0;   // owner of the lane's current entry (monotone in e)
       for (long long e0 = 0; e0 < T; e0 += PUSH_CHUNK) {
-        int u[PER], val[PER];
+        int u[PER], val[PER], sv[PER];
 #pragma unroll
         for (int j = 0; j < PER; ++j) {
           const long long e = e0 + lane + 32 * j;
           u[j] = -1;
           val[j] = INF;
+          sv[j] = 0;
           if (e < T) {
             while (o < 31 && w_excl[o + 1] <= e) ++o;
             u[j] = ldg(a.cols + w_start[o] + (e - w_excl[o]));
             val[j] = w_val[o];
+            if (BIDIR) sv[j] = w_src[o];
           }
         }
-        push_entries<PER>(u, val, a.F, a.G, a.N);
+        push_entries<PER, BIDIR>(u, val, sv, a.F, a.G, a.N);
       }
       __syncwarp();
     }
@@ -591,6 +615,7 @@ __device__ __forceinline__ void push_local(const PushArgs& a, long long* w_start
 }
 
 // Phase B: one warp per long-row chunk, contiguous columns.
+template <bool BIDIR>
 __device__ __forceinline__ void push_big(const PushArgs& a) {
   const int lane = threadIdx.x & 31;
   const unsigned long long total = __ldcg(a.nchunks);   // written before the grid barrier (L2)
@@ -599,14 +624,17 @@ __device__ __forceinline__ void push_big(const PushArgs& a) {
   for (long long q = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
        q < (long long)total; q += nw) {
     const PushChunk ck = a.chunks[q];
-    int u[PER], val[PER];
+    const long long pos = ck.pos_cnt & ((1LL << 48) - 1);
+    const int cnt = (int)(ck.pos_cnt >> 48);
+    int u[PER], val[PER], sv[PER];
 #pragma unroll
     for (int j = 0; j < PER; ++j) {
       const int e = lane + 32 * j;
-      u[j] = e < ck.cnt ? ldg(a.cols + ck.pos + e) : -1;
+      u[j] = e < cnt ? ldg(a.cols + pos + e) : -1;
       val[j] = ck.val;
+      sv[j] = ck.src;
     }
-    push_entries<PER>(u, val, a.F, a.G, a.N);
+    push_entries<PER, BIDIR>(u, val, sv, a.F, a.G, a.N);
   }
 }
 
@@ -647,6 +675,126 @@ __device__ __forceinline__ int gather_gf_tier(uint32_t c, uint32_t s_base, const
 // differs and no carried minimum is pending, the whole step is a no-op apart
 // from carry bookkeeping — the common case once components have converged.
 
+// The push over the listed vertices: phase A, grid barrier (every CTA is
+// resident: one persistent CTA per SM), phase B. The scratch aliases the hub
+// table in dynamic shared memory.
+template <bool BIDIR>
+__device__ __forceinline__ void hook_push(const HookArgs& a, int* s_hub) {
+  long long* s_start = reinterpret_cast<long long*>(s_hub);
+  long long* s_excl = s_start + HOOK_THREADS;
+  int* s_val = reinterpret_cast<int*>(s_excl + HOOK_THREADS);
+  int* s_src = s_val + HOOK_THREADS;
+  int* s_list = s_src + HOOK_THREADS;            // 128 expanded vertices per warp
+  const int wib = threadIdx.x >> 5;
+  DBG_T(0);
+  push_local<BIDIR>(a.push, s_start + wib * 32, s_excl + wib * 32, s_val + wib * 32, s_src + wib * 32,
+                    s_list + wib * 128);
+  __syncthreads();
+  DBG_T(1);
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(a.push.barrier, 1u);
+    while (*(volatile unsigned*)a.push.barrier < gridDim.x) __nanosleep(64);
+    __threadfence();
+  }
+  __syncthreads();
+  DBG_T(2);
+  push_big<BIDIR>(a.push);
+#ifdef FSV_DEBUG_TIMING
+  __syncthreads();
+  DBG_T(3);
+#endif
+}
+
+// Minority sweep of a dense iteration. Once one component dominates, almost
+// every vertex carries the same grandparent r, and an entry can only
+// contribute when its endpoints' gf differ, i.e. when at least one endpoint
+// is outside that majority. So instead of sweeping every stored entry, list
+// the vertices with gf != r (r = gf of the most connected vertex, hub slot
+// 0) and push along their symmetric CSR rows in both directions: gf[x] to a
+// neighbour y with a larger gf, and gf[y] back into N[x] when it is smaller
+// (an edge between two listed vertices is visited twice, which a min
+// absorbs). This is the same set of aggressive hooks as the dense sweep
+// makes; the stochastic ones follow in the vertex pass either way. The lists
+// go into the vertex pass's delta regions (free during a dense hook, same
+// 4-vertex group format), with the degree sum of the listed vertices; all
+// CTAs then take the same branch: the push if the sum is at most
+// minority_thr, else the dense sweep. Returns true when the iteration is done.
+__device__ __forceinline__ bool hook_minority(const HookArgs& a, int* s_hub, int r, unsigned long long* mdeg,
+                                              unsigned* mbar) {
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u;
+  const int nwarps = gridDim.x * (blockDim.x >> 5);
+  const int gw = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const long long n4 = a.n >> 2, ngroups = (a.n + 3) >> 2;
+  const int nreg = a.push.nregions;
+  const long long gper = (ngroups + nreg - 1) / nreg;          // groups per region (<= rcap, see upload_impl)
+  const int4* G4 = reinterpret_cast<const int4*>(a.G);
+  unsigned long long dsum = 0;
+  for (int w = gw; w < nreg; w += nwarps) {
+    int* region = a.mlist + (long long)w * a.push.rcap;
+    int wo = 0;
+    const long long g0 = w * gper, g1 = min(g0 + gper, ngroups);
+    for (long long gb = g0; gb < g1; gb += 32) {
+      const long long g = gb + lane;
+      unsigned m4 = 0;
+      if (g < g1) {
+        // the group's gf values and degrees from vector loads; vertices
+        // without edges (most of a skewed graph's minority) are not listed
+        long long d0, d1, d2, d3;
+        if (g < n4) {
+          const int4 v = G4[g];
+          m4 = (v.x != r) | ((v.y != r) << 1) | ((v.z != r) << 2) | ((v.w != r) << 3);
+          if (a.off32) {
+            const int4 o = reinterpret_cast<const int4*>(a.off32)[g];
+            const int o4 = a.off32[(g << 2) + 4];
+            d0 = o.y - o.x; d1 = o.z - o.y; d2 = o.w - o.z; d3 = o4 - o.w;
+          } else {
+            const longlong2 oa = reinterpret_cast<const longlong2*>(a.push.off)[2 * g];
+            const longlong2 ob = reinterpret_cast<const longlong2*>(a.push.off)[2 * g + 1];
+            const long long o4 = a.push.off[(g << 2) + 4];
+            d0 = oa.y - oa.x; d1 = ob.x - oa.y; d2 = ob.y - ob.x; d3 = o4 - ob.y;
+          }
+        } else {
+          d0 = d1 = d2 = d3 = 0;
+          for (int j = 0; j < (int)(a.n & 3); ++j) {
+            const long long v = (g << 2) + j;
+            m4 |= (a.G[v] != r ? 1u : 0u) << j;
+            const long long d = a.push.off[v + 1] - a.push.off[v];
+            if (j == 0) d0 = d; else if (j == 1) d1 = d; else d2 = d;
+          }
+        }
+        m4 &= (d0 > 0 ? 1u : 0u) | (d1 > 0 ? 2u : 0u) | (d2 > 0 ? 4u : 0u) | (d3 > 0 ? 8u : 0u);
+        dsum += (unsigned long long)(((m4 & 1u) ? d0 : 0) + ((m4 & 2u) ? d1 : 0) + ((m4 & 4u) ? d2 : 0) +
+                                     ((m4 & 8u) ? d3 : 0));
+      }
+      const bool on = m4 != 0u;
+      const unsigned bal = __ballot_sync(0xffffffffu, on);
+      if (on) region[wo + __popc(bal & lt)] = (int)(((unsigned)g << 4) | m4);
+      wo += __popc(bal);
+    }
+    if (lane == 0) a.mcount[w] = wo;
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) dsum += __shfl_xor_sync(0xffffffffu, dsum, o);
+  if (lane == 0 && dsum) atomicAdd(mdeg, dsum);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(mbar, 1u);
+    while (*(volatile unsigned*)mbar < gridDim.x) __nanosleep(32);
+    __threadfence();
+  }
+  __syncthreads();
+#ifdef FSV_DEBUG_MINORITY
+  if (blockIdx.x == 0 && threadIdx.x == 0)
+    printf("[minority] iter %d r %d degree sum %llu thr %lld\n", a.iter, r, __ldcg(mdeg), a.minority_thr);
+#endif
+  if ((long long)__ldcg(mdeg) > a.minority_thr) return false;
+  hook_push<true>(a, s_hub);
+  return true;
+}
+
 // HUBS = false (no hub slots, H == 0) compiles the hub table, hub mask and
 // accumulators out; TIER (implies HUBS) adds the L2 rank tier gathers.
 template <bool HUBS, bool TIER, int NSTEP>
@@ -668,32 +816,14 @@ __global__ void __launch_bounds__(HOOK_THREADS, 1) k_hook(HookArgs a) {
     a.task_ctr = reinterpret_cast<unsigned*>(slot + C_SPANS);
   }
   if (a.mode[a.iter] == 1) {
-    // sparse iteration: push from the vertices whose gf changed; the push
-    // scratch aliases the (unused) hub table in dynamic shared memory
-    long long* s_start = reinterpret_cast<long long*>(s_hub);
-    long long* s_excl = s_start + HOOK_THREADS;
-    int* s_val = reinterpret_cast<int*>(s_excl + HOOK_THREADS);
-    int* s_list = s_val + HOOK_THREADS;            // 128 expanded vertices per warp
-    const int wib = threadIdx.x >> 5;
-    DBG_T(0);
-    push_local(a.push, s_start + wib * 32, s_excl + wib * 32, s_val + wib * 32, s_list + wib * 128);
-    // grid barrier: every CTA is resident (one persistent CTA per SM)
-    __syncthreads();
-    DBG_T(1);
-    if (threadIdx.x == 0) {
-      __threadfence();
-      atomicAdd(a.push.barrier, 1u);
-      while (*(volatile unsigned*)a.push.barrier < gridDim.x) __nanosleep(64);
-      __threadfence();
-    }
-    __syncthreads();
-    DBG_T(2);
-    push_big(a.push);
-#ifdef FSV_DEBUG_TIMING
-    __syncthreads();
-    DBG_T(3);
-#endif
+    hook_push<false>(a, s_hub);   // sparse iteration: push from the vertices whose gf changed
     return;
+  }
+  if (HUBS && a.minority_thr >= 0 && a.iter >= 3) {
+    // (iteration 2 follows the closed-form first iteration: no majority yet)
+    unsigned long long* slot = a.lc.cnt_base + (size_t)(a.iter - 1) * NCOUNT;
+    if (hook_minority(a, s_hub, __ldcg(a.G_hub), slot + C_MDEG, reinterpret_cast<unsigned*>(slot + C_MBAR)))
+      return;
   }
   // s_hub[0, HOT_ACC): this CTA's accumulator of the hottest hub slots;
   // s_hub[HOT_ACC, HOT_ACC + H): gf of the shared-memory hubs. Both bases are

@@ -147,6 +147,11 @@ class Solver:
     def set_hub_slots(self, slots: int) -> None:
         _check(self._lib.fsv_set_hub_slots(self._ctx, int(slots)))
 
+    def set_minority_sweep(self, enable: bool) -> None:
+        """Minority sweep of late dense iterations (fsv_set_minority_sweep;
+        default on, results identical either way)."""
+        _check(self._lib.fsv_set_minority_sweep(self._ctx, int(bool(enable))))
+
     def set_tile_width(self, vertices: int) -> None:
         """Column-range tiling of the next upload's layout (0 off, > 0 width,
         < 0 auto); pays off over repeated solves of hub-less graphs whose

@@ -181,9 +181,9 @@ def test_config2_hub_table_sizes(solver, hub_slots):
     g = fb.build_csr(n, pairs)
     solver.set_hub_slots(hub_slots)
     solver.upload(g)
-    assert solver.stats.hub_slots == hub_slots
     labels, iters, gfc, fc, ms, _ = solver.run()
     solver.set_hub_slots(0)
+    assert solver.stats.hub_slots == hub_slots
     assert iters == rec["iterations"]
     assert gfc.tolist() == rec["gf_changed"] and fc.tolist() == rec["f_changed"]
     assert gen.pairs_digest(labels) == rec["labels_digest"]
@@ -195,7 +195,47 @@ def test_default_hub_table_keeps_l1(solver):
     n, pairs = gen.baseline_graph(2)
     solver.set_hub_slots(0)
     solver.upload(fb.build_csr(n, pairs))
+    solver.solve()
     assert solver.stats.hub_slots == 47104
+
+
+@pytest.mark.parametrize("index", [1, 2])
+def test_minority_sweep_on_and_off(solver, index):
+    """The minority sweep of late dense iterations (fsv_set_minority_sweep)
+    visits only the edges at vertices outside the majority grandparent; the
+    trace and the labels are the reference's with it and without it."""
+    rec = load_configs()[index]
+    n, pairs = gen.baseline_graph(index)
+    solver.set_hub_slots(0)
+    solver.upload(fb.build_csr(n, pairs))
+    try:
+        for on in (False, True):
+            solver.set_minority_sweep(on)
+            for batch in (0, 1):      # graph loop and host loop
+                labels, iters, gfc, fc, ms, _ = solver.run(batch=batch)
+                assert iters == rec["iterations"], (on, batch)
+                assert gfc.tolist() == rec["gf_changed"] and fc.tolist() == rec["f_changed"], (on, batch)
+                assert gen.pairs_digest(labels) == rec["labels_digest"], (on, batch)
+    finally:
+        solver.set_minority_sweep(True)
+
+
+def test_minority_sweep_snapshots_on_skewed_graphs(solver):
+    """Every per-iteration parent vector with the minority sweep on (RMAT and
+    star-heavy graphs with a hub table, where a giant component dominates
+    from the third iteration)."""
+    for scale, ef, seed in ((14, 16, 3), (15, 8, 4), (16, 16, 5)):
+        n, pairs = gen.rmat(scale, ef, seed=seed)
+        g = fb.build_csr(n, pairs)
+        o = oracle.fastsv_csr(n, g.row_offsets, g.col_indices, snapshots=True)
+        for hub_slots in (0, 1024):
+            solver.set_hub_slots(hub_slots)
+            solver.upload(g)
+            for policy in (3, 1):     # auto and dense-only schedules
+                labels, iters, gfc, fc, ms, snaps = solver.run(snapshots=True, snap_cap=64, policy=policy)
+                assert iters == o.iterations and gfc.tolist() == o.gf_changed.tolist(), (scale, hub_slots, policy)
+                assert np.array_equal(snaps, o.snapshots), (scale, hub_slots, policy)
+    solver.set_hub_slots(0)
 
 
 POLICY = {"auto": (3, 0.1), "auto_t1": (3, 1.0), "auto_t05": (3, 0.5), "sparse_only": (2, 0.1),
