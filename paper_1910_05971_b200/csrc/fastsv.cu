@@ -1952,14 +1952,14 @@ static int launch_hook(fsv_ctx* c, int k, bool graph) {
     a.fix_barrier = reinterpret_cast<unsigned*>(slot + C_FIXBAR);
     a.task_ctr = reinterpret_cast<unsigned*>(slot + C_SPANS);
     a.lc = lc;
-    // minority sweep: only when this context holds every row (one rank) — ranks
-    // would have to agree on the branch, and each only sees its own rows
+    // minority sweep: every rank holds the whole gf vector and all row offsets,
+    // so each computes the same global degree sum and takes the same branch;
+    // a rank then pushes from the listed vertices of its own rows
     a.n = c->n;
     a.mlist = c->dlist.p; a.mcount = c->dcount.p;
     a.off32 = c->off32 ? c->csr_off32.p : nullptr;
-    a.minority_thr = (c->minority && c->H && c->row_begin == 0 && c->row_end == c->n && !(c->comm && c->nranks > 1) &&
-                      (uintptr_t)c->offp % 16 == 0)   // (vector loads of a borrowed offset array)
-                         ? c->csr_local / kMinorityDiv : -1;
+    a.minority_thr = (c->minority && c->H && (uintptr_t)c->offp % 16 == 0)   // (vector loads of a borrowed offset array)
+                         ? c->m_dir / kMinorityDiv : -1;
     // persistent, one CTA per SM; cooperative launch guarantees co-residency
     // for the grid barrier of the sparse (push) path
     pmark(c, k, 0);

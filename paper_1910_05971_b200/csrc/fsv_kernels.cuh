@@ -337,7 +337,7 @@ struct HookArgs {
   int iter;
   PushArgs push;
   LoopCtl lc;
-  // minority sweep (hub-table layouts, one rank): see hook_minority
+  // minority sweep (hub-table layouts): see hook_minority
   long long n;            // vertices
   int* mlist;             // the vertex pass's delta regions, free during a dense hook
   int* mcount;
@@ -719,7 +719,12 @@ __device__ __forceinline__ void hook_push(const HookArgs& a, int* s_hub) {
 // go into the vertex pass's delta regions (free during a dense hook, same
 // 4-vertex group format), with the degree sum of the listed vertices; all
 // CTAs then take the same branch: the push if the sum is at most
-// minority_thr, else the dense sweep. Returns true when the iteration is done.
+// minority_thr, else the dense sweep. Across ranks the gf vector and the row
+// offsets are replicated, so every rank lists the same vertices, computes
+// the same sum and takes the same branch, and pushes only from the listed
+// vertices of its own rows (each edge at a listed vertex is then visited by
+// the rank that owns that vertex's row). Returns true when the iteration is
+// done.
 __device__ __forceinline__ bool hook_minority(const HookArgs& a, int* s_hub, int r, unsigned long long* mdeg,
                                               unsigned* mbar) {
   const int lane = threadIdx.x & 31;

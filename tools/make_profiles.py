@@ -87,8 +87,8 @@ def full(path: Path, out: Path, config: int, n: int | None):
             rd = float(r[h.index("dram__bytes_read.sum")]) * 1e6
             wr = float(r[h.index("dram__bytes_write.sum")]) * 1e6
             inst = float(r[h.index("smsp__inst_executed.sum")])
-            if inst > 2e7:          # dense launches (sparse push launches are tiny)
-                traffic.append(rd + wr)
+            if inst > 8e6:          # launches of dense iterations: the sweep (> 9e7 instructions on
+                traffic.append(rd + wr)   # config 2) and the minority sweep (1e7); the sparse push has 6e6
     (out / "hook_full_summary.txt").write_text("\n".join(lines) + "\n")
     if traffic:
         rec = {"config": config, "n": n, "bytes_per_launch": sum(traffic) / len(traffic),
