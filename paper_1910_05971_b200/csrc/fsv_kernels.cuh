@@ -7,17 +7,22 @@
 //
 //   k_hook      edge-parallel over the oriented layout (each undirected edge
 //               stored once, in the row of its lower-(degree,id) endpoint):
-//               row side   mngf run-min -> N[u], N[F[u]]  (aggressive/stochastic)
-//               column side gf[u]       -> N[v], N[F[v]]  (same rules, v <- u)
+//               row side   mngf run-min -> N[u]   (aggressive hook)
+//               column side gf[u]       -> N[v]   (same rule, v <- u)
 //               gf of the top-H degree vertices ("hubs") is read from shared
 //               memory; column-side writes aimed at hubs are min-reduced into
 //               a compact hub accumulator instead of random N atomics, which
 //               the same launch applies after a grid barrier (hub fix-up;
 //               k_hubfix when built with FSV_FUSE_HUBFIX=0). A sparse
-//               iteration takes the push branch of the same kernel.
-//   k_shortcut  vertex-parallel: gf_{k+1} = N[N], change counters, star and
-//               monotonicity checks, next N init, hub gf refresh, and the
-//               device-side convergence flag (last-block ticket).
+//               iteration takes the push branch of the same kernel (both
+//               hooks per contribution), and a late dense iteration the
+//               minority sweep (hook_minority) when few vertices are left
+//               outside the majority grandparent.
+//   k_shortcut  vertex-parallel: after a dense sweep the deferred stochastic
+//               hooks N[F[u]] <-min N[u] of the lowered vertices, then
+//               gf_{k+1} = N[N], change counters, star and monotonicity
+//               checks, next N init, hub gf refresh, and the device-side
+//               convergence flag (last-block ticket).
 //
 // Iteration 1 is closed-form (F = G = id): f_1[u] = min(u, min neighbour id),
 // computed by every solve from the sorted CSR rows (k_f1_solve), so k_first
