@@ -490,6 +490,7 @@ def main():
             "config": {"workload": f"config{args.config} (BASELINE.json configs[{args.config - 1}])",
                        "n": n, "edges": n_edges, "m_dir": g.m, "iterations": iters,
                        "oriented_entries": int(st.oriented_entries), "hub_slots": int(st.hub_slots),
+                       "minority_sweep_iterations": int(st.minority_iterations),
                        "l2": "flushed between steps (256 MiB write + 256 MiB read, outside the timed events)",
                        "layout_tiles": args.tile,
                        "parallelism": f"edge-partition x{world}" if world > 1 else "single GPU"},

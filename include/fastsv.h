@@ -35,7 +35,7 @@ extern "C" {
 #define FSV_ERR_INVARIANT 3
 #define FSV_ERR_RUNTIME 4
 
-#define FSV_ABI_VERSION 4
+#define FSV_ABI_VERSION 5
 
 typedef struct fsv_ctx fsv_ctx;
 
@@ -92,6 +92,8 @@ typedef struct fsv_stats {
    * bus bytes 2(P-1)/P*4n; delta: 8 bytes per pair to each other rank) */
   int32_t dense_exchanges, delta_exchanges;
   int64_t exchange_bytes;
+  int32_t minority_iterations;  /* dense iterations that ran the minority sweep instead of the full sweep */
+  int32_t reserved;
 } fsv_stats;
 
 const char* fsv_last_error(void);

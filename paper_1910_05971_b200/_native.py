@@ -34,7 +34,8 @@ class FsvStats(ctypes.Structure):
                 ("hook_ms", c_float), ("hubfix_ms", c_float), ("shortcut_ms", c_float),
                 ("first_ms", c_float), ("allreduce_ms", c_float), ("push_ms", c_float),
                 ("hook_launches", c_int32), ("sparse_iterations", c_int32),
-                ("dense_exchanges", c_int32), ("delta_exchanges", c_int32), ("exchange_bytes", c_int64)]
+                ("dense_exchanges", c_int32), ("delta_exchanges", c_int32), ("exchange_bytes", c_int64),
+                ("minority_iterations", c_int32), ("reserved", c_int32)]
 
 
 # symbol -> (restype, argtypes); mirrors include/fastsv.h one to one

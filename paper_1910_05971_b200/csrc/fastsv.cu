@@ -2797,6 +2797,10 @@ static void fill_stats(fsv_ctx* c, fsv_stats* s) {
   int sp = 0;
   for (int k = 2; k <= c->iterations && k < (int)c->h_mode.size(); ++k) sp += c->h_mode[k] == 1;
   s->sparse_iterations = sp;
+  int mi = 0;
+  for (int k = 0; k < c->iterations && (size_t)(k + 1) * NCOUNT <= c->h_cnt.size(); ++k)
+    mi += c->h_cnt[(size_t)k * NCOUNT + C_MDONE] != 0;
+  s->minority_iterations = mi;
   s->dense_exchanges = c->dense_x;
   s->delta_exchanges = c->delta_x;
   s->exchange_bytes = c->xbytes;

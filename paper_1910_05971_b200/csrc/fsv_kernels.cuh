@@ -102,7 +102,8 @@ enum { C_GF = 0, C_F = 1, C_NONSTAR = 2, C_ROOTS = 3, C_VIOL = 4,   // vertex-pa
        C_FIXBAR = 9,                                   // hub fix-up barrier of the dense hook
        C_SPANS = 10,                                   // dynamic task counter of the dense hook
        C_SCBAR = 11, C_SCBAR2 = 12,                    // grid barriers of the vertex pass (deferred hooks)
-       C_MDEG = 13, C_MBAR = 14 };                     // minority sweep: degree sum of the listed vertices, barrier
+       C_MDEG = 13, C_MBAR = 14,                       // minority sweep: degree sum of the listed vertices, barrier,
+       C_MDONE = 15 };                                 // 1 when it replaced this iteration's dense sweep (stats)
 
 // ---- memory helpers -------------------------------------------------------
 
@@ -801,6 +802,7 @@ __device__ __forceinline__ bool hook_minority(const HookArgs& a, int* s_hub, int
     printf("[minority] iter %d r %d degree sum %llu thr %lld\n", a.iter, r, __ldcg(mdeg), a.minority_thr);
 #endif
   if ((long long)__ldcg(mdeg) > a.minority_thr) return false;
+  if (blockIdx.x == 0 && threadIdx.x == 0) mdeg[C_MDONE - C_MDEG] = 1ull;
   hook_push<true>(a, s_hub);
   return true;
 }

@@ -38,7 +38,7 @@ def test_graphgen_exports_every_declared_symbol():
 
 def test_abi_version_and_error_string():
     lib = _native.fastsv_lib()
-    assert lib.fsv_abi_version() == 4
+    assert lib.fsv_abi_version() == 5
     assert isinstance(_native.last_error(), str)
 
 

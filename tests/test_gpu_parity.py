@@ -216,6 +216,8 @@ def test_minority_sweep_on_and_off(solver, index):
                 assert iters == rec["iterations"], (on, batch)
                 assert gfc.tolist() == rec["gf_changed"] and fc.tolist() == rec["f_changed"], (on, batch)
                 assert gen.pairs_digest(labels) == rec["labels_digest"], (on, batch)
+                if index == 2:    # RMAT-22: the third iteration is the minority one
+                    assert solver.stats.minority_iterations == (1 if on else 0), (on, batch)
     finally:
         solver.set_minority_sweep(True)
 
@@ -224,8 +226,12 @@ def test_minority_sweep_snapshots_on_skewed_graphs(solver):
     """Every per-iteration parent vector with the minority sweep on (RMAT and
     star-heavy graphs with a hub table, where a giant component dominates
     from the third iteration)."""
-    for scale, ef, seed in ((14, 16, 3), (15, 8, 4), (16, 16, 5)):
+    took = 0
+    for scale, ef, seed in ((14, 16, 3), (15, 8, 4), (16, 16, 5), (15, 16, 6)):
         n, pairs = gen.rmat(scale, ef, seed=seed)
+        if seed == 6:   # n % 4 != 0: the scalar tail group of the minority list
+            pairs = np.concatenate([pairs, np.array([[n, n + 1], [n + 2, 5], [n + 1, 7]], dtype=np.int32)])
+            n += 3
         g = fb.build_csr(n, pairs)
         o = oracle.fastsv_csr(n, g.row_offsets, g.col_indices, snapshots=True)
         for hub_slots in (0, 1024):
@@ -235,7 +241,10 @@ def test_minority_sweep_snapshots_on_skewed_graphs(solver):
                 labels, iters, gfc, fc, ms, snaps = solver.run(snapshots=True, snap_cap=64, policy=policy)
                 assert iters == o.iterations and gfc.tolist() == o.gf_changed.tolist(), (scale, hub_slots, policy)
                 assert np.array_equal(snaps, o.snapshots), (scale, hub_slots, policy)
+            solver.solve()
+            took += solver.stats.minority_iterations
     solver.set_hub_slots(0)
+    assert took > 0       # (the sweep did run on these graphs)
 
 
 POLICY = {"auto": (3, 0.1), "auto_t1": (3, 1.0), "auto_t05": (3, 0.5), "sparse_only": (2, 0.1),
