@@ -470,7 +470,11 @@ static_assert(PUSH_BCHUNK % 32 == 0 && PUSH_BIG <= 8192, "push chunk shapes");
 // BIDIR (minority sweep of a dense iteration): the neighbour's gf is also
 // pulled back into the source vertex, N[src] <-min gf[u], and only the
 // aggressive hooks are applied (the vertex pass defers the stochastic ones).
-template <int PER, bool BIDIR>
+// ONE_SRC: the whole warp pushes one vertex's entries (a long-row chunk), so
+// the pull-back is one warp-reduced minimum: a straggler of degree 25,000
+// whose neighbours all carry the majority value would otherwise queue 25,000
+// reductions on the one address N[src].
+template <int PER, bool BIDIR, bool ONE_SRC = false>
 __device__ __forceinline__ void push_entries(const int (&u)[PER], const int (&val)[PER], const int (&src)[PER],
                                              const int* __restrict__ F, const int* __restrict__ G,
                                              int* __restrict__ N) {
@@ -478,10 +482,16 @@ __device__ __forceinline__ void push_entries(const int (&u)[PER], const int (&va
 #pragma unroll
   for (int j = 0; j < PER; ++j) gt[j] = u[j] >= 0 ? ldg(G + u[j]) : INF;
   if (BIDIR) {
+    int back = INF;
 #pragma unroll
     for (int j = 0; j < PER; ++j) {
       if (u[j] >= 0 && val[j] < gt[j]) red_min(N + u[j], val[j]);
-      if (u[j] >= 0 && gt[j] < val[j]) red_min(N + src[j], gt[j]);
+      if (ONE_SRC) back = min(back, gt[j]);
+      else if (u[j] >= 0 && gt[j] < val[j]) red_min(N + src[j], gt[j]);
+    }
+    if (ONE_SRC) {
+      back = __reduce_min_sync(0xffffffffu, back);
+      if ((threadIdx.x & 31) == 0 && back < val[0]) red_min(N + src[0], back);
     }
     return;
   }
@@ -640,7 +650,7 @@ __device__ __forceinline__ void push_big(const PushArgs& a) {
       val[j] = ck.val;
       sv[j] = ck.src;
     }
-    push_entries<PER, BIDIR>(u, val, sv, a.F, a.G, a.N);
+    push_entries<PER, BIDIR, true>(u, val, sv, a.F, a.G, a.N);
   }
 }
 
