@@ -337,6 +337,7 @@ class Solver:
                                                ctypes.byref(iters),
                                                gfc.ctypes.data, fc.ctypes.data,
                                                snap.ctypes.data if n else ctypes.c_void_p(1), cap))
+            _check(self._lib.fsv_get_stats(self._ctx, ctypes.byref(self.stats)))
         else:
             _check(self._lib.fsv_solve(self._ctx, ctypes.byref(cfg), ctypes.byref(self.stats)))
             iters.value = self.stats.iterations
