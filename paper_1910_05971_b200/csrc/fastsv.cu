@@ -1958,7 +1958,11 @@ static int launch_hook(fsv_ctx* c, int k, bool graph) {
     a.n = c->n;
     a.mlist = c->dlist.p; a.mcount = c->dcount.p;
     a.off32 = c->off32 ? c->csr_off32.p : nullptr;
-    a.minority_thr = (c->minority && c->H && (uintptr_t)c->offp % 16 == 0)   // (vector loads of a borrowed offset array)
+    // (a region must hold one entry per 4-vertex group of its share, which the
+    // delta regions' capacity guarantees; vector loads need a 16-byte aligned
+    // offset array, which a borrowed one may not be)
+    const long long gper = ((c->n + 3) / 4 + p.nregions - 1) / std::max(p.nregions, 1);
+    a.minority_thr = (c->minority && c->H && gper <= c->rcap && (uintptr_t)c->offp % 16 == 0)
                          ? c->m_dir / kMinorityDiv : -1;
     // persistent, one CTA per SM; cooperative launch guarantees co-residency
     // for the grid barrier of the sparse (push) path
