@@ -161,10 +161,10 @@ static constexpr long long kTierMinN = 1LL << 23;   // rank tier only when the v
 #define FSV_TIER_MIN_DEG 8
 #endif
 #ifndef FSV_TIER_MAX_M
-#define FSV_TIER_MAX_M 8
+#define FSV_TIER_MAX_M 4   // config 5: 1 M 17.5 ms, 2 M 15.3, 4 M 14.6, 8 M 14.9, 16 M 15.8 (every slot is refreshed per vertex pass)
 #endif
 static constexpr int kTierMinDegree = FSV_TIER_MIN_DEG;
-static constexpr long long kTierMax = (long long)FSV_TIER_MAX_M << 20;   // 8M: 32 MB of gf + 32 MB of accumulators
+static constexpr long long kTierMax = (long long)FSV_TIER_MAX_M << 20;   // 4M: 16 MB of gf + 16 MB of accumulators
 #ifndef FSV_SMALL_TASKS
 #define FSV_SMALL_TASKS 4
 #endif
