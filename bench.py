@@ -501,7 +501,11 @@ def main():
                          "traffic": traffic, "bytes_per_launch": hook_bytes,
                          "launch_ms": per_launch_ms, "launches": hook_launches,
                          "share_of_step": hook_ms / solve_ms_prof if solve_ms_prof else None,
-                         "step_breakdown_ms": kernel_ms, "profiled_step_ms": solve_ms_prof},
+                         "step_breakdown_ms": kernel_ms, "profiled_step_ms": solve_ms_prof,
+                         "note": "launches = k_hook launches of dense iterations (mean duration); "
+                                 f"{int(st.minority_iterations)} of them took the minority sweep, which visits only "
+                                 "the edges at vertices outside the majority grandparent and moves far less "
+                                 "than bytes_per_launch; per-launch split in DESIGN.md section 8"},
             "e2e": {"value": n_edges / (e2e_ms * 1e-3), "unit": "edges/s",
                     "ms_per_step": e2e_ms,
                     "h2d_copy_floor_ms": h2d_floor_ms,
